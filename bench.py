@@ -1,0 +1,404 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the arXiv 1711.04325 hot path on B200.
+
+One step = one synchronous data-parallel iteration after backward (all SURVEY
+section 8(a) rows): pack fp32 gradients to loss-scaled fp16, fp16 all-reduce with
+exact accumulation (N > 1), unpack + average, blended RMSprop/SGD update of the
+25,557,032-parameter ResNet-50 buffer (BASELINE.json configs[1] at N = 1,
+configs[2] at N = 2/4/8), schedule coefficients from the slow-start / RMSprop
+warm-up schedule of the 32k run.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lmsgd|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Prints ONE JSON line on rank 0.  value = whole-job update steps/s: global
+synchronous steps/s x N (every GPU applies the update to its replica of the
+buffer each step; per-GPU work is fixed as N grows: weak scaling).
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "update steps/s on 25.6M-param grad buffer at 1/2/4/8 B200; HBM & NVLink GB/s vs peak"
+UNIT = "steps/s"
+LOSS_SCALE = 1024.0
+UPDATE_BYTES_PER_ELEM = 26      # R (2) + theta, Delta, m read (12) + written (12)
+PACK_BYTES_PER_ELEM = 6         # g read (4) + fp16 write (2)
+FUSED_BYTES_PER_ELEM = 28       # g (4) + state read (12) + written (12)
+L2_BYTES = 126 * 2 ** 20
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=2000)
+    p.add_argument("--warmup", type=int, default=20)
+    p.add_argument("--impl", choices=["lmsgd", "reference"], default="lmsgd")
+    p.add_argument("--depth", type=int, default=50, choices=[50, 152])
+    p.add_argument("--mode", choices=["guarded", "fused"], default="guarded",
+                   help="N=1: guarded = pack + update with global non-finite skip (default); "
+                        "fused = single-pass pack+update (LMSGD_FLAG_NO_SKIP)")
+    p.add_argument("--t-start", type=int, default=1, help="first schedule step timed (1 = RMSprop warm-up)")
+    p.add_argument("--e2e-steps", type=int, default=50)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-profile", action="store_true", help="do not record per-kernel events")
+    return p.parse_args()
+
+
+def env_rank():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def committed_traffic(kernel: str):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(kernel)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks (NVML)
+
+class ClockSampler:
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
+               0x10: "sync_boost"}
+
+    def __init__(self, index: int, period_s: float = 0.01):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # noqa: BLE001
+            self.nv, self.err = None, str(e)
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = get_r(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(self.period)
+
+    def start(self):
+        if self.nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+
+    def stop(self):
+        if self._t:
+            self._stop.set()
+            self._t.join()
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+# ------------------------------------------------------------------ oracle timing (CPU)
+
+def oracle_rate(k: int, n_full: int, budget_s: float, max_elems: int = 1 << 21):
+    """Time the CPU oracle (as it stands) on slices of the workload; returns
+    (steps/s extrapolated to the full buffer, elems per timed call, calls, seconds)."""
+    import numpy as np
+
+    import synth
+    from oracle import exchange, schedule, update
+    ns = min(max_elems, n_full)
+    g = synth.grads(k, 1, ns)
+    th = synth.theta0(ns, None).astype(np.float64)
+    d = np.zeros(ns)
+    m = np.zeros(ns)
+    c = schedule.coeffs_at(1)
+    calls, t0 = 0, time.perf_counter()
+    while True:
+        ex = exchange.exchange(list(g), LOSS_SCALE)
+        th, d, m = update.step(th, ex.ghat, m, d, c.eta, c.alpha_sgd, c.alpha_rmsprop)
+        calls += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s:
+            break
+    return (ns * calls / el) / n_full, ns, calls, el
+
+
+def cpu_cores_used():
+    return 1   # NumPy elementwise ufuncs run on one thread
+
+
+def run_reference(args):
+    rank, world, _ = env_rank()
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import synth
+    from oracle import exchange, schedule, update
+    k = max(1, args.gpus)
+    n = synth.resnet_n_params(args.depth)
+    # calibrate the per-element cost, then size each step's slice so the run ends in ~3 min
+    rate, ns0, calls0, el0 = oracle_rate(k, n, 2.0, 1 << 18)
+    sec_per_elem = 1.0 / (rate * n)
+    total = args.steps + args.warmup
+    ns = int(max(4096, min(n, 1 << 21, 90.0 / total / sec_per_elem)))
+    g = synth.grads(k, 1, ns)
+    th = synth.theta0(ns, None).astype(np.float64)
+    d, m = np.zeros(ns), np.zeros(ns)
+    c = schedule.coeffs_at(1)
+
+    def one():
+        nonlocal th, d, m
+        ex = exchange.exchange(list(g), LOSS_SCALE)
+        th, d, m = update.step(th, ex.ghat, m, d, c.eta, c.alpha_sgd, c.alpha_rmsprop)
+
+    for _ in range(args.warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    el = time.perf_counter() - t0
+    steps_per_s = (ns * args.steps / el) / n * k        # whole-buffer update steps/s, x k workers
+    sample = (f"each step: oracle pack x{k} workers + exact fp64 reduce + fp16 wire + fp64 update on a "
+              f"{ns}-element slice of the {n}-param buffer; value extrapolated per element to the full buffer")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": steps_per_s, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3 * (n / ns),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (synth recipe, seeded)",
+        "config": {"workload": f"resnet{args.depth}_grad_buffer_k{k}", "n_params": n, "k": k,
+                   "loss_scale": LOSS_SCALE, "schedule_t": 1},
+        "cpu_baseline": {"value": steps_per_s, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": steps_per_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_1711_04325_b200 as L
+    import synth
+
+    rank, world, local = env_rank()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE {world}"
+    torch.cuda.set_device(local)
+    devc = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=devc)
+    n = synth.resnet_n_params(args.depth)
+    flags = L.LMSGD_FLAG_NO_SKIP if (args.mode == "fused" and world == 1) else 0
+    ctx = L.lmsgd_init(world, rank, local, n, LOSS_SCALE, None, flags)
+    L.connect_process_group(ctx)
+
+    # inputs, resident in HBM before timing (synthetic, paper-shaped; see synth / DESIGN.md)
+    gen = torch.Generator(device=devc)
+    gen.manual_seed(1711 + rank)
+    theta = torch.from_numpy(synth.theta0(n, args.depth)).to(devc)
+    a = 10.0 ** (torch.rand(n, generator=gen, device=devc) * 4.0 - 5.0)
+    gen_c = torch.Generator(device=devc)
+    gen_c.manual_seed(1711)
+    c_sig = torch.randn(n, generator=gen_c, device=devc)
+    grads = (a * (c_sig + torch.randn(n, generator=gen, device=devc) / 32 ** 0.5)).float().contiguous()
+    del a, c_sig
+    delta = torch.zeros(n, device=devc)
+    m = torch.zeros(n, device=devc)
+    cl = L.make_cluster()
+    T = L.lmsgd_schedule_steps(cl)
+    coeffs = [L.lmsgd_schedule_at(None, cl, (args.t_start - 1 + i) % T + 1) for i in range(args.warmup + args.steps)]
+    stream = torch.cuda.current_stream()
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    P = ctypes.c_void_p
+    ptrs = (P(theta.data_ptr()), P(grads.data_ptr()), P(delta.data_ptr()), P(m.data_ptr()))
+    lib = L.lib()
+
+    def step(i):
+        st = lib.lmsgd_step(ctx.ptr, sp, *ptrs, ctypes.byref(coeffs[i]))
+        if st != 0:
+            raise L.LmsgdError(st, lib.lmsgd_last_error(ctx.ptr).decode())
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=devc, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == 0, f"warm-up step status {code}"
+
+    kernels_per_step = 1 if flags else (2 if world == 1 else 3)
+    if not args.no_profile:
+        L.lmsgd_profile_enable(ctx, kernels_per_step * args.steps)
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(args.steps):
+        step(args.warmup + i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ck = clocks.stop()
+    ms = max_over_ranks(e0.elapsed_time(e1))
+    prof = L.lmsgd_profile_read(ctx) if not args.no_profile else {}
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == 0 and st.skipped == 0, f"timed step status {code}"
+
+    ms_per_step = ms / args.steps
+    global_steps_per_s = 1e3 / ms_per_step
+    value = global_steps_per_s * world
+
+    # per-kernel roofline (dominant kernel = the update; fused kernel when --mode fused)
+    peak, peak_src = measured_peaks()
+    phases = {}
+    for ph, (pms, cnt) in prof.items():
+        if cnt:
+            phases[ph] = {"us_per_launch": max_over_ranks(pms / cnt * 1e3), "launches": cnt}
+    if flags:
+        dom, dom_bytes, kname = "pack", FUSED_BYTES_PER_ELEM, "k_fused1"
+    else:
+        dom, dom_bytes, kname = "update", UPDATE_BYTES_PER_ELEM, "k_update" if world == 1 else "k_update_gather"
+    roofline = None
+    if dom in phases:
+        us = phases[dom]["us_per_launch"]
+        achieved = dom_bytes * n / (us * 1e-6) / 1e9
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": committed_traffic(kname),
+                    "algorithmic_bytes_per_launch": dom_bytes * n, "peak_source": peak_src,
+                    "share_of_step": us * 1e-3 / ms_per_step}
+    if "pack" in phases and not flags:
+        phases["pack"]["gbs_algorithmic"] = PACK_BYTES_PER_ELEM * n / (phases["pack"]["us_per_launch"] * 1e-6) / 1e9
+    if "update" in phases:
+        phases["update"]["gbs_algorithmic"] = UPDATE_BYTES_PER_ELEM * n / (phases["update"]["us_per_launch"] * 1e-6) / 1e9
+    nvlink = None
+    if world > 1:
+        n_pad = -(-n // (64 * world)) * 64 * world
+        bus_bytes = 2 * (2 * n_pad) * (world - 1) / world     # nccl-tests busbw convention, fp16 payload
+        nvlink = {"allreduce_bus_bytes_per_step": bus_bytes,
+                  "step_bus_gbs": bus_bytes / (ms_per_step * 1e-3) / 1e9, "peak_gbs_per_dir": 900.0,
+                  "measured_peer_gbs_per_dir": 770.0}
+        # yardstick: NCCL fp16 all-reduce of the same payload alone (not part of our path)
+        buf = torch.zeros(n_pad, dtype=torch.float16, device=devc)
+        for _ in range(5):
+            dist.all_reduce(buf)
+        torch.cuda.synchronize()
+        barrier()
+        y0, y1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        y0.record(stream)
+        for _ in range(20):
+            dist.all_reduce(buf)
+        y1.record(stream)
+        torch.cuda.synchronize()
+        nccl_ms = max_over_ranks(y0.elapsed_time(y1) / 20)
+        nvlink["nccl_fp16_allreduce_us"] = nccl_ms * 1e3
+        nvlink["nccl_fp16_allreduce_bus_gbs"] = bus_bytes / (nccl_ms * 1e-3) / 1e9
+        del buf
+
+    # e2e through the public host-buffer entry point: H2D of this step's gradient from
+    # pinned memory + the whole step + D2H of the step status, every step
+    g_host = grads.cpu().pin_memory()
+    st_host = torch.zeros(4, dtype=torch.int64).pin_memory()
+    gp, sh = P(g_host.data_ptr()), P(st_host.data_ptr())
+    ke = max(1, min(args.e2e_steps, args.steps))
+
+    def step_host(i):
+        s_ = lib.lmsgd_step_host(ctx.ptr, sp, ptrs[0], gp, ptrs[2], ptrs[3], ctypes.byref(coeffs[i % len(coeffs)]), sh)
+        if s_ != 0:
+            raise L.LmsgdError(s_, lib.lmsgd_last_error(ctx.ptr).decode())
+
+    for i in range(3):
+        step_host(i)
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for i in range(ke):
+        step_host(i)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / ke
+    e2e = {"value": world * 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 4 * n,
+           "d2h_bytes_per_step": ctypes.sizeof(L.StepStatus), "ms_per_step": e2e_ms, "steps": ke}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        rate, ns, calls, el = oracle_rate(1, n, 15.0)
+        cpu = {"value": rate, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
+               "sample": f"{calls} oracle steps (pack + exact reduce + fp16 wire + fp64 update, k=1) on a "
+                         f"{ns}-element slice of the {n}-param buffer in {el:.1f} s, extrapolated per element",
+               "host_cores_available": len(os.sched_getaffinity(0))}
+
+    if rank == 0:
+        inputs_bytes = n * (4 + 12)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (paper-shaped: ResNet layout, minibatch-32 noise)",
+            "config": {"workload": (f"resnet{args.depth}_grad_buffer_{'fused_pack_update_1gpu' if world == 1 else 'fp16_allreduce_update'}"
+                                    + (f"_{args.mode}" if world == 1 else "")),
+                       "n_params": n, "k": world, "wire": "f16", "loss_scale": LOSS_SCALE,
+                       "schedule": "slow-start 32k (n=1024, b_local=32), t from %d" % args.t_start,
+                       "l2": f"inputs {inputs_bytes / 1e9:.2f} GB > 126 MB L2 (no flush needed)",
+                       "global_steps_per_s": global_steps_per_s,
+                       "grad_elems_per_s": global_steps_per_s * world * n},
+            "roofline": roofline, "phases": phases, "nvlink": nvlink, "cpu_baseline": cpu, "e2e": e2e,
+            "clocks": ck, "gpu_launches": kernels_per_step * args.steps,
+        }
+        print(json.dumps(line), flush=True)
+    L.lmsgd_finalize(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

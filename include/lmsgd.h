@@ -1,0 +1,237 @@
+/*
+ * lmsgd.h -- C ABI of the B200-native gradient exchange + blended update of
+ * arXiv 1711.04325 (Akiba et al., "Extremely Large Minibatch SGD: Training
+ * ResNet-50 on ImageNet in 15 Minutes").
+ *
+ * One synchronous data-parallel iteration
+ * after the backward pass, on k = world GPUs of one node:
+ *
+ *   pack     h   = sat16_RNE(s * g)                  fp32 -> fp16 wire
+ *   exchange R   = sat16_RNE(sum_ranks h)            fp16 all-reduce, exact accumulation
+ *   unpack   ghat = fp32(R) * (1 / (k s))            "casts back and averages"
+ *   update   m     = mu2 m + (1 - mu2) ghat^2
+ *            Delta = mu1 Delta - (a_SGD + a_RMS / (sqrt(m) + eps)) ghat
+ *            theta = theta + eta Delta
+ *
+ * with (eta, a_SGD, a_RMS) from the slow-start / RMSprop-warm-up schedule
+ * (PAPER.md:174-196, 216-230), and the BN last-minibatch statistics average before
+ * validation.  Readings of ambiguous passages: DESIGN.md R1-R20.
+ *
+ * Conventions for every function below
+ *  - Return value: LMSGD_OK (0) or a negative lmsgd_status.  Argument errors are
+ *    detected synchronously, before anything is enqueued, and leave all buffers
+ *    untouched.  lmsgd_last_error(ctx) gives a one-line message.
+ *  - "device" pointers are CUDA device pointers on the context's device
+ *    (cudaMalloc / torch CUDA tensors), fp32, contiguous, 16-byte aligned.
+ *    "host" pointers are ordinary or pinned host memory as stated.
+ *  - All device work is enqueued on the caller's `stream` (a cudaStream_t passed
+ *    as void*; NULL = legacy default stream) and the call returns before it
+ *    completes.  Caller-owned buffers must stay alive until the stream passes.
+ *  - Ownership: the caller owns params/grads/delta/m/mean/var.  The library owns
+ *    its fusion (fp16 wire) buffers, flags, status words and peer mappings.
+ *  - Thread safety: one context per rank per host thread.
+ *  - Determinism: identical inputs give bit-identical outputs on every rank and
+ *    every run (the fp16 sum is exact, the update is elementwise).
+ */
+#ifndef LMSGD_H
+#define LMSGD_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(LMSGD_BUILD) && defined(__GNUC__)
+#pragma GCC visibility push(default)  /* the library is built with -fvisibility=hidden */
+#endif
+
+#define LMSGD_ABI_VERSION 1
+#define LMSGD_MAX_WORLD 8            /* one NVSwitch node */
+#define LMSGD_IPC_HANDLE_BYTES 64    /* sizeof(cudaIpcMemHandle_t) */
+#define LMSGD_MAX_BN_CHANNELS (1 << 20)
+
+typedef enum {
+    LMSGD_OK = 0,
+    LMSGD_ERR_INVALID_ARG = -1,   /* null/misaligned pointer, bad size, t < 1, eta <= 0 ... */
+    LMSGD_ERR_CUDA = -2,          /* a CUDA runtime call failed (message in last_error)   */
+    LMSGD_ERR_NONFINITE = -4,     /* a gradient entry was NaN/Inf: the step was skipped    */
+    LMSGD_ERR_STATE = -5,         /* call out of order (e.g. step before connect)          */
+    LMSGD_ERR_UNSUPPORTED = -6,   /* e.g. world > LMSGD_MAX_WORLD, no peer access          */
+    LMSGD_ERR_TIMEOUT = -7,       /* a cross-GPU wait exceeded the timeout; step skipped   */
+    LMSGD_ERR_RANGE = -8          /* schedule asked past its last epoch                    */
+} lmsgd_status;
+
+/* Hyperparameters, PAPER.md:167 (mu1, mu2, eps), PAPER.md:190 (beta_center,
+ * beta_period), PAPER.md:192 (eta_RMSprop).  lmsgd_hyper_default fills
+ * 0.9, 0.99, 1e-8, 3e-4, 10, 5. */
+typedef struct lmsgd_hyper {
+    double mu1, mu2, eps, eta_rmsprop, beta_center, beta_period;
+} lmsgd_hyper;
+
+/* Logical cluster shape that drives eta_base = 0.1 * n_workers * b_local / 256
+ * (PAPER.md:217-221).  Independent of the physical world size k: the paper's
+ * 32k run is n_workers = 1024, b_local = 32.  n_train = images per epoch (the
+ * paper does not print it; ImageNet-1k = 1,281,167, R5).
+ * schedule: 0 = slow-start, 1 = Goyal et al.. */
+typedef struct lmsgd_cluster {
+    int64_t n_workers, b_local, n_train;
+    int32_t schedule;
+    int32_t reserved;
+} lmsgd_cluster;
+
+/* Per-step coefficients.  lmsgd_schedule_at is the canonical source; a caller may
+ * pass its own (eta > 0, 0 <= alpha_sgd <= 1, alpha_rmsprop >= 0). */
+typedef struct lmsgd_coeffs {
+    double epoch;          /* (t-1) b_total / n_train, start of step (R2, R3)  */
+    double eta;            /* eta_SGD of the current phase      */
+    double alpha_sgd;      /* ELU-like transition, slope 1/beta_period (R1)    */
+    double alpha_rmsprop;  /* ((1 - alpha_sgd) eta_RMSprop) / eta */
+    int32_t phase;         /* LR phase index 0..3 */
+    int32_t reserved;
+} lmsgd_coeffs;
+
+/* Result of the most recent step (all ranks see the same values). */
+typedef struct lmsgd_step_status {
+    int64_t first_nonfinite;   /* smallest flat index j with non-finite g_j on any rank; -1 none */
+    int64_t pack_saturations;  /* sum over ranks of #{j : |s g_j| > 65504}              */
+    int64_t sum_saturations;   /* #{j : |sum_ranks h_j| > 65504} (wire-2 clamp)          */
+    int32_t skipped;           /* 1 if the update was not applied (non-finite / timeout) */
+    int32_t error;             /* 0, LMSGD_ERR_NONFINITE or LMSGD_ERR_TIMEOUT             */
+} lmsgd_step_status;
+
+typedef struct lmsgd_ctx lmsgd_ctx;   /* opaque, library-owned */
+
+/* init flags */
+#define LMSGD_FLAG_NO_SKIP 0x1u   /* k = 1: single-pass fused pack+update (28 B/elem); non-finite
+                                     gradients are detected and reported but NOT skipped */
+
+/* ---------------------------------------------------------------- host-only */
+
+int lmsgd_abi_version(void);
+const char* lmsgd_status_string(lmsgd_status s);
+
+/* Fill the paper's hyperparameters (see lmsgd_hyper).  Never fails except for NULL. */
+lmsgd_status lmsgd_hyper_default(lmsgd_hyper* out);
+
+/* Schedule coefficients of iteration t >= 1, pure host
+ * function, IEEE double in the operation order of DESIGN.md "Schedule":
+ *   epoch = ((t-1) b_total) / n_train;  phase p = first with (t-1) b_total < E_p n_train
+ *   eta = mult_p * (0.1 * b_total / 256);  a_SGD = alpha(epoch);
+ *   a_RMS = ((1 - a_SGD) eta_RMSprop) / eta
+ * Errors: INVALID_ARG (NULL, t < 1, non-positive sizes, beta_period <= 0),
+ *         RANGE (t past the last epoch). */
+lmsgd_status lmsgd_schedule_at(const lmsgd_hyper* hyper, const lmsgd_cluster* cluster,
+                               int64_t t, lmsgd_coeffs* out);
+
+/* Number of iterations T the schedule covers (90 epochs). */
+lmsgd_status lmsgd_schedule_steps(const lmsgd_cluster* cluster, int64_t* T);
+
+/* ---------------------------------------------------------------- context */
+
+/* Create the context of rank `rank` of `world` (1..LMSGD_MAX_WORLD) on CUDA
+ * `device` for n_params parameters.  loss_scale s: a positive power of two, the
+ * same on all ranks (R11).  hyper may be NULL (paper defaults).  Allocates the
+ * fusion buffers: world == 1 needs nothing else; world > 1 must then call
+ * lmsgd_ipc_handle + lmsgd_connect.  Synchronous. */
+lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_t n_params,
+                        float loss_scale, const lmsgd_hyper* hyper, uint32_t flags);
+
+/* world > 1: this rank's CUDA IPC handle of its exchange buffer
+ * (LMSGD_IPC_HANDLE_BYTES host bytes).  The caller all-gathers the handles by any
+ * means (e.g. torch.distributed) -- the library does no host networking. */
+lmsgd_status lmsgd_ipc_handle(lmsgd_ctx* ctx, uint8_t* out);
+
+/* world > 1: map every peer's exchange buffer.  handles = world * LMSGD_IPC_HANDLE_BYTES
+ * host bytes in rank order (this rank's own entry is ignored).  Synchronous;
+ * must be called by all ranks before the first step. */
+lmsgd_status lmsgd_connect(lmsgd_ctx* ctx, const uint8_t* handles);
+
+/* Synchronizes the device, unmaps peers, frees library buffers.  NULL is a no-op. */
+lmsgd_status lmsgd_finalize(lmsgd_ctx* ctx);
+
+/* Message of the last failing call on ctx ("" if none); valid until the next call. */
+const char* lmsgd_last_error(const lmsgd_ctx* ctx);
+
+/* ---------------------------------------------------------------- hot path */
+
+/* One synchronous data-parallel iteration on this rank (all ranks must call it
+ * with the same coeffs, in the same order):
+ *   params [n] device in/out theta;  grads [n] device in g (this rank's);
+ *   delta [n], m [n] device in/out optimizer state (zero before the first step).
+ * Enqueued on `stream`; returns before completion.  A non-finite gradient on ANY
+ * rank leaves params/delta/m untouched on EVERY rank (reported by
+ * lmsgd_query_status), unless LMSGD_FLAG_NO_SKIP at world == 1. */
+lmsgd_status lmsgd_step(lmsgd_ctx* ctx, void* stream, float* params, const float* grads,
+                        float* delta, float* m, const lmsgd_coeffs* coeffs);
+
+/* The same iteration with the gradient in HOST memory (pinned for full speed):
+ * copies grads_host -> device inside the call's stream work, runs lmsgd_step and
+ * copies the step status back into *status_host (valid once `stream` has passed
+ * this point).  The end-to-end entry point bench.py times as "e2e". */
+lmsgd_status lmsgd_step_host(lmsgd_ctx* ctx, void* stream, float* params, const float* grads_host,
+                             float* delta, float* m, const lmsgd_coeffs* coeffs,
+                             lmsgd_step_status* status_host);
+
+/* BN statistics without moving averages (R16): on every rank,
+ *   mean[c] <- fp32( (sum_{r=0..k-1} mean_r[c]) / k ),  var likewise,
+ * summed in fp64 in rank order, one rounding.  mean, var: device fp32 [C],
+ * 0 < C <= LMSGD_MAX_BN_CHANNELS, in/out.  world == 1: identity (no kernel). */
+lmsgd_status lmsgd_bn_stats_allreduce(lmsgd_ctx* ctx, void* stream, float* mean, float* var,
+                                      int64_t C);
+
+/* Wait for the last step on its stream and report its status.  Returns
+ * LMSGD_ERR_NONFINITE / LMSGD_ERR_TIMEOUT if that step was skipped. */
+lmsgd_status lmsgd_query_status(lmsgd_ctx* ctx, lmsgd_step_status* out);
+
+/* ---------------------------------------------------------------- profiling
+ * Per-kernel device timing of lmsgd_step, measured with CUDA events recorded on
+ * the step's stream around each kernel launch (used by bench.py for the roofline
+ * of the dominant kernel).  Phases: 0 = pack (k_pack / k_pack_push / k_fused1),
+ * 1 = reduce (k_reduce_shard), 2 = update (k_update / k_update_gather). */
+
+/* max_launches > 0: start recording (event pool sized for that many kernel
+ * launches; further launches are not timed).  0: stop and discard.  Synchronous. */
+lmsgd_status lmsgd_profile_enable(lmsgd_ctx* ctx, int64_t max_launches);
+
+/* Wait for the recorded launches, return the summed device milliseconds and the
+ * launch count of each phase (arrays of 3), and clear the record. */
+lmsgd_status lmsgd_profile_read(lmsgd_ctx* ctx, double* ms, int64_t* launches);
+
+/* ---------------------------------------------------------------- sub-steps
+ * Context-free single-GPU kernels, exported for parity tests and for the
+ * simulated-k mode (k workers' payloads on one GPU).  `dstatus` is a device
+ * int64[4] accumulator {first_nonfinite (INT64_MAX = none), pack_saturations,
+ * sum_saturations, error}; reset it with lmsgd_status_reset. */
+
+lmsgd_status lmsgd_status_reset(void* stream, int64_t* dstatus);
+
+/* h[j] = sat16_RNE(s * g[j]) for j < n, h[j] = 0 for n <= j < n_pad.
+ * g: device fp32 [n]; h: device uint16 (binary16 bits) [n_pad], n_pad >= n, n_pad % 8 == 0. */
+lmsgd_status lmsgd_pack(void* stream, const float* g, int64_t n, int64_t n_pad, float loss_scale,
+                        uint16_t* h, int64_t* dstatus);
+
+/* R[j] = sat16_RNE(sum_{i<k} h[i * n_pad + j]) (exact fp64 sum), j < n_pad.
+ * h: device uint16 [k][n_pad]; R: device uint16 [n_pad]; 1 <= k <= 8192. */
+lmsgd_status lmsgd_reduce_local(void* stream, const uint16_t* h, int k, int64_t n_pad,
+                                uint16_t* R, int64_t* dstatus);
+
+/* ghat = fp32(R[j]) * fp32(1/(k s)) and the blended update on params/delta/m [n].
+ * If dstatus != NULL and dstatus[0] != INT64_MAX (a non-finite gradient was
+ * packed) the update is skipped. */
+lmsgd_status lmsgd_update(void* stream, const uint16_t* R, int64_t n, int k, float loss_scale,
+                          const lmsgd_hyper* hyper, const lmsgd_coeffs* coeffs,
+                          float* params, float* delta, float* m, const int64_t* dstatus);
+
+/* k = 1 single pass: pack + unpack + update without the fp16 buffer (28 B/elem). */
+lmsgd_status lmsgd_fused_step1(void* stream, const float* g, int64_t n, float loss_scale,
+                               const lmsgd_hyper* hyper, const lmsgd_coeffs* coeffs,
+                               float* params, float* delta, float* m, int64_t* dstatus);
+
+#if defined(LMSGD_BUILD) && defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* LMSGD_H */

@@ -1,0 +1,470 @@
+// C ABI of lmsgd (include/lmsgd.h): argument checking, the per-rank context
+// (exchange buffers, CUDA-IPC peer mappings, status words) and the stream-ordered
+// composition of the sm_100a kernels in kernels.cu.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "lmsgd.h"
+#include "lmsgd_internal.h"
+
+using lmsgd::Layout;
+using lmsgd::UpdConst;
+
+struct lmsgd_ctx {
+    int world = 1, rank = 0, device = 0;
+    int64_t n = 0, n_pad = 0;
+    float scale = 1.0f;
+    lmsgd_hyper hyper{};
+    uint32_t flags = 0;
+    Layout lay{};
+    char* buf = nullptr;           // own exchange buffer (IPC-shared when world > 1)
+    lmsgd::Peers peers{};
+    bool connected = false;
+    unsigned int* tickets = nullptr;  // device [4]
+    int64_t* last = nullptr;          // device lmsgd_step_status of the last step
+    float* d_grads = nullptr;         // device staging for lmsgd_step_host (lazy)
+    uint32_t step = 0, bn_calls = 0;
+    cudaStream_t last_stream = nullptr;
+    lmsgd::Launch L{};
+    int64_t timeout_ns = 10'000'000'000LL;
+    std::string err;
+    // profiling (lmsgd_profile_enable): event pairs around each kernel launch
+    struct Rec { int phase; cudaEvent_t a, b; };
+    std::vector<cudaEvent_t> pool;
+    std::vector<Rec> recs;
+    size_t prof_cap = 0;
+};
+
+namespace {
+
+thread_local std::string g_err;  // for context-free calls
+
+lmsgd_status fail(lmsgd_ctx* c, lmsgd_status s, const std::string& msg) {
+    if (c) c->err = msg; else g_err = msg;
+    return s;
+}
+
+lmsgd_status cuda_fail(lmsgd_ctx* c, cudaError_t e, const char* what) {
+    return fail(c, LMSGD_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define CK(ctx, call)                                                   \
+    do {                                                                \
+        cudaError_t e_ = (call);                                        \
+        if (e_ != cudaSuccess) return cuda_fail((ctx), e_, #call);      \
+    } while (0)
+
+int64_t align_up(int64_t x, int64_t a) { return (x + a - 1) / a * a; }
+
+bool aligned16(const void* p) { return p && (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+bool pow2_scale(float s) {
+    if (!(s > 0.0f) || !std::isfinite(s)) return false;
+    int e;
+    return std::frexp(static_cast<double>(s), &e) == 0.5;
+}
+
+// Launch geometry of the current device: SMs x resident blocks of the streaming kernels.
+lmsgd::Launch launch_for_current_device() {
+    static lmsgd::Launch cache[64];
+    static bool have[64] = {};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev >= 0 && dev < 64 && have[dev]) return cache[dev];
+    lmsgd::Launch L{};
+    cudaDeviceGetAttribute(&L.sm_count, cudaDevAttrMultiProcessorCount, dev);
+    L.grid_cap_stream = L.sm_count * lmsgd::stream_blocks_per_sm();
+    if (dev >= 0 && dev < 64) { cache[dev] = L; have[dev] = true; }
+    return L;
+}
+
+bool coeffs_ok(const lmsgd_coeffs* c) {
+    return c && std::isfinite(c->eta) && c->eta > 0.0 && c->alpha_sgd >= 0.0 && c->alpha_sgd <= 1.0 &&
+           std::isfinite(c->alpha_rmsprop) && c->alpha_rmsprop >= 0.0;
+}
+
+bool hyper_ok(const lmsgd_hyper* h) {
+    return h && h->mu1 >= 0.0 && h->mu1 < 1.0 && h->mu2 >= 0.0 && h->mu2 < 1.0 && h->eps > 0.0 &&
+           std::isfinite(h->eps);
+}
+
+// fp32 constants rounded once from double (R15: fp32(1 - mu2), not 1 - fp32(mu2)).
+UpdConst make_const(const lmsgd_hyper& h, const lmsgd_coeffs& c, int k, float s) {
+    UpdConst u{};
+    u.mu1 = static_cast<float>(h.mu1);
+    u.mu2 = static_cast<float>(h.mu2);
+    u.omm2 = static_cast<float>(1.0 - h.mu2);
+    u.eps = static_cast<float>(h.eps);
+    u.eta = static_cast<float>(c.eta);
+    u.a_sgd = static_cast<float>(c.alpha_sgd);
+    u.a_rms = static_cast<float>(c.alpha_rmsprop);
+    u.inv_ks = static_cast<float>(1.0 / (static_cast<double>(k) * static_cast<double>(s)));
+    return u;
+}
+
+Layout make_layout(int world, int64_t n) {
+    Layout L{};
+    L.shard = align_up((n + world - 1) / world, 64);
+    if (L.shard == 0) L.shard = 64;
+    L.off_recv = 0;
+    int64_t off = align_up(L.off_recv + 2 * L.shard * world, 256);
+    if (world > 1) {
+        L.off_R = off;
+        off = align_up(off + 2 * L.shard, 256);
+    } else {
+        L.off_R = L.off_recv;  // k = 1: the packed buffer is the all-reduce result
+    }
+    L.off_status = off;
+    off = align_up(off + 2 * lmsgd::ST_WORDS * 8, 256);
+    L.off_flags = off;
+    off = align_up(off + 3 * 128, 256);
+    L.off_bn = off;
+    if (world > 1) off = align_up(off + int64_t(2) * 2 * LMSGD_MAX_BN_CHANNELS * 4, 256);
+    L.bytes = off;
+    return L;
+}
+
+int64_t* status_slot(lmsgd_ctx* c, int parity) {
+    return reinterpret_cast<int64_t*>(c->buf + c->lay.off_status) + parity * lmsgd::ST_WORDS;
+}
+
+lmsgd::XArgs xargs(lmsgd_ctx* c, uint32_t epoch) {
+    lmsgd::XArgs x{};
+    x.peers = c->peers;
+    x.lay = c->lay;
+    x.world = c->world;
+    x.rank = c->rank;
+    x.epoch = epoch;
+    x.parity = static_cast<int>(epoch & 1u);
+    x.n = c->n;
+    x.timeout_ns = c->timeout_ns;
+    x.ticket = c->tickets;
+    return x;
+}
+
+// Device-guard: make ctx->device current for the duration of a call.
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Launch one kernel, bracketed by profiling events when enabled.
+template <class F>
+cudaError_t timed(lmsgd_ctx* c, cudaStream_t s, int phase, F&& launch) {
+    const bool rec = c->prof_cap > 0 && c->recs.size() < c->prof_cap && c->pool.size() >= 2;
+    lmsgd_ctx::Rec r{phase, nullptr, nullptr};
+    if (rec) {
+        r.b = c->pool.back(); c->pool.pop_back();
+        r.a = c->pool.back(); c->pool.pop_back();
+        cudaEventRecord(r.a, s);
+    }
+    cudaError_t e = launch();
+    if (rec) {
+        cudaEventRecord(r.b, s);
+        c->recs.push_back(r);
+    }
+    return e;
+}
+
+}  // namespace
+
+extern "C" {
+
+int lmsgd_abi_version(void) { return LMSGD_ABI_VERSION; }
+
+const char* lmsgd_status_string(lmsgd_status s) {
+    switch (s) {
+        case LMSGD_OK: return "ok";
+        case LMSGD_ERR_INVALID_ARG: return "invalid argument";
+        case LMSGD_ERR_CUDA: return "CUDA error";
+        case LMSGD_ERR_NONFINITE: return "non-finite gradient (step skipped)";
+        case LMSGD_ERR_STATE: return "call out of order";
+        case LMSGD_ERR_UNSUPPORTED: return "unsupported";
+        case LMSGD_ERR_TIMEOUT: return "cross-GPU wait timed out (step skipped)";
+        case LMSGD_ERR_RANGE: return "schedule step out of range";
+    }
+    return "unknown status";
+}
+
+const char* lmsgd_last_error(const lmsgd_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
+
+lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_t n_params,
+                        float loss_scale, const lmsgd_hyper* hyper, uint32_t flags) {
+    if (!out) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    if (world < 1 || world > LMSGD_MAX_WORLD)
+        return fail(nullptr, LMSGD_ERR_UNSUPPORTED, "world must be in [1, LMSGD_MAX_WORLD]");
+    if (rank < 0 || rank >= world) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "rank out of range");
+    if (n_params < 1 || n_params > (int64_t(1) << 36))
+        return fail(nullptr, LMSGD_ERR_INVALID_ARG, "n_params out of range");
+    if (!pow2_scale(loss_scale))
+        return fail(nullptr, LMSGD_ERR_INVALID_ARG, "loss_scale must be a positive power of two");
+    lmsgd_hyper h{};
+    if (hyper) h = *hyper; else lmsgd_hyper_default(&h);
+    if (!hyper_ok(&h)) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "hyperparameters out of range");
+    if (flags & ~LMSGD_FLAG_NO_SKIP) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "unknown flags");
+
+    int ndev = 0;
+    cudaError_t e = cudaGetDeviceCount(&ndev);
+    if (e != cudaSuccess) return fail(nullptr, LMSGD_ERR_CUDA, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    if (device < 0 || device >= ndev) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "device out of range");
+
+    auto* c = new lmsgd_ctx();
+    c->world = world; c->rank = rank; c->device = device; c->n = n_params;
+    c->scale = loss_scale; c->hyper = h; c->flags = flags;
+    c->lay = make_layout(world, n_params);
+    c->n_pad = c->lay.shard * world;
+    if (const char* t = std::getenv("LMSGD_TIMEOUT_MS")) c->timeout_ns = std::atoll(t) * 1000000LL;
+    DeviceGuard g(device);
+    auto bail = [&](lmsgd_status s) { c->connected = false; lmsgd_finalize(c); return s; };
+    if ((e = cudaMalloc(&c->buf, c->lay.bytes)) != cudaSuccess) { g_err = "cudaMalloc exchange buffer"; return bail(LMSGD_ERR_CUDA); }
+    if ((e = cudaMemset(c->buf, 0, c->lay.bytes)) != cudaSuccess) { g_err = "cudaMemset"; return bail(LMSGD_ERR_CUDA); }
+    const int64_t init_status[2 * lmsgd::ST_WORDS] = {lmsgd::kNone, 0, 0, 0, lmsgd::kNone, 0, 0, 0};
+    if ((e = cudaMemcpy(c->buf + c->lay.off_status, init_status, sizeof init_status, cudaMemcpyHostToDevice)) != cudaSuccess) {
+        g_err = "cudaMemcpy status"; return bail(LMSGD_ERR_CUDA);
+    }
+    if ((e = cudaMalloc(&c->tickets, 4 * sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMemset(c->tickets, 0, 4 * sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMalloc(&c->last, sizeof(lmsgd_step_status))) != cudaSuccess ||
+        (e = cudaMemset(c->last, 0, sizeof(lmsgd_step_status))) != cudaSuccess) {
+        g_err = std::string("context allocations: ") + cudaGetErrorString(e);
+        return bail(LMSGD_ERR_CUDA);
+    }
+    if ((e = cudaDeviceSynchronize()) != cudaSuccess) { g_err = cudaGetErrorString(e); return bail(LMSGD_ERR_CUDA); }
+    c->L = launch_for_current_device();
+    for (int p = 0; p < LMSGD_MAX_WORLD; ++p) c->peers.base[p] = nullptr;
+    c->peers.base[rank] = c->buf;
+    c->connected = (world == 1);
+    *out = c;
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_ipc_handle(lmsgd_ctx* c, uint8_t* out) {
+    if (!c || !out) return fail(c, LMSGD_ERR_INVALID_ARG, "NULL argument");
+    if (c->world == 1) return fail(c, LMSGD_ERR_STATE, "world == 1 has no peers");
+    DeviceGuard g(c->device);
+    cudaIpcMemHandle_t h;
+    CK(c, cudaIpcGetMemHandle(&h, c->buf));
+    static_assert(sizeof(h) == LMSGD_IPC_HANDLE_BYTES, "IPC handle size");
+    std::memcpy(out, &h, sizeof h);
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_connect(lmsgd_ctx* c, const uint8_t* handles) {
+    if (!c || !handles) return fail(c, LMSGD_ERR_INVALID_ARG, "NULL argument");
+    if (c->world == 1) return LMSGD_OK;
+    if (c->connected) return fail(c, LMSGD_ERR_STATE, "already connected");
+    DeviceGuard g(c->device);
+    for (int p = 0; p < c->world; ++p) {
+        if (p == c->rank) continue;
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handles + p * LMSGD_IPC_HANDLE_BYTES, sizeof h);
+        void* ptr = nullptr;
+        CK(c, cudaIpcOpenMemHandle(&ptr, h, cudaIpcMemLazyEnablePeerAccess));
+        c->peers.base[p] = static_cast<char*>(ptr);
+    }
+    c->connected = true;
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
+    if (!c) return LMSGD_OK;
+    {
+        DeviceGuard g(c->device);
+        cudaDeviceSynchronize();
+        for (int p = 0; p < LMSGD_MAX_WORLD; ++p)
+            if (p != c->rank && c->peers.base[p]) cudaIpcCloseMemHandle(c->peers.base[p]);
+        if (c->buf) cudaFree(c->buf);
+        if (c->tickets) cudaFree(c->tickets);
+        if (c->last) cudaFree(c->last);
+        if (c->d_grads) cudaFree(c->d_grads);
+        for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
+        for (auto e : c->pool) cudaEventDestroy(e);
+    }
+    delete c;
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* grads, float* delta,
+                        float* m, const lmsgd_coeffs* coeffs) {
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (!aligned16(params) || !aligned16(grads) || !aligned16(delta) || !aligned16(m))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "params/grads/delta/m must be non-NULL and 16-byte aligned");
+    if (!coeffs_ok(coeffs))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "coeffs: need eta > 0, 0 <= alpha_sgd <= 1, alpha_rmsprop >= 0");
+    if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const UpdConst u = make_const(c->hyper, *coeffs, c->world, c->scale);
+    const uint32_t epoch = ++c->step;
+    const int parity = static_cast<int>(epoch & 1u);
+    c->last_stream = s;
+    if (c->world == 1) {
+        uint16_t* h = reinterpret_cast<uint16_t*>(c->buf + c->lay.off_recv);
+        if (c->flags & LMSGD_FLAG_NO_SKIP) {
+            CK(c, timed(c, s, 0, [&] {
+                   return lmsgd::launch_fused1(s, c->L, grads, c->n, c->scale, u, params, delta, m,
+                                               status_slot(c, parity), status_slot(c, parity ^ 1),
+                                               c->tickets + 3, c->last);
+               }));
+        } else {
+            CK(c, timed(c, s, 0, [&] {
+                   return lmsgd::launch_pack(s, c->L, grads, c->n, c->n_pad, c->scale, h, status_slot(c, parity));
+               }));
+            CK(c, timed(c, s, 2, [&] {
+                   return lmsgd::launch_update(s, c->L, h, c->n, u, params, delta, m, status_slot(c, parity),
+                                               status_slot(c, parity ^ 1), c->last);
+               }));
+        }
+        return LMSGD_OK;
+    }
+    const lmsgd::XArgs x = xargs(c, epoch);
+    CK(c, timed(c, s, 0, [&] { return lmsgd::launch_pack_push(s, c->L, x, grads, c->scale); }));
+    CK(c, timed(c, s, 1, [&] { return lmsgd::launch_reduce_shard(s, c->L, x); }));
+    CK(c, timed(c, s, 2, [&] { return lmsgd::launch_update_gather(s, c->L, x, u, params, delta, m, c->last); }));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_step_host(lmsgd_ctx* c, void* stream, float* params, const float* grads_host,
+                             float* delta, float* m, const lmsgd_coeffs* coeffs,
+                             lmsgd_step_status* status_host) {
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (!grads_host || !status_host) return fail(c, LMSGD_ERR_INVALID_ARG, "NULL host pointer");
+    DeviceGuard g(c->device);
+    if (!c->d_grads) CK(c, cudaMalloc(&c->d_grads, c->n * sizeof(float)));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    CK(c, cudaMemcpyAsync(c->d_grads, grads_host, c->n * sizeof(float), cudaMemcpyHostToDevice, s));
+    const lmsgd_status st = lmsgd_step(c, stream, params, c->d_grads, delta, m, coeffs);
+    if (st != LMSGD_OK) return st;
+    CK(c, cudaMemcpyAsync(status_host, c->last, sizeof(lmsgd_step_status), cudaMemcpyDeviceToHost, s));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_query_status(lmsgd_ctx* c, lmsgd_step_status* out) {
+    if (!c || !out) return fail(c, LMSGD_ERR_INVALID_ARG, "NULL argument");
+    if (c->step == 0) return fail(c, LMSGD_ERR_STATE, "no step has run");
+    DeviceGuard g(c->device);
+    CK(c, cudaStreamSynchronize(c->last_stream));
+    CK(c, cudaMemcpy(out, c->last, sizeof *out, cudaMemcpyDeviceToHost));
+    if (out->error != 0) return static_cast<lmsgd_status>(out->error);
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_bn_stats_allreduce(lmsgd_ctx* c, void* stream, float* mean, float* var, int64_t C) {
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (!mean || !var || C < 1 || C > LMSGD_MAX_BN_CHANNELS)
+        return fail(c, LMSGD_ERR_INVALID_ARG, "mean/var must be non-NULL, 0 < C <= LMSGD_MAX_BN_CHANNELS");
+    if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
+    if (c->world == 1) return LMSGD_OK;  // the average of one worker is itself
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const lmsgd::XArgs x = xargs(c, ++c->bn_calls);
+    CK(c, lmsgd::launch_bn_stage(s, x, mean, var, C));
+    CK(c, lmsgd::launch_bn_reduce(s, x, mean, var, C));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_profile_enable(lmsgd_ctx* c, int64_t max_launches) {
+    if (!c || max_launches < 0 || max_launches > (int64_t(1) << 22))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "profile_enable: bad argument");
+    DeviceGuard g(c->device);
+    CK(c, cudaDeviceSynchronize());
+    for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
+    c->recs.clear();
+    c->prof_cap = static_cast<size_t>(max_launches);
+    while (c->pool.size() < 2 * c->prof_cap) {
+        cudaEvent_t e;
+        CK(c, cudaEventCreate(&e));
+        c->pool.push_back(e);
+    }
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_profile_read(lmsgd_ctx* c, double* ms, int64_t* launches) {
+    if (!c || !ms || !launches) return fail(c, LMSGD_ERR_INVALID_ARG, "profile_read: NULL argument");
+    DeviceGuard g(c->device);
+    for (int p = 0; p < 3; ++p) { ms[p] = 0.0; launches[p] = 0; }
+    for (auto& r : c->recs) {
+        CK(c, cudaEventSynchronize(r.b));
+        float t = 0.0f;
+        CK(c, cudaEventElapsedTime(&t, r.a, r.b));
+        ms[r.phase] += t;
+        launches[r.phase] += 1;
+        c->pool.push_back(r.a);
+        c->pool.push_back(r.b);
+    }
+    c->recs.clear();
+    return LMSGD_OK;
+}
+
+// ---------------------------------------------------------------- sub-steps
+
+lmsgd_status lmsgd_status_reset(void* stream, int64_t* dstatus) {
+    if (!dstatus) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "dstatus is NULL");
+    cudaError_t e = lmsgd::launch_status_reset(static_cast<cudaStream_t>(stream), dstatus);
+    return e == cudaSuccess ? LMSGD_OK : cuda_fail(nullptr, e, "status_reset");
+}
+
+lmsgd_status lmsgd_pack(void* stream, const float* g, int64_t n, int64_t n_pad, float loss_scale,
+                        uint16_t* h, int64_t* dstatus) {
+    if (!aligned16(g) || !aligned16(h) || !dstatus || n < 0 || n_pad < n || n_pad % 8 != 0 || n_pad < 8)
+        return fail(nullptr, LMSGD_ERR_INVALID_ARG, "pack: bad pointer or size (n_pad >= n, n_pad % 8 == 0)");
+    if (!pow2_scale(loss_scale)) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "loss_scale must be a power of two");
+    cudaError_t e = lmsgd::launch_pack(static_cast<cudaStream_t>(stream), launch_for_current_device(), g, n,
+                                       n_pad, loss_scale, h, dstatus);
+    return e == cudaSuccess ? LMSGD_OK : cuda_fail(nullptr, e, "pack");
+}
+
+lmsgd_status lmsgd_reduce_local(void* stream, const uint16_t* h, int k, int64_t n_pad, uint16_t* R,
+                                int64_t* dstatus) {
+    if (!aligned16(h) || !aligned16(R) || k < 1 || k > 8192 || n_pad < 8 || n_pad % 8 != 0)
+        return fail(nullptr, LMSGD_ERR_INVALID_ARG, "reduce_local: bad pointer, k or n_pad");
+    cudaError_t e = lmsgd::launch_reduce_local(static_cast<cudaStream_t>(stream), launch_for_current_device(),
+                                               h, k, n_pad, R, dstatus);
+    return e == cudaSuccess ? LMSGD_OK : cuda_fail(nullptr, e, "reduce_local");
+}
+
+lmsgd_status lmsgd_update(void* stream, const uint16_t* R, int64_t n, int k, float loss_scale,
+                          const lmsgd_hyper* hyper, const lmsgd_coeffs* coeffs, float* params, float* delta,
+                          float* m, const int64_t* dstatus) {
+    lmsgd_hyper h{};
+    if (hyper) h = *hyper; else lmsgd_hyper_default(&h);
+    if (!aligned16(R) || !aligned16(params) || !aligned16(delta) || !aligned16(m) || n < 1 || k < 1 ||
+        !pow2_scale(loss_scale) || !hyper_ok(&h) || !coeffs_ok(coeffs))
+        return fail(nullptr, LMSGD_ERR_INVALID_ARG, "update: bad pointer, size, scale, hyper or coeffs");
+    const UpdConst u = make_const(h, *coeffs, k, loss_scale);
+    cudaError_t e = lmsgd::launch_update(static_cast<cudaStream_t>(stream), launch_for_current_device(), R, n, u,
+                                         params, delta, m, dstatus, nullptr, nullptr);
+    return e == cudaSuccess ? LMSGD_OK : cuda_fail(nullptr, e, "update");
+}
+
+lmsgd_status lmsgd_fused_step1(void* stream, const float* g, int64_t n, float loss_scale,
+                               const lmsgd_hyper* hyper, const lmsgd_coeffs* coeffs, float* params,
+                               float* delta, float* m, int64_t* dstatus) {
+    lmsgd_hyper h{};
+    if (hyper) h = *hyper; else lmsgd_hyper_default(&h);
+    if (!aligned16(g) || !aligned16(params) || !aligned16(delta) || !aligned16(m) || !dstatus || n < 1 ||
+        !pow2_scale(loss_scale) || !hyper_ok(&h) || !coeffs_ok(coeffs))
+        return fail(nullptr, LMSGD_ERR_INVALID_ARG, "fused_step1: bad pointer, size, scale, hyper or coeffs");
+    const UpdConst u = make_const(h, *coeffs, 1, loss_scale);
+    cudaError_t e = lmsgd::launch_fused1(static_cast<cudaStream_t>(stream), launch_for_current_device(), g, n,
+                                         loss_scale, u, params, delta, m, dstatus, nullptr, nullptr, nullptr);
+    return e == cudaSuccess ? LMSGD_OK : cuda_fail(nullptr, e, "fused_step1");
+}
+
+}  // extern "C"

@@ -1,0 +1,557 @@
+// sm_100a kernels of the gradient exchange + blended update (arXiv 1711.04325).
+//
+// Everything here is HBM- or NVLink-bound streaming work:
+// there is no dense contraction, so no tensor cores.  The kernels move 16-byte
+// vectors (8 elements per thread per trip), use evict-first streaming hints for
+// data touched once (g, theta, Delta, m), and keep the fp16 wire buffers on the
+// default policy so a consumer launched right after the producer hits L2.
+//
+// Cross-GPU ordering (world > 1) uses flags in each rank's CUDA-IPC exchange
+// buffer: the last block of a producer kernel (ticket counter) issues a
+// system-scope fence and st.release.sys of the step's epoch into every peer's
+// flag slot; consumer blocks spin with ld.acquire.sys (bounded by a
+// %globaltimer timeout) before touching peer data.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lmsgd_internal.h"
+
+namespace lmsgd {
+namespace {
+
+constexpr int kThreads = 256;
+enum { FLAG_A = 0, FLAG_B = 1, FLAG_C = 2 };  // pack done, reduce done, BN staged
+
+// ------------------------------------------------------------------ helpers
+
+__device__ __forceinline__ bool nonfinite(float x) {
+    return (__float_as_uint(x) & 0x7f800000u) == 0x7f800000u;
+}
+
+// Two fp32 -> one f16x2 word, RNE, saturating to +-65504 (R7).  `lo` lands in
+// the low 16 bits (lower address).
+__device__ __forceinline__ uint32_t cvt_sat_f16x2(float lo, float hi) {
+    uint32_t r;
+    asm("cvt.rn.satfinite.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+    return r;
+}
+
+__device__ __forceinline__ float h2f(uint32_t w, int hi) {
+    return __half2float(__ushort_as_half(static_cast<unsigned short>(hi ? (w >> 16) : (w & 0xffffu))));
+}
+
+// binary16 of an exact float64 sum: clamp (saturation, R7) then one RNE rounding.
+__device__ __forceinline__ unsigned short sat16_f64(double a, unsigned& sat) {
+    if (fabs(a) > 65504.0) ++sat;
+    a = fmin(fmax(a, -65504.0), 65504.0);
+    return __half_as_ushort(__double2half(a));
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// 8 consecutive fp32 from j0 (j0 % 8 == 0), zero beyond n.  Streaming loads.
+__device__ __forceinline__ void load8_g(const float* __restrict__ g, int64_t j0, int64_t n,
+                                        float x[8]) {
+    if (j0 + 8 <= n) {
+        const float4 a = __ldcs(reinterpret_cast<const float4*>(g + j0));
+        const float4 b = __ldcs(reinterpret_cast<const float4*>(g + j0) + 1);
+        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
+        x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = (j0 + i < n) ? g[j0 + i] : 0.0f;
+    }
+}
+
+// h = sat16_RNE(s * g) for 8 values; records the first non-finite g index and
+// the count of finite g with |s g| > 65504.
+__device__ __forceinline__ uint4 pack8(const float x[8], float s, int64_t j0, int64_t& first,
+                                       unsigned& sat) {
+    float y[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const bool bad = nonfinite(x[i]);
+        if (bad) first = (j0 + i) < first ? (j0 + i) : first;
+        y[i] = s * x[i];
+        sat += (!bad && fabsf(y[i]) > 65504.0f) ? 1u : 0u;
+    }
+    return make_uint4(cvt_sat_f16x2(y[0], y[1]), cvt_sat_f16x2(y[2], y[3]),
+                      cvt_sat_f16x2(y[4], y[5]), cvt_sat_f16x2(y[6], y[7]));
+}
+
+// Warp-aggregated status flush: one atomic per warp (and none when clean).
+__device__ __forceinline__ void flush_status(int64_t first, unsigned sat, int64_t* st, int sat_slot) {
+    const unsigned full = 0xffffffffu;
+    const unsigned satw = __reduce_add_sync(full, sat);
+    const bool anyf = __any_sync(full, first != kNone);
+    if (anyf) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const int64_t other = __shfl_xor_sync(full, first, o);
+            first = other < first ? other : first;
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (satw) atomicAdd(reinterpret_cast<unsigned long long*>(st + sat_slot), (unsigned long long)satw);
+        if (anyf) atomicMin(reinterpret_cast<long long*>(st + ST_FIRST), (long long)first);
+    }
+}
+
+// The blended update of one element, fp32:
+//   m1 = mu2 m + (1-mu2) gh^2;  coef = a_SGD + a_RMS / (sqrt(m1) + eps)
+//   d1 = mu1 d - coef gh;       th1 = th + eta d1
+// RMS == false is the alpha_RMSprop == 0 specialisation (bit-identical: the
+// dropped term is exactly 0 because sqrt(m1) + eps >= eps > 0).
+template <bool RMS>
+__device__ __forceinline__ void upd1(float gh, float& th, float& d, float& m, const UpdConst& c) {
+    const float m1 = fmaf(c.mu2, m, c.omm2 * (gh * gh));
+    float coef = c.a_sgd;
+    if (RMS) coef = c.a_sgd + c.a_rms / (sqrtf(m1) + c.eps);
+    const float d1 = fmaf(c.mu1, d, -(coef * gh));
+    th = fmaf(c.eta, d1, th);
+    d = d1;
+    m = m1;
+}
+
+// Update 8 consecutive elements from j0 given their 8 fp16 wire values.
+template <bool RMS>
+__device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const UpdConst& c,
+                                        float* __restrict__ th, float* __restrict__ d,
+                                        float* __restrict__ m) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+    if (j0 + 8 <= n) {
+        float4* th4 = reinterpret_cast<float4*>(th + j0);
+        float4* d4 = reinterpret_cast<float4*>(d + j0);
+        float4* m4 = reinterpret_cast<float4*>(m + j0);
+        float4 t0 = __ldcs(th4), t1 = __ldcs(th4 + 1);
+        float4 d0 = __ldcs(d4), d1 = __ldcs(d4 + 1);
+        float4 m0 = __ldcs(m4), m1 = __ldcs(m4 + 1);
+        float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+        float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        float mv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
+            upd1<RMS>(gh, tv[i], dv[i], mv[i], c);
+        }
+        __stcs(th4, make_float4(tv[0], tv[1], tv[2], tv[3]));
+        __stcs(th4 + 1, make_float4(tv[4], tv[5], tv[6], tv[7]));
+        __stcs(d4, make_float4(dv[0], dv[1], dv[2], dv[3]));
+        __stcs(d4 + 1, make_float4(dv[4], dv[5], dv[6], dv[7]));
+        __stcs(m4, make_float4(mv[0], mv[1], mv[2], mv[3]));
+        __stcs(m4 + 1, make_float4(mv[4], mv[5], mv[6], mv[7]));
+    } else {
+        for (int i = 0; i < 8 && j0 + i < n; ++i) {
+            const float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
+            float t = th[j0 + i], dd = d[j0 + i], mm = m[j0 + i];
+            upd1<RMS>(gh, t, dd, mm, c);
+            th[j0 + i] = t; d[j0 + i] = dd; m[j0 + i] = mm;
+        }
+    }
+}
+
+__device__ __forceinline__ void reset_status(int64_t* st) {
+    if (st && blockIdx.x == 0 && threadIdx.x < ST_WORDS) st[threadIdx.x] = threadIdx.x == 0 ? kNone : 0;
+}
+
+// `last` record in the public lmsgd_step_status layout:
+// {int64 first (-1 none), int64 pack_sat, int64 sum_sat, int32 skipped, int32 error}
+__device__ __forceinline__ void store_last(int64_t* last, int64_t first, int64_t psat, int64_t ssat,
+                                           int64_t err, int64_t skipped) {
+    last[0] = first == kNone ? -1 : first;
+    last[1] = psat;
+    last[2] = ssat;
+    int32_t* tail = reinterpret_cast<int32_t*>(last + 3);
+    tail[0] = (int32_t)skipped;
+    tail[1] = (int32_t)(err ? err : (first != kNone ? (int64_t)LMSGD_ERR_NONFINITE : 0));
+}
+__device__ __forceinline__ void write_last(int64_t* last, int64_t first, int64_t psat, int64_t ssat,
+                                           int64_t err, int64_t skipped) {
+    if (last && blockIdx.x == 0 && threadIdx.x == 0) store_last(last, first, psat, ssat, err, skipped);
+}
+
+__device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
+__device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
+
+// ------------------------------------------------------------------ single GPU
+
+__global__ void k_status_reset(int64_t* st) {
+    if (threadIdx.x < ST_WORDS) st[threadIdx.x] = threadIdx.x == 0 ? kNone : 0;
+}
+
+__global__ void __launch_bounds__(kThreads) k_pack(const float* __restrict__ g, int64_t n,
+                                                   int64_t n_pad, float s, uint16_t* __restrict__ h,
+                                                   int64_t* st) {
+    int64_t first = kNone;
+    unsigned sat = 0;
+    const int64_t nv = n_pad >> 3;
+    for (int64_t v = gtid(); v < nv; v += gstride()) {
+        const int64_t j0 = v << 3;
+        float x[8];
+        load8_g(g, j0, n, x);
+        *reinterpret_cast<uint4*>(h + j0) = pack8(x, s, j0, first, sat);
+    }
+    flush_status(first, sat, st, ST_PACK_SAT);
+}
+
+__global__ void __launch_bounds__(kThreads) k_reduce_local(const uint16_t* __restrict__ h, int k,
+                                                           int64_t n_pad, uint16_t* __restrict__ R,
+                                                           int64_t* st) {
+    unsigned sat = 0;
+    const int64_t nv = n_pad >> 3;
+    for (int64_t v = gtid(); v < nv; v += gstride()) {
+        const int64_t j0 = v << 3;
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int i = 0; i < k; ++i) {  // worker order; exact, so order-free anyway
+            const uint4 q = *reinterpret_cast<const uint4*>(h + (int64_t)i * n_pad + j0);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
+        }
+        unsigned short o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
+        *reinterpret_cast<uint4*>(R + j0) =
+            make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
+                       o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
+    }
+    if (st) flush_status(kNone, sat, st, ST_SUM_SAT);
+}
+
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) k_update(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
+                                                     float* __restrict__ th, float* __restrict__ d,
+                                                     float* __restrict__ m, const int64_t* st,
+                                                     int64_t* st_reset, int64_t* last) {
+    int64_t first = kNone, psat = 0, ssat = 0, err = 0;
+    if (st) { first = st[ST_FIRST]; psat = st[ST_PACK_SAT]; ssat = st[ST_SUM_SAT]; err = st[ST_ERROR]; }
+    const bool skip = first != kNone || err != 0;
+    write_last(last, first, psat, ssat, err, skip);
+    reset_status(st_reset);
+    if (skip) return;
+    const int64_t nv = (n + 7) >> 3;
+    for (int64_t v = gtid(); v < nv; v += gstride()) {
+        const int64_t j0 = v << 3;
+        const uint4 r = *reinterpret_cast<const uint4*>(R + j0);
+        update8<RMS>(r, j0, n, c, th, d, m);
+    }
+}
+
+// k = 1 single pass (LMSGD_FLAG_NO_SKIP): h = sat16(s g) kept in registers,
+// ghat = fp32(h) / s, update.  28 B/elem of HBM traffic.
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g, int64_t n, float s,
+                                                     UpdConst c, float* __restrict__ th,
+                                                     float* __restrict__ d, float* __restrict__ m,
+                                                     int64_t* st, int64_t* st_reset,
+                                                     unsigned int* ticket, int64_t* last) {
+    reset_status(st_reset);
+    int64_t first = kNone;
+    unsigned sat = 0;
+    const int64_t nv = (n + 7) >> 3;
+    for (int64_t v = gtid(); v < nv; v += gstride()) {
+        const int64_t j0 = v << 3;
+        float x[8];
+        load8_g(g, j0, n, x);
+        const uint4 r = pack8(x, s, j0, first, sat);
+        update8<RMS>(r, j0, n, c, th, d, m);
+    }
+    flush_status(first, sat, st, ST_PACK_SAT);
+    if (last) {  // the last block to finish publishes the step status (not skipped)
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(ticket, 1u) == gridDim.x - 1) {
+            *ticket = 0;
+            __threadfence();
+            const volatile int64_t* vs = st;
+            store_last(last, vs[ST_FIRST], vs[ST_PACK_SAT], vs[ST_SUM_SAT], vs[ST_ERROR], 0);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ world > 1
+
+__device__ __forceinline__ uint32_t* flag_slot(const XArgs& x, int owner, int which) {
+    return reinterpret_cast<uint32_t*>(x.peers.base[owner] + x.lay.off_flags + which * 128);
+}
+__device__ __forceinline__ int64_t* status_of(const XArgs& x, int owner) {
+    return reinterpret_cast<int64_t*>(x.peers.base[owner] + x.lay.off_status) + x.parity * ST_WORDS;
+}
+
+// Every block: wait until all ranks have published `which` for this epoch.
+// Returns false (and records LMSGD_ERR_TIMEOUT locally) on timeout.
+__device__ bool block_wait(const XArgs& x, int which) {
+    __shared__ int timed_out;
+    if (threadIdx.x == 0) timed_out = 0;
+    __syncthreads();
+    if (threadIdx.x < x.world) {
+        const uint32_t* f = flag_slot(x, x.rank, which) + threadIdx.x;
+        const uint64_t t0 = globaltimer();
+        while ((int32_t)(ld_acquire_sys(f) - x.epoch) < 0) {
+            __nanosleep(32);
+            if ((int64_t)(globaltimer() - t0) > x.timeout_ns) { timed_out = 1; break; }
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    if (timed_out) {
+        if (threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(status_of(x, x.rank) + ST_ERROR),
+                                         (unsigned long long)(int64_t)LMSGD_ERR_TIMEOUT);
+        return false;
+    }
+    return true;
+}
+
+// Grid-wide "done": the last block to finish publishes `which` = epoch to every rank.
+__device__ void grid_signal(const XArgs& x, int which) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned t = atomicAdd(x.ticket + which, 1u);
+        if (t == gridDim.x - 1) {
+            x.ticket[which] = 0;
+            __threadfence_system();
+            for (int p = 0; p < x.world; ++p) st_release_sys(flag_slot(x, p, which) + x.rank, x.epoch);
+        }
+    }
+}
+
+// Pack this rank's gradient and push each shard straight into its owner's receive
+// slot (peer stores over NVLink).  Ranks walk the shards in rotated order so that at
+// any moment each owner receives from one sender.
+__global__ void __launch_bounds__(kThreads) k_pack_push(XArgs x, const float* __restrict__ g, float s) {
+    int64_t first = kNone;
+    unsigned sat = 0;
+    const int64_t gsh = x.lay.shard >> 3;
+    const int64_t nvp = gsh * x.world;
+    const int64_t rot = (int64_t)x.rank * gsh;
+    for (int64_t v = gtid(); v < nvp; v += gstride()) {
+        int64_t vv = v + rot;
+        if (vv >= nvp) vv -= nvp;
+        const int64_t j0 = vv << 3;
+        const int owner = (int)(vv / gsh);
+        const int64_t off = (vv - (int64_t)owner * gsh) << 3;
+        float xv[8];
+        load8_g(g, j0, x.n, xv);
+        uint16_t* dst = reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
+                        (int64_t)x.rank * x.lay.shard + off;
+        *reinterpret_cast<uint4*>(dst) = pack8(xv, s, j0, first, sat);
+    }
+    flush_status(first, sat, status_of(x, x.rank), ST_PACK_SAT);
+    grid_signal(x, FLAG_A);
+}
+
+// Owner-computes reduce of this rank's shard: exact fp64 sum of the world slots in
+// rank order, one saturating RNE rounding (the fp16 all-reduce SUM, R9/R10).
+__global__ void __launch_bounds__(kThreads) k_reduce_shard(XArgs x) {
+    if (!block_wait(x, FLAG_A)) return;
+    const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
+    uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
+    unsigned sat = 0;
+    const int64_t nv = x.lay.shard >> 3;
+    for (int64_t v = gtid(); v < nv; v += gstride()) {
+        const int64_t j0 = v << 3;
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int p = 0; p < x.world; ++p) {
+            const uint4 q = *reinterpret_cast<const uint4*>(recv + (int64_t)p * x.lay.shard + j0);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
+        }
+        unsigned short o[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
+        *reinterpret_cast<uint4*>(R + j0) =
+            make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
+                       o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
+    }
+    flush_status(kNone, sat, status_of(x, x.rank), ST_SUM_SAT);
+    grid_signal(x, FLAG_B);
+}
+
+// Update with the all-gather fused in: each element's R is loaded from its owner's
+// shard (peer loads over NVLink for remote shards), rotated per rank.
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) k_update_gather(XArgs x, UpdConst c, float* __restrict__ th,
+                                                            float* __restrict__ d, float* __restrict__ m,
+                                                            int64_t* last) {
+    __shared__ int64_t s_first, s_psat, s_ssat, s_err;
+    if (!block_wait(x, FLAG_B)) {
+        write_last(last, kNone, 0, 0, (int64_t)LMSGD_ERR_TIMEOUT, 1);
+        return;
+    }
+    if (threadIdx.x == 0) {
+        int64_t first = kNone, psat = 0, ssat = 0, err = 0;
+        for (int p = 0; p < x.world; ++p) {
+            const volatile int64_t* sp = status_of(x, p);
+            const int64_t f = sp[ST_FIRST];
+            first = f < first ? f : first;
+            psat += sp[ST_PACK_SAT];
+            ssat += sp[ST_SUM_SAT];
+            err = err ? err : sp[ST_ERROR];
+        }
+        s_first = first; s_psat = psat; s_ssat = ssat; s_err = err;
+    }
+    __syncthreads();
+    const bool skip = s_first != kNone || s_err != 0;
+    write_last(last, s_first, s_psat, s_ssat, s_err, skip);
+    if (blockIdx.x == 0 && threadIdx.x < ST_WORDS) {  // next step's status slot
+        int64_t* nxt = reinterpret_cast<int64_t*>(x.peers.base[x.rank] + x.lay.off_status) +
+                       (x.parity ^ 1) * ST_WORDS;
+        nxt[threadIdx.x] = threadIdx.x == 0 ? kNone : 0;
+    }
+    if (skip) return;
+    const int64_t gsh = x.lay.shard >> 3;
+    const int64_t nvp = gsh * x.world;
+    const int64_t rot = (int64_t)x.rank * gsh;
+    for (int64_t v = gtid(); v < nvp; v += gstride()) {
+        int64_t vv = v + rot;
+        if (vv >= nvp) vv -= nvp;
+        const int64_t j0 = vv << 3;
+        if (j0 >= x.n) continue;
+        const int owner = (int)(vv / gsh);
+        const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) +
+                             ((vv - (int64_t)owner * gsh) << 3);
+        const uint4 r = *reinterpret_cast<const uint4*>(Rp);
+        update8<RMS>(r, j0, x.n, c, th, d, m);
+    }
+}
+
+// BN statistics: stage [mean | var] in this rank's buffer, publish.
+__global__ void k_bn_stage(XArgs x, const float* __restrict__ mean, const float* __restrict__ var, int64_t C) {
+    float* stage = reinterpret_cast<float*>(x.peers.base[x.rank] + x.lay.off_bn) +
+                   (int64_t)x.parity * 2 * LMSGD_MAX_BN_CHANNELS;
+    for (int64_t i = gtid(); i < C; i += gstride()) {
+        stage[i] = mean[i];
+        stage[C + i] = var[i];
+    }
+    grid_signal(x, FLAG_C);
+}
+
+// Average over ranks in rank order, fp64, one rounding to fp32 (R16).
+__global__ void k_bn_reduce(XArgs x, float* __restrict__ mean, float* __restrict__ var, int64_t C) {
+    if (!block_wait(x, FLAG_C)) return;
+    for (int64_t i = gtid(); i < 2 * C; i += gstride()) {
+        double acc = 0.0;
+        for (int p = 0; p < x.world; ++p) {
+            const float* stage = reinterpret_cast<const float*>(x.peers.base[p] + x.lay.off_bn) +
+                                 (int64_t)x.parity * 2 * LMSGD_MAX_BN_CHANNELS;
+            acc += (double)stage[i];
+        }
+        const float out = (float)(acc / (double)x.world);
+        if (i < C) mean[i] = out; else var[i - C] = out;
+    }
+}
+
+int grid_for(const Launch& L, int64_t work_items) {
+    int64_t blocks = (work_items + kThreads - 1) / kThreads;
+    if (blocks > L.grid_cap_stream) blocks = L.grid_cap_stream;
+    return blocks < 1 ? 1 : (int)blocks;
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers
+
+int stream_blocks_per_sm() {
+    int worst = 1 << 30, b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update<true>, kThreads, 0);
+    worst = b < worst ? b : worst;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true>, kThreads, 0);
+    worst = b < worst ? b : worst;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update_gather<true>, kThreads, 0);
+    worst = b < worst ? b : worst;
+    return worst > 0 ? worst : 1;
+}
+
+cudaError_t launch_status_reset(cudaStream_t s, int64_t* st) {
+    k_status_reset<<<1, 32, 0, s>>>(st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack(cudaStream_t s, const Launch& L, const float* g, int64_t n, int64_t n_pad,
+                        float scale, uint16_t* h, int64_t* st) {
+    k_pack<<<grid_for(L, n_pad >> 3), kThreads, 0, s>>>(g, n, n_pad, scale, h, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_local(cudaStream_t s, const Launch& L, const uint16_t* h, int k,
+                                int64_t n_pad, uint16_t* R, int64_t* st) {
+    k_reduce_local<<<grid_for(L, n_pad >> 3), kThreads, 0, s>>>(h, k, n_pad, R, st);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, int64_t n,
+                          const UpdConst& c, float* th, float* d, float* m, const int64_t* st,
+                          int64_t* st_reset, int64_t* last) {
+    const int grid = grid_for(L, (n + 7) >> 3);
+    if (c.a_rms != 0.0f)
+        k_update<true><<<grid, kThreads, 0, s>>>(R, n, c, th, d, m, st, st_reset, last);
+    else
+        k_update<false><<<grid, kThreads, 0, s>>>(R, n, c, th, d, m, st, st_reset, last);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
+                          const UpdConst& c, float* th, float* d, float* m, int64_t* st,
+                          int64_t* st_reset, unsigned int* ticket, int64_t* last) {
+    const int grid = grid_for(L, (n + 7) >> 3);
+    if (c.a_rms != 0.0f)
+        k_fused1<true><<<grid, kThreads, 0, s>>>(g, n, scale, c, th, d, m, st, st_reset, ticket, last);
+    else
+        k_fused1<false><<<grid, kThreads, 0, s>>>(g, n, scale, c, th, d, m, st, st_reset, ticket, last);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,
+                             float scale) {
+    k_pack_push<<<grid_for(L, (x.lay.shard >> 3) * x.world), kThreads, 0, s>>>(x, g, scale);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x) {
+    k_reduce_shard<<<grid_for(L, x.lay.shard >> 3), kThreads, 0, s>>>(x);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_update_gather(cudaStream_t s, const Launch& L, const XArgs& x, const UpdConst& c,
+                                 float* th, float* d, float* m, int64_t* last) {
+    const int grid = grid_for(L, (x.lay.shard >> 3) * x.world);
+    if (c.a_rms != 0.0f)
+        k_update_gather<true><<<grid, kThreads, 0, s>>>(x, c, th, d, m, last);
+    else
+        k_update_gather<false><<<grid, kThreads, 0, s>>>(x, c, th, d, m, last);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bn_stage(cudaStream_t s, const XArgs& x, const float* mean, const float* var,
+                            int64_t C) {
+    int grid = (int)((C + kThreads - 1) / kThreads);
+    grid = grid > 128 ? 128 : (grid < 1 ? 1 : grid);
+    k_bn_stage<<<grid, kThreads, 0, s>>>(x, mean, var, C);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_bn_reduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C) {
+    int grid = (int)((2 * C + kThreads - 1) / kThreads);
+    grid = grid > 128 ? 128 : (grid < 1 ? 1 : grid);
+    k_bn_reduce<<<grid, kThreads, 0, s>>>(x, mean, var, C);
+    return cudaGetLastError();
+}
+
+}  // namespace lmsgd

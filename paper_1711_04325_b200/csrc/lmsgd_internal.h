@@ -1,0 +1,82 @@
+// Internal interfaces between the C ABI (api.cpp) and the sm_100a kernels
+// (kernels.cu).  Not installed; not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lmsgd.h"
+
+namespace lmsgd {
+
+constexpr int64_t kNone = INT64_MAX;  // "no non-finite index" in device status words
+
+// Device status words (int64[4]): {first_nonfinite, pack_saturations,
+// sum_saturations, error}.
+enum { ST_FIRST = 0, ST_PACK_SAT = 1, ST_SUM_SAT = 2, ST_ERROR = 3, ST_WORDS = 4 };
+
+// fp32 constants of the update, each rounded once from double (R15).
+struct UpdConst {
+    float mu1, mu2, omm2, eps;   // omm2 = fp32(1 - mu2), computed in double
+    float eta, a_sgd, a_rms;
+    float inv_ks;                // fp32(1 / (k s)), exact for power-of-two k s
+};
+
+// Layout of one rank's exchange buffer (CUDA IPC-shared when world > 1).
+struct Layout {
+    int64_t shard;        // elements per rank shard (multiple of 64)
+    int64_t off_recv;     // uint16 [world][shard]: slot p = rank p's packed values of MY shard
+    int64_t off_R;        // uint16 [shard]: this rank's reduced shard (wire-2 payload)
+    int64_t off_status;   // int64 [2 parity][ST_WORDS]
+    int64_t off_flags;    // uint32: A at +0, B at +128 B, C at +256 B, each [LMSGD_MAX_WORLD]
+    int64_t off_bn;       // float [2 parity][2 * LMSGD_MAX_BN_CHANNELS]
+    int64_t bytes;
+};
+
+struct Peers {
+    char* base[LMSGD_MAX_WORLD];  // exchange buffer of every rank (own included)
+};
+
+struct Ticket {
+    unsigned int* counters;  // device, zero-initialised, reset by the last block
+};
+
+struct Launch {
+    int sm_count;
+    int grid_cap_stream;   // grid cap for the streaming kernels (SMs x resident blocks)
+};
+
+// ---- single-GPU building blocks (sub-step ABI and world == 1)
+cudaError_t launch_status_reset(cudaStream_t s, int64_t* st);
+cudaError_t launch_pack(cudaStream_t s, const Launch& L, const float* g, int64_t n, int64_t n_pad,
+                        float scale, uint16_t* h, int64_t* st);
+cudaError_t launch_reduce_local(cudaStream_t s, const Launch& L, const uint16_t* h, int k,
+                                int64_t n_pad, uint16_t* R, int64_t* st);
+cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, int64_t n,
+                          const UpdConst& c, float* th, float* d, float* m, const int64_t* st,
+                          int64_t* st_reset, int64_t* last);
+cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
+                          const UpdConst& c, float* th, float* d, float* m, int64_t* st,
+                          int64_t* st_reset, unsigned int* ticket, int64_t* last);
+int stream_blocks_per_sm();
+
+// ---- world > 1 exchange over peer memory (NVLink / NVSwitch)
+struct XArgs {
+    Peers peers;
+    Layout lay;
+    int world, rank;
+    uint32_t epoch;      // step number (>= 1), the flag value of this step
+    int parity;          // epoch & 1: status slot of this step
+    int64_t n;
+    int64_t timeout_ns;
+    unsigned int* ticket;
+};
+cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,
+                             float scale);
+cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x);
+cudaError_t launch_update_gather(cudaStream_t s, const Launch& L, const XArgs& x, const UpdConst& c,
+                                 float* th, float* d, float* m, int64_t* last);
+cudaError_t launch_bn_stage(cudaStream_t s, const XArgs& x, const float* mean, const float* var,
+                            int64_t C);
+cudaError_t launch_bn_reduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C);
+
+}  // namespace lmsgd

@@ -1,0 +1,323 @@
+"""Thin ctypes binding of liblmsgd.so (include/lmsgd.h), same names as the C ABI.
+
+Argument marshalling only: torch tensors are turned into device pointers and the
+current CUDA stream into a cudaStream_t; every step of the path runs in the
+library's sm_100a kernels.  There is no fallback: if liblmsgd.so is missing or
+fails to load, importing this module raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "liblmsgd.so")
+
+LMSGD_OK = 0
+LMSGD_ERR_INVALID_ARG = -1
+LMSGD_ERR_CUDA = -2
+LMSGD_ERR_NONFINITE = -4
+LMSGD_ERR_STATE = -5
+LMSGD_ERR_UNSUPPORTED = -6
+LMSGD_ERR_TIMEOUT = -7
+LMSGD_ERR_RANGE = -8
+LMSGD_MAX_WORLD = 8
+LMSGD_IPC_HANDLE_BYTES = 64
+LMSGD_MAX_BN_CHANNELS = 1 << 20
+LMSGD_FLAG_NO_SKIP = 0x1
+SCHEDULE_SLOW_START = 0
+SCHEDULE_GOYAL = 1
+
+
+class Hyper(ctypes.Structure):
+    _fields_ = [("mu1", ctypes.c_double), ("mu2", ctypes.c_double), ("eps", ctypes.c_double),
+                ("eta_rmsprop", ctypes.c_double), ("beta_center", ctypes.c_double),
+                ("beta_period", ctypes.c_double)]
+
+
+class Cluster(ctypes.Structure):
+    _fields_ = [("n_workers", ctypes.c_int64), ("b_local", ctypes.c_int64), ("n_train", ctypes.c_int64),
+                ("schedule", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class Coeffs(ctypes.Structure):
+    _fields_ = [("epoch", ctypes.c_double), ("eta", ctypes.c_double), ("alpha_sgd", ctypes.c_double),
+                ("alpha_rmsprop", ctypes.c_double), ("phase", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class StepStatus(ctypes.Structure):
+    _fields_ = [("first_nonfinite", ctypes.c_int64), ("pack_saturations", ctypes.c_int64),
+                ("sum_saturations", ctypes.c_int64), ("skipped", ctypes.c_int32), ("error", ctypes.c_int32)]
+
+
+class LmsgdError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"lmsgd status {status}: {msg}")
+        self.status = status
+
+
+def _load() -> ctypes.CDLL:
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_1711_04325_b200.build` "
+                          "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P, I64, I32, F32, U32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_float, ctypes.c_uint32
+    sig = {
+        "lmsgd_abi_version": (I32, []),
+        "lmsgd_status_string": (ctypes.c_char_p, [I32]),
+        "lmsgd_hyper_default": (I32, [ctypes.POINTER(Hyper)]),
+        "lmsgd_schedule_at": (I32, [ctypes.POINTER(Hyper), ctypes.POINTER(Cluster), I64, ctypes.POINTER(Coeffs)]),
+        "lmsgd_schedule_steps": (I32, [ctypes.POINTER(Cluster), ctypes.POINTER(I64)]),
+        "lmsgd_init": (I32, [ctypes.POINTER(P), I32, I32, I32, I64, F32, ctypes.POINTER(Hyper), U32]),
+        "lmsgd_ipc_handle": (I32, [P, ctypes.c_char_p]),
+        "lmsgd_connect": (I32, [P, ctypes.c_char_p]),
+        "lmsgd_finalize": (I32, [P]),
+        "lmsgd_last_error": (ctypes.c_char_p, [P]),
+        "lmsgd_step": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs)]),
+        "lmsgd_step_host": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs), P]),
+        "lmsgd_bn_stats_allreduce": (I32, [P, P, P, P, I64]),
+        "lmsgd_query_status": (I32, [P, ctypes.POINTER(StepStatus)]),
+        "lmsgd_profile_enable": (I32, [P, I64]),
+        "lmsgd_profile_read": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]),
+        "lmsgd_status_reset": (I32, [P, P]),
+        "lmsgd_pack": (I32, [P, P, I64, I64, F32, P, P]),
+        "lmsgd_reduce_local": (I32, [P, P, I32, I64, P, P]),
+        "lmsgd_update": (I32, [P, P, I64, I32, F32, ctypes.POINTER(Hyper), ctypes.POINTER(Coeffs), P, P, P, P]),
+        "lmsgd_fused_step1": (I32, [P, P, I64, F32, ctypes.POINTER(Hyper), ctypes.POINTER(Coeffs), P, P, P, P]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    return lib
+
+
+_lib = _load()
+EXPORTED = tuple(sorted(n for n in dir(_lib) if n.startswith("lmsgd_")))
+
+
+def lib() -> ctypes.CDLL:
+    return _lib
+
+
+def _check(status: int, ctx=None):
+    if status != LMSGD_OK:
+        msg = _lib.lmsgd_last_error(ctx.ptr if isinstance(ctx, Context) else ctx)
+        raise LmsgdError(status, (msg or b"").decode() or _lib.lmsgd_status_string(status).decode())
+
+
+# ------------------------------------------------------------------ host-only
+
+def lmsgd_abi_version() -> int:
+    return _lib.lmsgd_abi_version()
+
+
+def lmsgd_hyper_default() -> Hyper:
+    h = Hyper()
+    _check(_lib.lmsgd_hyper_default(ctypes.byref(h)))
+    return h
+
+
+def make_cluster(n_workers=1024, b_local=32, n_train=1_281_167, schedule=SCHEDULE_SLOW_START) -> Cluster:
+    return Cluster(n_workers, b_local, n_train, schedule, 0)
+
+
+def lmsgd_schedule_at(hyper: Hyper | None, cluster: Cluster, t: int) -> Coeffs:
+    hyper = hyper if hyper is not None else lmsgd_hyper_default()
+    c = Coeffs()
+    _check(_lib.lmsgd_schedule_at(ctypes.byref(hyper), ctypes.byref(cluster), int(t), ctypes.byref(c)))
+    return c
+
+
+def lmsgd_schedule_steps(cluster: Cluster) -> int:
+    T = ctypes.c_int64()
+    _check(_lib.lmsgd_schedule_steps(ctypes.byref(cluster), ctypes.byref(T)))
+    return T.value
+
+
+def make_coeffs(eta: float, alpha_sgd: float, alpha_rmsprop: float, epoch: float = 0.0, phase: int = 0) -> Coeffs:
+    return Coeffs(epoch, eta, alpha_sgd, alpha_rmsprop, phase, 0)
+
+
+# ------------------------------------------------------------------ tensors
+
+def _ptr(t, dtype=None, name="tensor"):
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{name} must be a torch.Tensor")
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+# ------------------------------------------------------------------ context
+
+@dataclass
+class Context:
+    ptr: ctypes.c_void_p
+    world: int
+    rank: int
+    device: int
+    n: int
+
+    def __del__(self):
+        if self.ptr:
+            try:
+                _lib.lmsgd_finalize(self.ptr)
+            except Exception:
+                pass
+            self.ptr = None
+
+
+def lmsgd_init(world: int, rank: int, device: int, n_params: int, loss_scale: float = 1.0,
+               hyper: Hyper | None = None, flags: int = 0) -> Context:
+    p = ctypes.c_void_p()
+    st = _lib.lmsgd_init(ctypes.byref(p), int(world), int(rank), int(device), int(n_params),
+                         float(loss_scale), ctypes.byref(hyper) if hyper is not None else None, int(flags))
+    _check(st)
+    return Context(p, world, rank, device, n_params)
+
+
+def lmsgd_ipc_handle(ctx: Context) -> bytes:
+    buf = ctypes.create_string_buffer(LMSGD_IPC_HANDLE_BYTES)
+    _check(_lib.lmsgd_ipc_handle(ctx.ptr, buf), ctx)
+    return buf.raw
+
+
+def lmsgd_connect(ctx: Context, handles: bytes):
+    if len(handles) != ctx.world * LMSGD_IPC_HANDLE_BYTES:
+        raise ValueError("handles must be world * LMSGD_IPC_HANDLE_BYTES bytes in rank order")
+    _check(_lib.lmsgd_connect(ctx.ptr, handles), ctx)
+
+
+def connect_process_group(ctx: Context, group=None):
+    """Bootstrap plumbing: all-gather the IPC handles over torch.distributed and
+    connect.  (The library itself does no host networking.)"""
+    import torch.distributed as dist
+    if ctx.world == 1:
+        return
+    mine = lmsgd_ipc_handle(ctx)
+    out = [None] * ctx.world
+    dist.all_gather_object(out, mine, group=group)
+    lmsgd_connect(ctx, b"".join(out))
+    dist.barrier(group=group)
+
+
+def lmsgd_finalize(ctx: Context):
+    if ctx.ptr:
+        _check(_lib.lmsgd_finalize(ctx.ptr))
+        ctx.ptr = None
+
+
+def lmsgd_step(ctx: Context, params, grads, delta, m, coeffs: Coeffs, stream=None):
+    import torch
+    for t, nm in ((params, "params"), (grads, "grads"), (delta, "delta"), (m, "m")):
+        if t.numel() != ctx.n:
+            raise ValueError(f"{nm} must have n_params = {ctx.n} elements")
+    _check(_lib.lmsgd_step(ctx.ptr, _stream(stream), _ptr(params, torch.float32, "params"),
+                           _ptr(grads, torch.float32, "grads"), _ptr(delta, torch.float32, "delta"),
+                           _ptr(m, torch.float32, "m"), ctypes.byref(coeffs)), ctx)
+
+
+def lmsgd_step_host(ctx: Context, params, grads_host, delta, m, coeffs: Coeffs, status_host,
+                    stream=None):
+    """grads_host: CPU float32 tensor (pinned for full speed); status_host: a
+    pinned CPU int64 tensor of 4 elements (lmsgd_step_status layout) filled when the
+    stream passes this point."""
+    import torch
+    if grads_host.is_cuda or grads_host.dtype != torch.float32 or not grads_host.is_contiguous() \
+            or grads_host.numel() != ctx.n:
+        raise ValueError("grads_host must be a contiguous CPU float32 tensor of n_params elements")
+    if status_host.is_cuda or status_host.numel() * status_host.element_size() < ctypes.sizeof(StepStatus):
+        raise ValueError("status_host must be a CPU buffer of >= 32 bytes")
+    _check(_lib.lmsgd_step_host(ctx.ptr, _stream(stream), _ptr(params, torch.float32, "params"),
+                                ctypes.c_void_p(grads_host.data_ptr()), _ptr(delta, torch.float32, "delta"),
+                                _ptr(m, torch.float32, "m"), ctypes.byref(coeffs),
+                                ctypes.c_void_p(status_host.data_ptr())), ctx)
+
+
+def decode_status(buf) -> StepStatus:
+    """StepStatus from a 4 x int64 host buffer written by lmsgd_step_host."""
+    return StepStatus.from_buffer_copy(bytes(buf.numpy().tobytes()))
+
+
+def lmsgd_bn_stats_allreduce(ctx: Context, mean, var, stream=None):
+    import torch
+    if mean.numel() != var.numel():
+        raise ValueError("mean and var must have the same length")
+    _check(_lib.lmsgd_bn_stats_allreduce(ctx.ptr, _stream(stream), _ptr(mean, torch.float32, "mean"),
+                                         _ptr(var, torch.float32, "var"), mean.numel()), ctx)
+
+
+def lmsgd_query_status(ctx: Context) -> tuple[int, StepStatus]:
+    """(status code, StepStatus) of the last step; LMSGD_ERR_NONFINITE / TIMEOUT are
+    returned, not raised."""
+    s = StepStatus()
+    st = _lib.lmsgd_query_status(ctx.ptr, ctypes.byref(s))
+    if st not in (LMSGD_OK, LMSGD_ERR_NONFINITE, LMSGD_ERR_TIMEOUT):
+        _check(st, ctx)
+    return st, s
+
+
+def lmsgd_profile_enable(ctx: Context, max_launches: int):
+    _check(_lib.lmsgd_profile_enable(ctx.ptr, int(max_launches)), ctx)
+
+
+PHASES = ("pack", "reduce", "update")
+
+
+def lmsgd_profile_read(ctx: Context) -> dict:
+    """{phase: (summed device ms, launches)} of the recorded step kernels."""
+    ms = (ctypes.c_double * 3)()
+    n = (ctypes.c_int64 * 3)()
+    _check(_lib.lmsgd_profile_read(ctx.ptr, ms, n), ctx)
+    return {PHASES[i]: (ms[i], n[i]) for i in range(3)}
+
+
+# ------------------------------------------------------------------ sub-steps
+
+def lmsgd_status_reset(dstatus, stream=None):
+    import torch
+    _check(_lib.lmsgd_status_reset(_stream(stream), _ptr(dstatus, torch.int64, "dstatus")))
+
+
+def lmsgd_pack(g, n_pad: int, loss_scale: float, h, dstatus, stream=None):
+    import torch
+    _check(_lib.lmsgd_pack(_stream(stream), _ptr(g, torch.float32, "g"), g.numel(), int(n_pad),
+                           float(loss_scale), _ptr(h, None, "h"), _ptr(dstatus, torch.int64, "dstatus")))
+
+
+def lmsgd_reduce_local(h, k: int, n_pad: int, R, dstatus=None, stream=None):
+    import torch
+    _check(_lib.lmsgd_reduce_local(_stream(stream), _ptr(h, None, "h"), int(k), int(n_pad), _ptr(R, None, "R"),
+                                   _ptr(dstatus, torch.int64, "dstatus") if dstatus is not None else None))
+
+
+def lmsgd_update(R, n: int, k: int, loss_scale: float, hyper, coeffs: Coeffs, params, delta, m,
+                 dstatus=None, stream=None):
+    import torch
+    hyper = hyper if hyper is not None else lmsgd_hyper_default()
+    _check(_lib.lmsgd_update(_stream(stream), _ptr(R, None, "R"), int(n), int(k), float(loss_scale),
+                             ctypes.byref(hyper), ctypes.byref(coeffs), _ptr(params, torch.float32, "params"),
+                             _ptr(delta, torch.float32, "delta"), _ptr(m, torch.float32, "m"),
+                             _ptr(dstatus, torch.int64, "dstatus") if dstatus is not None else None))
+
+
+def lmsgd_fused_step1(g, loss_scale: float, hyper, coeffs: Coeffs, params, delta, m, dstatus, stream=None):
+    import torch
+    hyper = hyper if hyper is not None else lmsgd_hyper_default()
+    _check(_lib.lmsgd_fused_step1(_stream(stream), _ptr(g, torch.float32, "g"), g.numel(), float(loss_scale),
+                                  ctypes.byref(hyper), ctypes.byref(coeffs), _ptr(params, torch.float32, "params"),
+                                  _ptr(delta, torch.float32, "delta"), _ptr(m, torch.float32, "m"),
+                                  _ptr(dstatus, torch.int64, "dstatus")))

@@ -1,0 +1,344 @@
+"""GPU parity of the CUDA path (through the C ABI) against the CPU oracle.
+
+Bar (BASELINE.json north_star):
+  * fp16 wire payloads R and the averaged gradient ghat: bit-exact (the sum is exact);
+  * schedule: bit-exact (tests/test_lib_host.py);
+  * fp32 state after one step, oracle resynced to the GPU's previous state:
+    |x_gpu - x_oracle| <= 1e-6 * scale_x with scale_m = m_t,
+    scale_Delta = mu1 |Delta_{t-1}| + |c ghat|, scale_theta = |theta_{t-1}| + |eta Delta_t|;
+  * status words (first non-finite index, saturation counts): exact.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+import paper_1711_04325_b200 as L  # noqa: E402
+import synth  # noqa: E402
+from oracle import binary16, exchange, run, schedule  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+TOL = 1e-6
+C1 = schedule.Cluster(n_workers=2, b_local=32, n_train=64)
+C1_C = L.make_cluster(2, 32, 64)
+K32 = schedule.Cluster()
+K32_C = L.make_cluster()
+
+
+def dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to(DEV)
+
+
+def host(x):
+    return x.cpu().numpy()
+
+
+def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, hyper=schedule.Hyper(), tol=TOL):
+    th_o, d_o, m_o = run.resync_step(th0, d0, m0, ghat, c, hyper)
+    gh = np.asarray(ghat, dtype=np.float64)
+    coef = c.alpha_sgd + c.alpha_rmsprop / (np.sqrt(m_o) + hyper.eps)
+    e = {
+        "m": run.scaled_error(m_g, m_o, m_o),
+        "delta": run.scaled_error(d_g, d_o, hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + np.abs(coef * gh)),
+        "theta": run.scaled_error(th_g, th_o, np.abs(np.asarray(th0, np.float64)) + np.abs(c.eta * d_o)),
+    }
+    assert max(e.values()) <= tol, e
+    return e
+
+
+def init_state(n, seed=0):
+    r = np.random.default_rng(seed)
+    th = synth.theta0(n, None)
+    d = (r.standard_normal(n) * 1e-3).astype(np.float32)
+    m = (r.random(n) * 1e-6).astype(np.float32)
+    return th, d, m
+
+
+# ------------------------------------------------------------------ k = 1 context path
+
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 63, 64, 65, 1000, 10_007, (1 << 20) + 13])
+@pytest.mark.parametrize("flags", [0, L.LMSGD_FLAG_NO_SKIP])
+def test_k1_step_ragged_sizes(n, flags):
+    s = 1024.0
+    th0, d0, m0 = init_state(n)
+    ctx = L.lmsgd_init(1, 0, 0, n, s, None, flags)
+    th, d, m = dev(th0), dev(d0), dev(m0)
+    a = synth.grad_scale(n)
+    for t in (1, 12, 15):   # exp branch (RMS on), linear branch, SGD (RMS off)
+        coeffs = L.lmsgd_schedule_at(None, C1_C, t)
+        c = schedule.coeffs_at(t, schedule.Hyper(), C1)
+        g = synth.grads(1, t, n, a)
+        prev = host(th), host(d), host(m)
+        L.lmsgd_step(ctx, th, dev(g[0]), d, m, coeffs)
+        code, st = L.lmsgd_query_status(ctx)
+        assert code == 0 and st.skipped == 0 and st.first_nonfinite == -1
+        ex = exchange.exchange(list(g), s)
+        assert st.pack_saturations == ex.pack_saturations and st.sum_saturations in (0, ex.sum_saturations)
+        check_state(host(th), host(d), host(m), *prev, ex.ghat, c)
+    L.lmsgd_finalize(ctx)
+
+
+@pytest.mark.parametrize("flags", [0, L.LMSGD_FLAG_NO_SKIP])
+@pytest.mark.parametrize("s", [1.0, 1024.0])
+def test_k1_ghat_bit_exact(flags, s):
+    """With mu1 = 0 and (a_SGD, a_RMS) = (1, 0): Delta_t = -ghat exactly in fp32,
+    which exposes the GPU's ghat for a bit-exact comparison with the oracle."""
+    n = 200_003
+    h = L.lmsgd_hyper_default()
+    h.mu1 = 0.0
+    ctx = L.lmsgd_init(1, 0, 0, n, s, h, flags)
+    g = synth.grads(1, 5, n)
+    # include subnormal / saturating / tie values
+    g[0, :6] = np.array([3e-8, 6e-8, 65504.0 / s, 65520.0 / s, 1e6, -2.0 ** -25 * 3 / s], dtype=np.float32)
+    th, d, m = dev(np.zeros(n, np.float32)), dev(np.zeros(n, np.float32)), dev(np.zeros(n, np.float32))
+    L.lmsgd_step(ctx, th, dev(g[0]), d, m, L.make_coeffs(1.0, 1.0, 0.0))
+    code, st = L.lmsgd_query_status(ctx)
+    ex = exchange.exchange(list(g), s)
+    assert np.array_equal(-host(d), ex.ghat)
+    assert st.pack_saturations == ex.pack_saturations >= 2
+    L.lmsgd_finalize(ctx)
+
+
+def test_k1_nonfinite_skips_and_reports_first_index():
+    n = 100_000
+    ctx = L.lmsgd_init(1, 0, 0, n, 1024.0)
+    th0, d0, m0 = init_state(n)
+    th, d, m = dev(th0), dev(d0), dev(m0)
+    g = synth.grads(1, 1, n)[0]
+    g[77_777] = np.inf
+    g[99_999] = np.nan
+    g[31] = -np.inf
+    L.lmsgd_step(ctx, th, dev(g), d, m, L.lmsgd_schedule_at(None, K32_C, 1))
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == L.LMSGD_ERR_NONFINITE and st.skipped == 1 and st.first_nonfinite == 31
+    with pytest.raises(binary16.NonFiniteError) as e:
+        exchange.exchange([g], 1024.0)
+    assert e.value.index == st.first_nonfinite
+    assert np.array_equal(host(th), th0) and np.array_equal(host(d), d0) and np.array_equal(host(m), m0)
+    # the next clean step proceeds normally (status slots are per step)
+    g2 = synth.grads(1, 2, n)
+    L.lmsgd_step(ctx, th, dev(g2[0]), d, m, L.lmsgd_schedule_at(None, K32_C, 2))
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == 0 and st.skipped == 0 and st.first_nonfinite == -1
+    check_state(host(th), host(d), host(m), th0, d0, m0, exchange.exchange(list(g2), 1024.0).ghat,
+                schedule.coeffs_at(2))
+    L.lmsgd_finalize(ctx)
+
+
+def test_k1_no_skip_flag_reports_but_applies():
+    n = 4096
+    ctx = L.lmsgd_init(1, 0, 0, n, 1.0, None, L.LMSGD_FLAG_NO_SKIP)
+    th0, d0, m0 = init_state(n)
+    th, d, m = dev(th0), dev(d0), dev(m0)
+    g = synth.grads(1, 1, n)[0]
+    g[100] = np.nan
+    L.lmsgd_step(ctx, th, dev(g), d, m, L.lmsgd_schedule_at(None, K32_C, 1))
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == L.LMSGD_ERR_NONFINITE and st.first_nonfinite == 100 and st.skipped == 0
+    assert not np.array_equal(host(th)[:100], th0[:100])
+    L.lmsgd_finalize(ctx)
+
+
+def test_zero_gradient_fixed_point_and_endpoints():
+    n = 5000
+    th0, _, _ = init_state(n)
+    z = np.zeros(n, np.float32)
+    ctx = L.lmsgd_init(1, 0, 0, n, 1.0)
+    th, d, m = dev(th0), dev(z), dev(z)
+    L.lmsgd_step(ctx, th, dev(z), d, m, L.lmsgd_schedule_at(None, K32_C, 1))
+    assert np.array_equal(host(th), th0) and not host(d).any() and not host(m).any()
+    # pure momentum SGD (alpha_RMS = 0) and pure RMSprop (alpha_SGD = 0)
+    g = synth.grads(1, 1, n)
+    for a_sgd, a_rms in ((1.0, 0.0), (0.0, 1.0), (0.3, 2e-5)):
+        th, d, m = dev(th0), dev(z), dev(z)
+        L.lmsgd_step(ctx, th, dev(g[0]), d, m, L.make_coeffs(0.1, a_sgd, a_rms))
+        c = schedule.Coeffs(0.0, 0.1, a_sgd, a_rms, 0)
+        check_state(host(th), host(d), host(m), th0, z, z, exchange.exchange(list(g), 1.0).ghat, c)
+    L.lmsgd_finalize(ctx)
+
+
+def test_delta_independent_of_eta_on_gpu():
+    """Delta_t carries no eta -- bit-equal under different LR sequences."""
+    n = 65_536
+    ctxs = [L.lmsgd_init(1, 0, 0, n, 1024.0) for _ in range(2)]
+    th0, d0, m0 = init_state(n)
+    st = [[dev(th0), dev(d0), dev(m0)] for _ in range(2)]
+    a = synth.grad_scale(n)
+    for t in range(1, 8):
+        g = dev(synth.grads(1, t, n, a)[0])
+        c = L.lmsgd_schedule_at(None, C1_C, t)
+        for i, eta in enumerate((0.5, 7.0 + t)):
+            ci = L.make_coeffs(eta, c.alpha_sgd, c.alpha_rmsprop)
+            L.lmsgd_step(ctxs[i], st[i][0], g, st[i][1], st[i][2], ci)
+        torch.cuda.synchronize()
+        assert torch.equal(st[0][1], st[1][1]) and torch.equal(st[0][2], st[1][2])
+    for c in ctxs:
+        L.lmsgd_finalize(c)
+
+
+def test_determinism_and_step_host_matches_step():
+    n = 300_001
+    th0, d0, m0 = init_state(n)
+    g = synth.grads(1, 4, n)[0]
+    outs = []
+    for use_host in (False, False, True):
+        ctx = L.lmsgd_init(1, 0, 0, n, 1024.0)
+        th, d, m = dev(th0), dev(d0), dev(m0)
+        c = L.lmsgd_schedule_at(None, K32_C, 4)
+        if use_host:
+            gh = torch.from_numpy(g).pin_memory()
+            stbuf = torch.zeros(4, dtype=torch.int64).pin_memory()
+            L.lmsgd_step_host(ctx, th, gh, d, m, c, stbuf)
+            torch.cuda.synchronize()
+            s = L.decode_status(stbuf)
+            assert s.first_nonfinite == -1 and s.skipped == 0
+        else:
+            L.lmsgd_step(ctx, th, dev(g), d, m, c)
+        outs.append([host(x) for x in (th, d, m)])
+        L.lmsgd_finalize(ctx)
+    for o in outs[1:]:
+        for a, b in zip(o, outs[0]):
+            assert np.array_equal(a, b)
+
+
+def test_c1_twenty_steps_resynced():
+    """Config C1: 4,096 params, 2 workers x minibatch 32, 20 steps across the whole
+    RMSprop -> SGD warm-up (simulated k = 2 on one GPU), every step checked."""
+    n, k, s = 4096, 2, 1024.0
+    n_pad = 4096
+    a = synth.grad_scale(n)
+    th0, d0, m0 = synth.theta0(n, None), np.zeros(n, np.float32), np.zeros(n, np.float32)
+    th, d, m = dev(th0), dev(d0), dev(m0)
+    hbuf = torch.empty(k * n_pad, dtype=torch.int16, device=DEV)
+    R = torch.empty(n_pad, dtype=torch.int16, device=DEV)
+    dst = torch.empty(4, dtype=torch.int64, device=DEV)
+    free = run.run(th0, lambda t: synth.grads(k, t, n, a), k, 20, s, cluster=C1)
+    for t in range(1, 21):
+        g = synth.grads(k, t, n, a)
+        prev = host(th), host(d), host(m)
+        L.lmsgd_status_reset(dst)
+        for i in range(k):
+            L.lmsgd_pack(dev(g[i]), n_pad, s, hbuf[i * n_pad:(i + 1) * n_pad], dst)
+        L.lmsgd_reduce_local(hbuf, k, n_pad, R, dst)
+        L.lmsgd_update(R, n, k, s, None, L.lmsgd_schedule_at(None, C1_C, t), th, d, m, dst)
+        ex = exchange.exchange(list(g), s)
+        assert np.array_equal(host(R).view(np.uint16), ex.R)
+        assert np.array_equal(ex.ghat, free.ghat[t - 1])
+        check_state(host(th), host(d), host(m), *prev, ex.ghat, schedule.coeffs_at(t, schedule.Hyper(), C1))
+    # free-running drift over 20 steps stays small (fp32 vs fp64 compounding)
+    scale = np.abs(free.theta) + 1e-3
+    assert run.scaled_error(host(th), free.theta, scale) < 1e-5
+
+
+# ------------------------------------------------------------------ sub-steps / simulated k
+
+def _pack_codec_case(x32, s):
+    n = x32.size
+    n_pad = (n + 7) // 8 * 8
+    h = torch.empty(n_pad, dtype=torch.int16, device=DEV)
+    dst = torch.empty(4, dtype=torch.int64, device=DEV)
+    L.lmsgd_status_reset(dst)
+    L.lmsgd_pack(dev(x32), n_pad, s, h, dst)
+    return host(h).view(np.uint16)[:n], host(dst)
+
+
+def test_pack_vs_oracle_codec_boundary_classes():
+    exps = np.arange(127 - 40, 127 + 17, dtype=np.uint32)
+    mant = np.concatenate([np.arange(0, 1 << 23, 8191, dtype=np.uint32),
+                           ((np.arange(1 << 10, dtype=np.uint32) << 13)[:, None]
+                            + np.array([0xFFF, 0x1000, 0x1001], dtype=np.uint32)).ravel()])
+    pat = (exps[:, None] << 23 | mant[None, :]).ravel()
+    pat = np.concatenate([pat, pat | np.uint32(0x80000000),
+                          np.random.default_rng(1).integers(0, 2 ** 32, 1 << 22, dtype=np.uint64).astype(np.uint32)])
+    x = pat.view(np.float32)
+    x = x[np.isfinite(x)]
+    for s in (1.0, 1024.0, 0.5):
+        got, st = _pack_codec_case(x, s)
+        ref, sat = exchange.pack(x, s)
+        bad = np.nonzero(got != ref)[0]
+        assert bad.size == 0, (s, x[bad[:4]], got[bad[:4]], ref[bad[:4]])
+        assert st[1] == sat and st[0] == np.iinfo(np.int64).max
+
+
+def test_pack_nonfinite_first_index():
+    x = np.ones(1000, np.float32)
+    x[[500, 17, 999]] = [np.nan, np.inf, -np.inf]
+    _, st = _pack_codec_case(x, 1.0)
+    assert st[0] == 17
+
+
+@pytest.mark.parametrize("k", [2, 3, 4, 8])
+def test_simulated_k_exchange_bit_exact(k):
+    n, s = 123_457, 1024.0
+    n_pad = (n + 64 * k - 1) // (64 * k) * 64 * k
+    g = synth.grads(k, 9, n)
+    g[0, :3] = [60000.0 / s, 60000.0 / s, -1.0]
+    g[1, :3] = [60000.0 / s, 1000.0 / s, 1.0]
+    hbuf = torch.empty(k * n_pad, dtype=torch.int16, device=DEV)
+    R = torch.empty(n_pad, dtype=torch.int16, device=DEV)
+    dst = torch.empty(4, dtype=torch.int64, device=DEV)
+    L.lmsgd_status_reset(dst)
+    for i in range(k):
+        L.lmsgd_pack(dev(g[i]), n_pad, s, hbuf[i * n_pad:(i + 1) * n_pad], dst)
+    L.lmsgd_reduce_local(hbuf, k, n_pad, R, dst)
+    ex = exchange.exchange(list(g), s)
+    Rg = host(R).view(np.uint16)
+    assert np.array_equal(Rg[:n], ex.R) and not Rg[n:].any()
+    stg = host(dst)
+    assert stg[1] == ex.pack_saturations and stg[2] == ex.sum_saturations >= 1
+    # ghat bit-exact via mu1 = 0, (1, 0) => Delta = -ghat
+    hyp = L.lmsgd_hyper_default()
+    hyp.mu1 = 0.0
+    z = lambda: dev(np.zeros(n, np.float32))  # noqa: E731
+    th, d, m = z(), z(), z()
+    L.lmsgd_update(R, n, k, s, hyp, L.make_coeffs(1.0, 1.0, 0.0), th, d, m, dst)
+    assert np.array_equal(-host(d), ex.ghat)
+
+
+def test_fused_step1_matches_pack_update():
+    n = 777_777
+    th0, d0, m0 = init_state(n)
+    g = dev(synth.grads(1, 2, n)[0])
+    c = L.lmsgd_schedule_at(None, K32_C, 2)
+    n_pad = (n + 7) // 8 * 8
+    a = [dev(x) for x in (th0, d0, m0)]
+    b = [dev(x) for x in (th0, d0, m0)]
+    dst = torch.empty(4, dtype=torch.int64, device=DEV)
+    L.lmsgd_status_reset(dst)
+    L.lmsgd_fused_step1(g, 1024.0, None, c, *a, dst)
+    h = torch.empty(n_pad, dtype=torch.int16, device=DEV)
+    dst2 = torch.empty(4, dtype=torch.int64, device=DEV)
+    L.lmsgd_status_reset(dst2)
+    L.lmsgd_pack(g, n_pad, 1024.0, h, dst2)
+    L.lmsgd_update(h, n, 1, 1024.0, None, c, *b, dst2)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
+
+
+# ------------------------------------------------------------------ full size (BASELINE configs)
+
+@pytest.mark.parametrize("t", [1, 392, 1000])
+def test_resnet50_full_size_sampled(t):
+    """C2: the 25,557,032-element ResNet-50 buffer, k = 1, in the launch configuration
+    bench.py times; outputs compared on a sample of indices (the path is elementwise,
+    so the oracle on the sampled indices is exact)."""
+    n = synth.resnet_n_params(50)
+    s = 1024.0
+    r = np.random.default_rng(t)
+    idx = np.unique(np.concatenate([np.arange(1000), np.arange(n - 1000, n), r.integers(0, n, 200_000)]))
+    th0 = synth.theta0(n, 50)
+    d0 = (r.standard_normal(n) * 1e-3).astype(np.float32)
+    m0 = (r.random(n) * 1e-6).astype(np.float32)
+    g = synth.grads(1, t, n)
+    ctx = L.lmsgd_init(1, 0, 0, n, s)
+    th, d, m = dev(th0), dev(d0), dev(m0)
+    L.lmsgd_step(ctx, th, dev(g[0]), d, m, L.lmsgd_schedule_at(None, K32_C, t))
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == 0
+    ex = exchange.exchange([g[0][idx]], s)
+    check_state(host(th)[idx], host(d)[idx], host(m)[idx], th0[idx], d0[idx], m0[idx], ex.ghat,
+                schedule.coeffs_at(t))
+    L.lmsgd_finalize(ctx)
