@@ -127,6 +127,12 @@ lmsgd_status lmsgd_schedule_at(const lmsgd_hyper* hyper, const lmsgd_cluster* cl
 /* Number of iterations T the schedule covers (90 epochs). */
 lmsgd_status lmsgd_schedule_steps(const lmsgd_cluster* cluster, int64_t* T);
 
+/* Exchange layout for world ranks and n parameters (host-only): shard =
+ * ceil(n / world) rounded up to 64 elements (128 B of fp16), n_pad = world * shard.
+ * Rank r owns the reduction of elements [r shard, (r+1) shard); elements >= n are
+ * zero padding. */
+lmsgd_status lmsgd_layout(int world, int64_t n, int64_t* shard, int64_t* n_pad);
+
 /* ---------------------------------------------------------------- context */
 
 /* Create the context of rank `rank` of `world` (1..LMSGD_MAX_WORLD) on CUDA

@@ -201,6 +201,15 @@ const char* lmsgd_status_string(lmsgd_status s) {
     return "unknown status";
 }
 
+lmsgd_status lmsgd_layout(int world, int64_t n, int64_t* shard, int64_t* n_pad) {
+    if (world < 1 || world > LMSGD_MAX_WORLD || n < 1 || n > (int64_t(1) << 36) || !shard || !n_pad)
+        return fail(nullptr, LMSGD_ERR_INVALID_ARG, "layout: bad world, n or NULL output");
+    const Layout L = make_layout(world, n);
+    *shard = L.shard;
+    *n_pad = L.shard * world;
+    return LMSGD_OK;
+}
+
 const char* lmsgd_last_error(const lmsgd_ctx* ctx) { return ctx ? ctx->err.c_str() : g_err.c_str(); }
 
 lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_t n_params,
@@ -234,7 +243,11 @@ lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_
     auto bail = [&](lmsgd_status s) { c->connected = false; lmsgd_finalize(c); return s; };
     if ((e = cudaMalloc(&c->buf, c->lay.bytes)) != cudaSuccess) { g_err = "cudaMalloc exchange buffer"; return bail(LMSGD_ERR_CUDA); }
     if ((e = cudaMemset(c->buf, 0, c->lay.bytes)) != cudaSuccess) { g_err = "cudaMemset"; return bail(LMSGD_ERR_CUDA); }
-    const int64_t init_status[2 * lmsgd::ST_WORDS] = {lmsgd::kNone, 0, 0, 0, lmsgd::kNone, 0, 0, 0};
+    int64_t init_status[2 * lmsgd::ST_WORDS] = {};
+    for (int p = 0; p < 2; ++p) {
+        init_status[p * lmsgd::ST_WORDS + lmsgd::ST_FIRST] = lmsgd::kNone;
+        init_status[p * lmsgd::ST_WORDS + lmsgd::ST_G_FIRST] = lmsgd::kNone;
+    }
     if ((e = cudaMemcpy(c->buf + c->lay.off_status, init_status, sizeof init_status, cudaMemcpyHostToDevice)) != cudaSuccess) {
         g_err = "cudaMemcpy status"; return bail(LMSGD_ERR_CUDA);
     }

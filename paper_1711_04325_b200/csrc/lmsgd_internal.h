@@ -10,9 +10,12 @@ namespace lmsgd {
 
 constexpr int64_t kNone = INT64_MAX;  // "no non-finite index" in device status words
 
-// Device status words (int64[4]): {first_nonfinite, pack_saturations,
-// sum_saturations, error}.
-enum { ST_FIRST = 0, ST_PACK_SAT = 1, ST_SUM_SAT = 2, ST_ERROR = 3, ST_WORDS = 4 };
+// Device status words of a step: this rank's {first_nonfinite, pack_saturations,
+// sum_saturations, error} and, world > 1, the global decision {first, pack_sat,
+// error} that the rank's reduce computes from every rank's words.  The public
+// sub-step status (lmsgd_status_reset) is the first four words.
+enum { ST_FIRST = 0, ST_PACK_SAT = 1, ST_SUM_SAT = 2, ST_ERROR = 3,
+       ST_G_FIRST = 4, ST_G_PACK_SAT = 5, ST_G_ERROR = 6, ST_WORDS = 8 };
 
 // fp32 constants of the update, each rounded once from double (R15).
 struct UpdConst {

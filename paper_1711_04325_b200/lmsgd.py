@@ -69,6 +69,7 @@ def _load() -> ctypes.CDLL:
         "lmsgd_hyper_default": (I32, [ctypes.POINTER(Hyper)]),
         "lmsgd_schedule_at": (I32, [ctypes.POINTER(Hyper), ctypes.POINTER(Cluster), I64, ctypes.POINTER(Coeffs)]),
         "lmsgd_schedule_steps": (I32, [ctypes.POINTER(Cluster), ctypes.POINTER(I64)]),
+        "lmsgd_layout": (I32, [I32, I64, ctypes.POINTER(I64), ctypes.POINTER(I64)]),
         "lmsgd_init": (I32, [ctypes.POINTER(P), I32, I32, I32, I64, F32, ctypes.POINTER(Hyper), U32]),
         "lmsgd_ipc_handle": (I32, [P, ctypes.c_char_p]),
         "lmsgd_connect": (I32, [P, ctypes.c_char_p]),
@@ -133,6 +134,13 @@ def lmsgd_schedule_steps(cluster: Cluster) -> int:
     T = ctypes.c_int64()
     _check(_lib.lmsgd_schedule_steps(ctypes.byref(cluster), ctypes.byref(T)))
     return T.value
+
+
+def lmsgd_layout(world: int, n: int) -> tuple[int, int]:
+    """(shard, n_pad) of the exchange layout."""
+    sh, npad = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.lmsgd_layout(int(world), int(n), ctypes.byref(sh), ctypes.byref(npad)))
+    return sh.value, npad.value
 
 
 def make_coeffs(eta: float, alpha_sgd: float, alpha_rmsprop: float, epoch: float = 0.0, phase: int = 0) -> Coeffs:

@@ -1,0 +1,155 @@
+"""Multi-GPU parity worker, launched by tests/test_multigpu.py through torchrun
+(one process per GPU, NCCL process group for bootstrap only).
+
+Checks on world = k real GPUs over NVLink, through the C ABI:
+  * R (fp16 all-reduce sum) and ghat bit-exact vs the oracle's k-worker exchange;
+  * state after each step within the one-step tolerance (oracle resynced);
+  * replica bit-identity of theta / Delta / m on every rank after every step;
+  * a non-finite gradient on one rank skips the step on every rank, same status;
+  * saturation counts summed over ranks;
+  * BN statistics average bit-exact vs the oracle;
+  * the full 25.6M ResNet-50 buffer (sampled check) in bench.py's launch configuration.
+Exit code 0 and "MGPU_OK" on rank 0 when everything passes.
+"""
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+
+import paper_1711_04325_b200 as L  # noqa: E402
+import synth  # noqa: E402
+from oracle import binary16, bn, exchange, run, schedule  # noqa: E402
+
+S = 1024.0
+C1 = schedule.Cluster(n_workers=2, b_local=32, n_train=64)
+C1_C = L.make_cluster(2, 32, 64)
+
+
+def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, tol=1e-6):
+    hyper = schedule.Hyper()
+    th_o, d_o, m_o = run.resync_step(th0, d0, m0, ghat, c, hyper)
+    gh = np.asarray(ghat, dtype=np.float64)
+    coef = c.alpha_sgd + c.alpha_rmsprop / (np.sqrt(m_o) + hyper.eps)
+    scale_d = hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + np.abs(coef * gh)
+    e = (run.scaled_error(m_g, m_o, m_o), run.scaled_error(d_g, d_o, scale_d),
+         run.scaled_error(th_g, th_o, np.abs(np.asarray(th0, np.float64)) + c.eta * scale_d))
+    assert max(e) <= tol, e
+
+
+def replicas_identical(*tensors):
+    for t in tensors:
+        ref = t.clone()
+        dist.broadcast(ref, 0)
+        assert torch.equal(ref, t), "replica divergence"
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    D = lambda x: torch.from_numpy(np.ascontiguousarray(x)).to(dev)  # noqa: E731
+    H = lambda x: x.cpu().numpy()  # noqa: E731
+
+    # ---- exchange + update parity on ragged sizes, across the warm-up
+    for n in (1, 100, 64 * world + 3, 123_457, (1 << 20) + 13):
+        ctx = L.lmsgd_init(world, rank, local, n, S)
+        L.connect_process_group(ctx)
+        a = synth.grad_scale(n)
+        r = np.random.default_rng(n)
+        th0 = synth.theta0(n, None)
+        d0 = (r.standard_normal(n) * 1e-3).astype(np.float32)
+        m0 = (r.random(n) * 1e-6).astype(np.float32)
+        th, d, m = D(th0), D(d0), D(m0)
+        for t in (1, 2, 11, 12, 15):
+            g = synth.grads(world, t, n, a)
+            prev = H(th), H(d), H(m)
+            L.lmsgd_step(ctx, th, D(g[rank]), d, m, L.lmsgd_schedule_at(None, C1_C, t))
+            code, st = L.lmsgd_query_status(ctx)
+            assert code == 0 and st.skipped == 0 and st.first_nonfinite == -1, (code, st.skipped)
+            ex = exchange.exchange(list(g), S)
+            assert st.pack_saturations == ex.pack_saturations and st.sum_saturations == ex.sum_saturations
+            check_state(H(th), H(d), H(m), *prev, ex.ghat, schedule.coeffs_at(t, schedule.Hyper(), C1))
+            replicas_identical(th, d, m)
+        L.lmsgd_finalize(ctx)
+
+    # ---- ghat bit-exact (mu1 = 0, (a_SGD, a_RMS) = (1, 0) => Delta = -ghat), with saturation
+    n = 200_003
+    hyp = L.lmsgd_hyper_default()
+    hyp.mu1 = 0.0
+    ctx = L.lmsgd_init(world, rank, local, n, S, hyp)
+    L.connect_process_group(ctx)
+    g = synth.grads(world, 7, n)
+    g[:, 0] = 60000.0 / S          # every rank near the top: the sum saturates at wire-2
+    g[0, 1] = 70000.0 / S          # rank 0 saturates at pack
+    z = lambda: D(np.zeros(n, np.float32))  # noqa: E731
+    th, d, m = z(), z(), z()
+    L.lmsgd_step(ctx, th, D(g[rank]), d, m, L.make_coeffs(1.0, 1.0, 0.0))
+    code, st = L.lmsgd_query_status(ctx)
+    ex = exchange.exchange(list(g), S)
+    assert np.array_equal(-H(d), ex.ghat), "ghat not bit-exact"
+    assert st.pack_saturations == ex.pack_saturations >= 1 and st.sum_saturations == ex.sum_saturations >= 1
+
+    # ---- non-finite on one rank: every rank skips, same first index (the global minimum)
+    th0, d0, m0 = H(th), H(d), H(m)
+    g = synth.grads(world, 8, n)
+    g[world - 1, 4321] = np.nan
+    g[0, 9999] = np.inf
+    L.lmsgd_step(ctx, th, D(g[rank]), d, m, L.make_coeffs(1.0, 1.0, 0.0))
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == L.LMSGD_ERR_NONFINITE and st.skipped == 1 and st.first_nonfinite == 4321, (code, st.first_nonfinite)
+    assert np.array_equal(H(th), th0) and np.array_equal(H(d), d0) and np.array_equal(H(m), m0)
+    try:
+        exchange.exchange(list(g), S)
+        raise AssertionError("oracle accepted a non-finite gradient")
+    except binary16.NonFiniteError as e:
+        assert e.index == 4321
+    # and the next clean step goes through
+    g = synth.grads(world, 9, n)
+    L.lmsgd_step(ctx, th, D(g[rank]), d, m, L.make_coeffs(1.0, 1.0, 0.0))
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == 0 and np.array_equal(-H(d), exchange.exchange(list(g), S).ghat)
+
+    # ---- BN last-minibatch statistics average
+    for C in (1, 64, sum(synth.resnet_bn_channels(50))):
+        mean_all, var_all = synth.bn_stats(world, C, seed=C)
+        mean, var = D(mean_all[rank]), D(var_all[rank])
+        L.lmsgd_bn_stats_allreduce(ctx, mean, var)
+        torch.cuda.synchronize()
+        om, ov = bn.sync_statistics(mean_all, var_all)
+        assert np.array_equal(H(mean), om) and np.array_equal(H(var), ov), "BN average not bit-exact"
+    L.lmsgd_finalize(ctx)
+
+    # ---- full ResNet-50 buffer, sampled check
+    n = synth.resnet_n_params(50)
+    ctx = L.lmsgd_init(world, rank, local, n, S)
+    L.connect_process_group(ctx)
+    th0 = synth.theta0(n, 50)
+    g = synth.grads(world, 1, n)
+    th, d, m = D(th0), D(np.zeros(n, np.float32)), D(np.zeros(n, np.float32))
+    cfull = L.lmsgd_schedule_at(None, L.make_cluster(), 1)
+    L.lmsgd_step(ctx, th, D(g[rank]), d, m, cfull)
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == 0
+    idx = np.unique(np.concatenate([np.arange(2000), np.arange(n - 2000, n),
+                                    np.random.default_rng(3).integers(0, n, 100_000)]))
+    ex = exchange.exchange([gi[idx] for gi in g], S)
+    z = np.zeros(idx.size, np.float32)
+    check_state(H(th)[idx], H(d)[idx], H(m)[idx], th0[idx], z, z, ex.ghat, schedule.coeffs_at(1))
+    replicas_identical(th, d, m)
+    L.lmsgd_finalize(ctx)
+
+    dist.barrier()
+    if rank == 0:
+        print(f"MGPU_OK world={world}", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -5,7 +5,7 @@ Bar (BASELINE.json north_star):
   * schedule: bit-exact (tests/test_lib_host.py);
   * fp32 state after one step, oracle resynced to the GPU's previous state:
     |x_gpu - x_oracle| <= 1e-6 * scale_x with scale_m = m_t,
-    scale_Delta = mu1 |Delta_{t-1}| + |c ghat|, scale_theta = |theta_{t-1}| + |eta Delta_t|;
+    scale_Delta = mu1 |Delta_{t-1}| + |c ghat|, scale_theta = |theta_{t-1}| + eta scale_Delta;
   * status words (first non-finite index, saturation counts): exact.
 """
 import numpy as np
@@ -40,10 +40,12 @@ def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, hyper=schedule.Hyper(), to
     th_o, d_o, m_o = run.resync_step(th0, d0, m0, ghat, c, hyper)
     gh = np.asarray(ghat, dtype=np.float64)
     coef = c.alpha_sgd + c.alpha_rmsprop / (np.sqrt(m_o) + hyper.eps)
+    scale_d = hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + np.abs(coef * gh)
     e = {
         "m": run.scaled_error(m_g, m_o, m_o),
-        "delta": run.scaled_error(d_g, d_o, hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + np.abs(coef * gh)),
-        "theta": run.scaled_error(th_g, th_o, np.abs(np.asarray(th0, np.float64)) + np.abs(c.eta * d_o)),
+        "delta": run.scaled_error(d_g, d_o, scale_d),
+        # Delta's own rounding (relative to scale_d) propagates through eta: DESIGN.md "Tolerances"
+        "theta": run.scaled_error(th_g, th_o, np.abs(np.asarray(th0, np.float64)) + c.eta * scale_d),
     }
     assert max(e.values()) <= tol, e
     return e

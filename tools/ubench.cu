@@ -1,0 +1,317 @@
+// Micro-benchmark of kernel variants for the k = 1 step on a 25.6M-element buffer
+// (development tool; the product kernels live in paper_1711_04325_b200/csrc).
+// Every variant must be bit-identical to the production kernels; timings are CUDA
+// events over 200 back-to-back launches after warm-up.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//        -I paper_1711_04325_b200/csrc tools/ubench.cu -o tools/ubench
+#include "../paper_1711_04325_b200/csrc/kernels.cu"
+
+namespace lmsgd {
+namespace {
+#include "../paper_1711_04325_b200/csrc/stream_tma.cuh"
+}  // namespace
+}  // namespace lmsgd
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+#include <functional>
+
+namespace lmsgd {
+namespace {
+
+// V1: two groups per thread per trip, all loads hoisted.
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) k_update_u2(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
+                                                        float* __restrict__ th, float* __restrict__ d,
+                                                        float* __restrict__ m) {
+    const int64_t nv = n >> 3;
+    const int64_t st = gstride();
+    for (int64_t v = gtid(); v < nv; v += 2 * st) {
+        const int64_t v2 = v + st;
+        const bool has2 = v2 < nv;
+        const int64_t j0 = v << 3, j1 = v2 << 3;
+        const uint4 r0 = *reinterpret_cast<const uint4*>(R + j0);
+        const uint4 r1 = has2 ? *reinterpret_cast<const uint4*>(R + j1) : make_uint4(0, 0, 0, 0);
+        float4 a[6], b[6];
+        const float4* p0[3] = {reinterpret_cast<float4*>(th + j0), reinterpret_cast<float4*>(d + j0), reinterpret_cast<float4*>(m + j0)};
+        const float4* p1[3] = {reinterpret_cast<float4*>(th + j1), reinterpret_cast<float4*>(d + j1), reinterpret_cast<float4*>(m + j1)};
+#pragma unroll
+        for (int q = 0; q < 3; ++q) { a[2 * q] = __ldcs(p0[q]); a[2 * q + 1] = __ldcs(p0[q] + 1); }
+        if (has2) {
+#pragma unroll
+            for (int q = 0; q < 3; ++q) { b[2 * q] = __ldcs(p1[q]); b[2 * q + 1] = __ldcs(p1[q] + 1); }
+        }
+        auto go = [&](uint4 r, float4* x, int64_t j) {
+            const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+            float tv[8] = {x[0].x, x[0].y, x[0].z, x[0].w, x[1].x, x[1].y, x[1].z, x[1].w};
+            float dv[8] = {x[2].x, x[2].y, x[2].z, x[2].w, x[3].x, x[3].y, x[3].z, x[3].w};
+            float mv[8] = {x[4].x, x[4].y, x[4].z, x[4].w, x[5].x, x[5].y, x[5].z, x[5].w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i) upd1<RMS>(h2f(w[i >> 1], i & 1) * c.inv_ks, tv[i], dv[i], mv[i], c);
+            float4* t4 = reinterpret_cast<float4*>(th + j);
+            float4* d4 = reinterpret_cast<float4*>(d + j);
+            float4* m4 = reinterpret_cast<float4*>(m + j);
+            __stcs(t4, make_float4(tv[0], tv[1], tv[2], tv[3])); __stcs(t4 + 1, make_float4(tv[4], tv[5], tv[6], tv[7]));
+            __stcs(d4, make_float4(dv[0], dv[1], dv[2], dv[3])); __stcs(d4 + 1, make_float4(dv[4], dv[5], dv[6], dv[7]));
+            __stcs(m4, make_float4(mv[0], mv[1], mv[2], mv[3])); __stcs(m4 + 1, make_float4(mv[4], mv[5], mv[6], mv[7]));
+        };
+        go(r0, a, j0);
+        if (has2) go(r1, b, j1);
+    }
+}
+
+// V2: one group per thread, one-shot grid.
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) k_update_flat(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
+                                                          float* __restrict__ th, float* __restrict__ d,
+                                                          float* __restrict__ m) {
+    const int64_t v = gtid();
+    if (v < (n >> 3)) update8<RMS>(*reinterpret_cast<const uint4*>(R + (v << 3)), v << 3, n, c, th, d, m);
+}
+
+// V8: flat, two groups per thread (loads of both hoisted)
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) k_update_flat2(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
+                                                           float* __restrict__ th, float* __restrict__ d,
+                                                           float* __restrict__ m) {
+    const int64_t v0 = (int64_t)blockIdx.x * (2 * blockDim.x) + threadIdx.x;
+    const int64_t v1 = v0 + blockDim.x;
+    const int64_t nv = n >> 3;
+    uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0;
+    if (v0 < nv) r0 = *reinterpret_cast<const uint4*>(R + (v0 << 3));
+    if (v1 < nv) r1 = *reinterpret_cast<const uint4*>(R + (v1 << 3));
+    if (v0 < nv) update8<RMS>(r0, v0 << 3, n, c, th, d, m);
+    if (v1 < nv) update8<RMS>(r1, v1 << 3, n, c, th, d, m);
+}
+
+template <int BS>
+__global__ void __launch_bounds__(BS) k_update_flat_bs(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
+                                                       float* __restrict__ th, float* __restrict__ d,
+                                                       float* __restrict__ m) {
+    const int64_t v = (int64_t)blockIdx.x * BS + threadIdx.x;
+    if (v < (n >> 3)) update8<true>(*reinterpret_cast<const uint4*>(R + (v << 3)), v << 3, n, c, th, d, m);
+}
+
+__global__ void __launch_bounds__(kThreads) k_pack_flat(const float* __restrict__ g, int64_t n, int64_t n_pad, float s,
+                                                        uint16_t* __restrict__ h, int64_t* st) {
+    int64_t first = kNone;
+    unsigned sat = 0;
+    const int64_t v = gtid();
+    if (v < (n_pad >> 3)) {
+        const int64_t j0 = v << 3;
+        float x[8];
+        load8_g(g, j0, n, x);
+        *reinterpret_cast<uint4*>(h + j0) = pack8(x, s, j0, first, sat);
+    }
+    flush_status(first, sat, st, ST_PACK_SAT);
+}
+
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) k_fused_flat(const float* __restrict__ g, int64_t n, float s, UpdConst c,
+                                                         float* __restrict__ th, float* __restrict__ d,
+                                                         float* __restrict__ m, int64_t* st) {
+    int64_t first = kNone;
+    unsigned sat = 0;
+    const int64_t v = gtid();
+    if (v < ((n + 7) >> 3)) {
+        const int64_t j0 = v << 3;
+        float x[8];
+        load8_g(g, j0, n, x);
+        update8<RMS>(pack8(x, s, j0, first, sat), j0, n, c, th, d, m);
+    }
+    flush_status(first, sat, st, ST_PACK_SAT);
+}
+
+// P1: pack with h kept in L2 (evict_last) for the update that follows.
+__global__ void __launch_bounds__(kThreads) k_pack_l2(const float* __restrict__ g, int64_t n, int64_t n_pad, float s,
+                                                      uint16_t* __restrict__ h, int64_t* st) {
+    int64_t first = kNone;
+    unsigned sat = 0;
+    const uint64_t pol = policy_evict_last();
+    const int64_t nv = n_pad >> 3;
+    for (int64_t v = gtid(); v < nv; v += gstride()) {
+        const int64_t j0 = v << 3;
+        float x[8];
+        load8_g(g, j0, n, x);
+        const uint4 o = pack8(x, s, j0, first, sat);
+        asm volatile("st.global.L2::cache_hint.v4.b32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(h + j0), "r"(o.x), "r"(o.y),
+                     "r"(o.z), "r"(o.w), "l"(pol) : "memory");
+    }
+    flush_status(first, sat, st, ST_PACK_SAT);
+}
+
+// update reading h then discarding its L2 lines (no write-back of dead wire data)
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) k_update_discard(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
+                                                             float* __restrict__ th, float* __restrict__ d,
+                                                             float* __restrict__ m, const int64_t* st) {
+    if (st[ST_FIRST] != kNone || st[ST_ERROR] != 0) return;
+    const int64_t nv = (n + 7) >> 3;
+    for (int64_t v = gtid(); v < nv; v += gstride()) {
+        const int64_t j0 = v << 3;
+        const uint4 r = *reinterpret_cast<const uint4*>(R + j0);
+        // each lane holds 16 B; lanes 0,8,16,24 own whole 128-B lines when the warp is aligned
+        if ((j0 & 63) == 0 && j0 + 64 <= ((n + 7) & ~int64_t(7)))
+            asm volatile("discard.global.L2 [%0], 128;" ::"l"(R + j0) : "memory");
+        update8<RMS>(r, j0, n, c, th, d, m);
+    }
+}
+
+}  // namespace
+}  // namespace lmsgd
+
+using namespace lmsgd;
+
+#define CKE(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1);} } while (0)
+
+static float time_it(int iters, const std::function<void()>& f) {
+    cudaEvent_t a, b;
+    cudaEventCreate(&a); cudaEventCreate(&b);
+    for (int i = 0; i < 5; ++i) f();
+    cudaEventRecord(a);
+    for (int i = 0; i < iters; ++i) f();
+    cudaEventRecord(b);
+    CKE(cudaEventSynchronize(b));
+    float ms; cudaEventElapsedTime(&ms, a, b);
+    return ms / iters * 1e3f;  // us
+}
+
+int main(int argc, char** argv) {
+    const int64_t n = argc > 1 ? atoll(argv[1]) : 25557032;
+    const int iters = 200;
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    const int64_t n_pad = (n + 63) / 64 * 64;
+    std::vector<float> hg(n), ht(n), hd(n), hm(n);
+    srand(1);
+    for (int64_t i = 0; i < n; ++i) {
+        hg[i] = ((rand() / (float)RAND_MAX) - 0.5f) * 1e-3f;
+        ht[i] = ((rand() / (float)RAND_MAX) - 0.5f) * 0.1f;
+        hd[i] = ((rand() / (float)RAND_MAX) - 0.5f) * 1e-3f;
+        hm[i] = (rand() / (float)RAND_MAX) * 1e-6f;
+    }
+    float *g, *th, *d, *m, *th0, *d0, *m0;
+    uint16_t* h; int64_t* st;
+    CKE(cudaMalloc(&g, n * 4)); CKE(cudaMalloc(&th, n * 4)); CKE(cudaMalloc(&d, n * 4)); CKE(cudaMalloc(&m, n * 4));
+    CKE(cudaMalloc(&th0, n * 4)); CKE(cudaMalloc(&d0, n * 4)); CKE(cudaMalloc(&m0, n * 4));
+    CKE(cudaMalloc(&h, n_pad * 2)); CKE(cudaMalloc(&st, 64));
+    cudaMemcpy(g, hg.data(), n * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(th0, ht.data(), n * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(d0, hd.data(), n * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(m0, hm.data(), n * 4, cudaMemcpyHostToDevice);
+    UpdConst c{0.9f, 0.99f, (float)(1.0 - 0.99), 1e-8f, 6.4f, 0.00915781944436709f, 4.644572721354529e-05f, 1.0f / 1024};
+    const Launch L{sms, sms * stream_blocks_per_sm()};  // production launchers now use flat grids
+    auto reset = [&] {
+        cudaMemcpy(th, th0, n * 4, cudaMemcpyDeviceToDevice);
+        cudaMemcpy(d, d0, n * 4, cudaMemcpyDeviceToDevice);
+        cudaMemcpy(m, m0, n * 4, cudaMemcpyDeviceToDevice);
+        k_status_reset<<<1, 32>>>(st, 4);
+    };
+    std::vector<float> rt(n), rd(n), rm(n), xt(n), xd(n), xm(n);
+    auto snapshot = [&](std::vector<float>& a, std::vector<float>& b, std::vector<float>& cc) {
+        CKE(cudaDeviceSynchronize());
+        cudaMemcpy(a.data(), th, n * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(b.data(), d, n * 4, cudaMemcpyDeviceToHost);
+        cudaMemcpy(cc.data(), m, n * 4, cudaMemcpyDeviceToHost);
+    };
+    auto same = [&]() {
+        snapshot(xt, xd, xm);
+        return memcmp(xt.data(), rt.data(), n * 4) == 0 && memcmp(xd.data(), rd.data(), n * 4) == 0 &&
+               memcmp(xm.data(), rm.data(), n * 4) == 0;
+    };
+    const double upd_bytes = 26.0 * n, fused_bytes = 28.0 * n, pack_bytes = 6.0 * n;
+    // reference result: one pack + update (production kernels)
+    reset();
+    launch_pack(0, L, g, n, n_pad, 1024.f, h, st);
+    launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr);
+    snapshot(rt, rd, rm);
+
+    printf("n=%lld sms=%d blocks/sm(stream)=%d\n", (long long)n, sms, stream_blocks_per_sm());
+    float t;
+    t = time_it(iters, [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st); });
+    printf("P0 pack            %8.2f us  %7.1f GB/s\n", t, pack_bytes / t / 1e3);
+    t = time_it(iters, [&] { k_pack_l2<<<L.grid_cap_stream, kThreads>>>(g, n, n_pad, 1024.f, h, st); });
+    printf("P1 pack evict_last %8.2f us  %7.1f GB/s\n", t, pack_bytes / t / 1e3);
+    const int fgrid = (int)(((n_pad >> 3) + kThreads - 1) / kThreads);
+    t = time_it(iters, [&] { k_pack_flat<<<fgrid, kThreads>>>(g, n, n_pad, 1024.f, h, st); });
+    printf("P2 pack flat       %8.2f us  %7.1f GB/s\n", t, pack_bytes / t / 1e3);
+
+    reset(); launch_pack(0, L, g, n, n_pad, 1024.f, h, st); CKE(cudaDeviceSynchronize());
+    // update variants (single step each for bitwise check, then timed repeatedly)
+    struct V { const char* name; std::function<void()> f; };
+    const int gridc = L.grid_cap_stream;
+    std::vector<V> vs = {
+        {"V0 update (prod)", [&] { k_update<true><<<gridc, kThreads>>>(h, n, c, th, d, m, st, nullptr, nullptr); }},
+        {"V1 update unroll2", [&] { k_update_u2<true><<<gridc, kThreads>>>(h, n, c, th, d, m); }},
+        {"V2 update flat", [&] { k_update_flat<true><<<(int)(((n >> 3) + kThreads - 1) / kThreads), kThreads>>>(h, n, c, th, d, m); }},
+        {"V7 update flat bs512", [&] { k_update_flat_bs<512><<<(int)(((n >> 3) + 511) / 512), 512>>>(h, n, c, th, d, m); }},
+        {"V7b update flat bs128", [&] { k_update_flat_bs<128><<<(int)(((n >> 3) + 127) / 128), 128>>>(h, n, c, th, d, m); }},
+        {"V8 update flat2", [&] { k_update_flat2<true><<<(int)(((n >> 3) + 511) / 512), kThreads>>>(h, n, c, th, d, m); }},
+        {"V3 update tma TE2048 S6", [&] {
+             k_stream_tma<true, false, 2048, 6><<<sms, kTmaThreads, 6 * tma_stage_bytes<false, 2048>()>>>(h, n, 1024.f, c, th, d, m, st, nullptr); }},
+        {"V4 update tma TE4096 S4", [&] {
+             k_stream_tma<true, false, 4096, 4><<<sms, kTmaThreads, 4 * tma_stage_bytes<false, 4096>()>>>(h, n, 1024.f, c, th, d, m, st, nullptr); }},
+        {"V5 update tma TE1024 S3 x2/SM", [&] {
+             k_stream_tma<true, false, 1024, 3><<<2 * sms, kTmaThreads, 3 * tma_stage_bytes<false, 1024>()>>>(h, n, 1024.f, c, th, d, m, st, nullptr); }},
+        {"V6 update tma TE2048 S3 x2/SM", [&] {
+             k_stream_tma<true, false, 2048, 3><<<2 * sms, kTmaThreads, 3 * tma_stage_bytes<false, 2048>()>>>(h, n, 1024.f, c, th, d, m, st, nullptr); }},
+    };
+    CKE(cudaFuncSetAttribute(k_stream_tma<true, false, 2048, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * tma_stage_bytes<false, 2048>()));
+    CKE(cudaFuncSetAttribute(k_stream_tma<true, false, 4096, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * tma_stage_bytes<false, 4096>()));
+    CKE(cudaFuncSetAttribute(k_stream_tma<true, false, 1024, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * tma_stage_bytes<false, 1024>()));
+    CKE(cudaFuncSetAttribute(k_stream_tma<true, false, 2048, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * tma_stage_bytes<false, 2048>()));
+    CKE(cudaFuncSetAttribute(k_stream_tma<true, true, 2048, 6>, cudaFuncAttributeMaxDynamicSharedMemorySize, 6 * tma_stage_bytes<true, 2048>()));
+    CKE(cudaFuncSetAttribute(k_stream_tma<true, true, 2048, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 3 * tma_stage_bytes<true, 2048>()));
+    for (auto& v : vs) {
+        reset(); CKE(cudaGetLastError());
+        v.f(); CKE(cudaGetLastError());
+        const bool ok = same();
+        t = time_it(iters, v.f);
+        CKE(cudaGetLastError());
+        printf("%-30s %8.2f us  %7.1f GB/s  bitexact=%d\n", v.name, t, upd_bytes / t / 1e3, ok);
+    }
+    // fused variants vs production fused
+    reset(); launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr, nullptr); snapshot(rt, rd, rm);
+    std::vector<V> fs = {
+        {"F0 fused (prod)", [&] { launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr, nullptr); }},
+        {"F2 fused flat", [&] { k_fused_flat<true><<<(int)((((n + 7) >> 3) + kThreads - 1) / kThreads), kThreads>>>(g, n, 1024.f, c, th, d, m, st); }},
+        {"F3 fused tma TE2048 S6", [&] {
+             k_stream_tma<true, true, 2048, 6><<<sms, kTmaThreads, 6 * tma_stage_bytes<true, 2048>()>>>(g, n, 1024.f, c, th, d, m, nullptr, st); }},
+        {"F6 fused tma TE2048 S3 x2/SM", [&] {
+             k_stream_tma<true, true, 2048, 3><<<2 * sms, kTmaThreads, 3 * tma_stage_bytes<true, 2048>()>>>(g, n, 1024.f, c, th, d, m, nullptr, st); }},
+    };
+    for (auto& v : fs) {
+        reset(); v.f(); CKE(cudaGetLastError());
+        const bool ok = same();
+        t = time_it(iters, v.f);
+        CKE(cudaGetLastError());
+        printf("%-30s %8.2f us  %7.1f GB/s  bitexact=%d\n", v.name, t, fused_bytes / t / 1e3, ok);
+    }
+    // guarded pair: pack + update, and the L2-resident variant
+    reset(); launch_pack(0, L, g, n, n_pad, 1024.f, h, st); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr); snapshot(rt, rd, rm);
+    std::vector<V> ps = {
+        {"G0 pack+update (prod)", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr); }},
+        {"G1 pack_l2+update_discard", [&] { k_pack_l2<<<gridc, kThreads>>>(g, n, n_pad, 1024.f, h, st);
+                                             k_update_discard<true><<<gridc, kThreads>>>(h, n, c, th, d, m, st); }},
+        {"G2 pack_l2+update tma", [&] { k_pack_l2<<<gridc, kThreads>>>(g, n, n_pad, 1024.f, h, st);
+             k_stream_tma<true, false, 2048, 6><<<sms, kTmaThreads, 6 * tma_stage_bytes<false, 2048>()>>>(h, n, 1024.f, c, th, d, m, st, nullptr); }},
+        {"G4 pack flat+update flat", [&] { k_pack_flat<<<fgrid, kThreads>>>(g, n, n_pad, 1024.f, h, st);
+             k_update_flat<true><<<(int)(((n >> 3) + kThreads - 1) / kThreads), kThreads>>>(h, n, c, th, d, m); }},
+        {"G3 pack+update tma", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st);
+             k_stream_tma<true, false, 2048, 6><<<sms, kTmaThreads, 6 * tma_stage_bytes<false, 2048>()>>>(h, n, 1024.f, c, th, d, m, st, nullptr); }},
+    };
+    for (auto& v : ps) {
+        reset(); v.f(); CKE(cudaGetLastError());
+        const bool ok = same();
+        t = time_it(iters, v.f);
+        CKE(cudaGetLastError());
+        printf("%-30s %8.2f us  %7.1f GB/s(32B/e) bitexact=%d\n", v.name, t, 32.0 * n / t / 1e3, ok);
+    }
+    // plain copy reference (HBM ceiling for a 1:1 read/write stream)
+    t = time_it(iters, [&] { cudaMemcpyAsync(th, th0, n * 4, cudaMemcpyDeviceToDevice);
+                             cudaMemcpyAsync(d, d0, n * 4, cudaMemcpyDeviceToDevice);
+                             cudaMemcpyAsync(m, m0, n * 4, cudaMemcpyDeviceToDevice); });
+    printf("memcpy D2D 3x%lld floats   %8.2f us  %7.1f GB/s (r+w)\n", (long long)n, t, 2.0 * 12 * n / t / 1e3);
+    return 0;
+}
