@@ -72,9 +72,23 @@ def unpack_average(R, k: int, s: float = 1.0) -> np.ndarray:
     return binary16.from_binary16(R).astype(np.float32) * inv
 
 
+def check_finite(g_workers):
+    """Reading R7: a non-finite gradient on any worker is an error; the reported
+    index is the smallest flat index j at which any worker's g_j is non-finite."""
+    first = None
+    for g in g_workers:
+        bad = ~np.isfinite(np.asarray(g, dtype=np.float32))
+        if bad.any():
+            j = int(np.argmax(bad))
+            first = j if first is None else min(first, j)
+    if first is not None:
+        raise binary16.NonFiniteError(first)
+
+
 def exchange(g_workers, s: float = 1.0) -> ExchangeResult:
     """The whole exchange for k = len(g_workers) workers."""
     k = len(g_workers)
+    check_finite(g_workers)
     packed = [pack(g, s) for g in g_workers]
     S = reduce_sum([p[0] for p in packed])
     R, sat2 = binary16.to_binary16(S, return_saturation=True)

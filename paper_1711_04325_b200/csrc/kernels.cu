@@ -345,21 +345,33 @@ __device__ void grid_signal(const XArgs& x, int which) {
     if (grid_last(x, which)) publish(x, which);
 }
 
+// Work units of the exchange kernels: a unit is kThreads consecutive 8-element groups
+// of one shard.  Units are interleaved over owners -- unit u belongs to owner
+// (u + rank) % world -- so that the blocks in flight on every rank touch all owners
+// evenly (no owner's links are a hot spot) and local and remote traffic mix.
+__device__ __forceinline__ int64_t units_of(const XArgs& x) {
+    const int64_t gsh = x.lay.shard >> 3;
+    return (int64_t)x.world * ((gsh + kThreads - 1) / kThreads);
+}
+__device__ __forceinline__ bool map_unit(const XArgs& x, int64_t u, int& owner, int64_t& gi) {
+    owner = (int)((u % x.world + x.rank) % x.world);
+    gi = (u / x.world) * kThreads + threadIdx.x;   // group index inside the owner's shard
+    return gi < (x.lay.shard >> 3);
+}
+
 // Pack this rank's gradient and push each shard straight into its owner's receive
-// slot (peer stores over NVLink).  Ranks walk the shards in rotated order so that at
-// any moment each owner receives from one sender.
+// slot (peer stores over NVLink), interleaved over owners.
 __global__ void __launch_bounds__(kThreads) k_pack_push(XArgs x, const float* __restrict__ g, float s) {
     int64_t first = kNone;
     unsigned sat = 0;
     const int64_t gsh = x.lay.shard >> 3;
-    const int64_t nvp = gsh * x.world;
-    const int64_t rot = (int64_t)x.rank * gsh;
-    for (int64_t v = gtid(); v < nvp; v += gstride()) {
-        int64_t vv = v + rot;
-        if (vv >= nvp) vv -= nvp;
-        const int64_t j0 = vv << 3;
-        const int owner = (int)(vv / gsh);
-        const int64_t off = (vv - (int64_t)owner * gsh) << 3;
+    const int64_t units = units_of(x);
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int owner;
+        int64_t gi;
+        if (!map_unit(x, u, owner, gi)) continue;
+        const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+        const int64_t off = gi << 3;
         float xv[8];
         load8_g(g, j0, x.n, xv);
         uint16_t* dst = reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
@@ -440,16 +452,14 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(XArgs x, UpdConst c,
     }
     if (skip) return;
     const int64_t gsh = x.lay.shard >> 3;
-    const int64_t nvp = gsh * x.world;
-    const int64_t rot = (int64_t)x.rank * gsh;
-    for (int64_t v = gtid(); v < nvp; v += gstride()) {
-        int64_t vv = v + rot;
-        if (vv >= nvp) vv -= nvp;
-        const int64_t j0 = vv << 3;
+    const int64_t units = units_of(x);
+    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        int owner;
+        int64_t gi;
+        if (!map_unit(x, u, owner, gi)) continue;
+        const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
         if (j0 >= x.n) continue;
-        const int owner = (int)(vv / gsh);
-        const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) +
-                             ((vv - (int64_t)owner * gsh) << 3);
+        const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
         const uint4 r = *reinterpret_cast<const uint4*>(Rp);
         update8<RMS>(r, j0, x.n, c, th, d, m);
     }
@@ -493,6 +503,12 @@ int grid_for(const Launch&, int64_t work_items) {
 }  // namespace
 
 // ------------------------------------------------------------------ launchers
+
+int push_blocks_per_sm() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pack_push, kThreads, 0);
+    return b > 0 ? b : 1;
+}
 
 int stream_blocks_per_sm() {
     int worst = 1 << 30, b = 0;
@@ -544,9 +560,20 @@ cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64
     return cudaGetLastError();
 }
 
+// Persistent grid for the push: the system-scope fence each block issues before the
+// ticket waits for its remote stores to be acknowledged, so it is paid once per
+// resident block, not once per 2048 elements (tools/p2pbench.cu: 80.7 us vs 120 us
+// for a 51 MB push at k = 2 on NVLink 5).
+int64_t host_units(const XArgs& x) {
+    const int64_t gsh = x.lay.shard >> 3;
+    return (int64_t)x.world * ((gsh + kThreads - 1) / kThreads);
+}
+
 cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,
                              float scale) {
-    k_pack_push<<<grid_for(L, (x.lay.shard >> 3) * x.world), kThreads, 0, s>>>(x, g, scale);
+    int64_t blocks = host_units(x);
+    if (blocks > L.grid_cap_push) blocks = L.grid_cap_push;
+    k_pack_push<<<(int)blocks, kThreads, 0, s>>>(x, g, scale);
     return cudaGetLastError();
 }
 
@@ -557,7 +584,7 @@ cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x)
 
 cudaError_t launch_update_gather(cudaStream_t s, const Launch& L, const XArgs& x, const UpdConst& c,
                                  float* th, float* d, float* m, int64_t* last) {
-    const int grid = grid_for(L, (x.lay.shard >> 3) * x.world);
+    const int grid = (int)host_units(x);  // flat: one unit per block
     if (c.a_rms != 0.0f)
         k_update_gather<true><<<grid, kThreads, 0, s>>>(x, c, th, d, m, last);
     else

@@ -45,7 +45,8 @@ struct Ticket {
 
 struct Launch {
     int sm_count;
-    int grid_cap_stream;   // grid cap for the streaming kernels (SMs x resident blocks)
+    int grid_cap_stream;   // SMs x resident blocks of the streaming kernels (informational)
+    int grid_cap_push;     // SMs x resident blocks of k_pack_push (persistent grid)
 };
 
 // ---- single-GPU building blocks (sub-step ABI and world == 1)
@@ -61,6 +62,7 @@ cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64
                           const UpdConst& c, float* th, float* d, float* m, int64_t* st,
                           int64_t* st_reset, unsigned int* ticket, int64_t* last);
 int stream_blocks_per_sm();
+int push_blocks_per_sm();
 
 // ---- world > 1 exchange over peer memory (NVLink / NVSwitch)
 struct XArgs {

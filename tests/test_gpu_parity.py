@@ -232,7 +232,8 @@ def test_c1_twenty_steps_resynced():
         check_state(host(th), host(d), host(m), *prev, ex.ghat, schedule.coeffs_at(t, schedule.Hyper(), C1))
     # free-running drift over 20 steps stays small (fp32 vs fp64 compounding)
     scale = np.abs(free.theta) + 1e-3
-    assert run.scaled_error(host(th), free.theta, scale) < 1e-5
+    # bound: 20 steps x momentum gain 1/(1-mu1) = 10 x per-step 5e-7
+    assert run.scaled_error(host(th), free.theta, scale) < 1e-4
 
 
 # ------------------------------------------------------------------ sub-steps / simulated k

@@ -121,3 +121,14 @@ def test_loss_scale_reduces_subnormal_loss():
     e1 = abs(float(ex.exchange([g], 1.0).ghat[0]) - 3e-6) / 3e-6
     e2 = abs(float(ex.exchange([g], 1024.0).ghat[0]) - 3e-6) / 3e-6
     assert e2 < 2.0 ** -11 < e1
+
+
+def test_nonfinite_index_is_minimum_over_workers():
+    # R7: the smallest flat index at which ANY worker is non-finite
+    a = np.ones(100, dtype=np.float32)
+    b = np.ones(100, dtype=np.float32)
+    a[60] = np.nan
+    b[25] = np.inf
+    with pytest.raises(b16.NonFiniteError) as e:
+        ex.exchange([a, b])
+    assert e.value.index == 25
