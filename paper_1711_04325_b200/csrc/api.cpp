@@ -333,9 +333,9 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
         if (c->flags & LMSGD_FLAG_NO_SKIP) {
             CK(c, timed(c, s, 0, [&] {
                    return lmsgd::launch_fused1(s, c->L, grads, c->n, c->scale, u, params, delta, m,
-                                               status_slot(c, parity), status_slot(c, parity ^ 1),
-                                               c->tickets + 3, c->last);
+                                               status_slot(c, parity), status_slot(c, parity ^ 1), nullptr);
                }));
+            CK(c, lmsgd::launch_finalize_fused(s, status_slot(c, parity), c->last));
         } else {
             CK(c, timed(c, s, 0, [&] {
                    return lmsgd::launch_pack(s, c->L, grads, c->n, c->n_pad, c->scale, h, status_slot(c, parity));
@@ -477,7 +477,7 @@ lmsgd_status lmsgd_fused_step1(void* stream, const float* g, int64_t n, float lo
         return fail(nullptr, LMSGD_ERR_INVALID_ARG, "fused_step1: bad pointer, size, scale, hyper or coeffs");
     const UpdConst u = make_const(h, *coeffs, 1, loss_scale);
     cudaError_t e = lmsgd::launch_fused1(static_cast<cudaStream_t>(stream), launch_for_current_device(), g, n,
-                                         loss_scale, u, params, delta, m, dstatus, nullptr, nullptr, nullptr);
+                                         loss_scale, u, params, delta, m, dstatus, nullptr, nullptr);
     return e == cudaSuccess ? LMSGD_OK : cuda_fail(nullptr, e, "fused_step1");
 }
 

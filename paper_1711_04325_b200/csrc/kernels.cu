@@ -261,8 +261,7 @@ template <bool RMS>
 __global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g, int64_t n, float s,
                                                      UpdConst c, float* __restrict__ th,
                                                      float* __restrict__ d, float* __restrict__ m,
-                                                     int64_t* st, int64_t* st_reset,
-                                                     unsigned int* ticket, int64_t* last) {
+                                                     int64_t* st, int64_t* st_reset) {
     reset_status(st_reset);
     int64_t first = kNone;
     unsigned sat = 0;
@@ -275,16 +274,12 @@ __global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g
         update8<RMS>(r, j0, n, c, th, d, m);
     }
     flush_status(first, sat, st, ST_PACK_SAT);
-    if (last) {  // the last block to finish publishes the step status (not skipped)
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0 && atomicAdd(ticket, 1u) == gridDim.x - 1) {
-            *ticket = 0;
-            __threadfence();
-            const volatile int64_t* vs = st;
-            store_last(last, vs[ST_FIRST], vs[ST_PACK_SAT], vs[ST_SUM_SAT], vs[ST_ERROR], 0);
-        }
-    }
+}
+
+// Publishes the fused step's status (never skipped) into the public `last` record.
+// A separate 1-warp launch: a per-block fence + ticket in k_fused1 cost 16% of it.
+__global__ void k_finalize_fused(const int64_t* st, int64_t* last) {
+    if (threadIdx.x == 0) store_last(last, st[ST_FIRST], st[ST_PACK_SAT], st[ST_SUM_SAT], st[ST_ERROR], 0);
 }
 
 // ------------------------------------------------------------------ world > 1
@@ -514,7 +509,7 @@ int stream_blocks_per_sm() {
     int worst = 1 << 30, b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update<true>, kThreads, 0);
     worst = b < worst ? b : worst;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true>, kThreads, 0);  // NOLINT
     worst = b < worst ? b : worst;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update_gather<true>, kThreads, 0);
     worst = b < worst ? b : worst;
@@ -551,12 +546,13 @@ cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, in
 
 cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                           const UpdConst& c, float* th, float* d, float* m, int64_t* st,
-                          int64_t* st_reset, unsigned int* ticket, int64_t* last) {
+                          int64_t* st_reset, int64_t* last) {
     const int grid = grid_for(L, (n + 7) >> 3);
     if (c.a_rms != 0.0f)
-        k_fused1<true><<<grid, kThreads, 0, s>>>(g, n, scale, c, th, d, m, st, st_reset, ticket, last);
+        k_fused1<true><<<grid, kThreads, 0, s>>>(g, n, scale, c, th, d, m, st, st_reset);
     else
-        k_fused1<false><<<grid, kThreads, 0, s>>>(g, n, scale, c, th, d, m, st, st_reset, ticket, last);
+        k_fused1<false><<<grid, kThreads, 0, s>>>(g, n, scale, c, th, d, m, st, st_reset);
+    (void)last;
     return cudaGetLastError();
 }
 
@@ -567,6 +563,11 @@ cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64
 int64_t host_units(const XArgs& x) {
     const int64_t gsh = x.lay.shard >> 3;
     return (int64_t)x.world * ((gsh + kThreads - 1) / kThreads);
+}
+
+cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last) {
+    k_finalize_fused<<<1, 32, 0, s>>>(st, last);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,

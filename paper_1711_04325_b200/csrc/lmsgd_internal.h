@@ -60,7 +60,8 @@ cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, in
                           int64_t* st_reset, int64_t* last);
 cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                           const UpdConst& c, float* th, float* d, float* m, int64_t* st,
-                          int64_t* st_reset, unsigned int* ticket, int64_t* last);
+                          int64_t* st_reset, int64_t* last);
+cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last);
 int stream_blocks_per_sm();
 int push_blocks_per_sm();
 

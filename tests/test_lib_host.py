@@ -140,3 +140,9 @@ def test_no_oracle_in_product_path():
                 src = open(os.path.join(dirpath, f)).read()
                 assert not re.search(r"^\s*(import|from)\s+(oracle|synth)\b", src, re.M), f
                 assert "oracle/" not in src and "oracle." not in src.replace("oracle.  ", ""), f
+
+
+def test_no_undefined_library_symbols():
+    out = subprocess.run(["nm", "-D", "--undefined-only", L.LIB_PATH], capture_output=True, text=True).stdout
+    bad = [ln for ln in out.splitlines() if "@" not in ln and ln.strip()]
+    assert not bad, bad

@@ -272,9 +272,9 @@ int main(int argc, char** argv) {
         printf("%-30s %8.2f us  %7.1f GB/s  bitexact=%d\n", v.name, t, upd_bytes / t / 1e3, ok);
     }
     // fused variants vs production fused
-    reset(); launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr, nullptr); snapshot(rt, rd, rm);
+    reset(); launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr); snapshot(rt, rd, rm);
     std::vector<V> fs = {
-        {"F0 fused (prod)", [&] { launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr, nullptr); }},
+        {"F0 fused (prod)", [&] { launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr); }},
         {"F2 fused flat", [&] { k_fused_flat<true><<<(int)((((n + 7) >> 3) + kThreads - 1) / kThreads), kThreads>>>(g, n, 1024.f, c, th, d, m, st); }},
         {"F3 fused tma TE2048 S6", [&] {
              k_stream_tma<true, true, 2048, 6><<<sms, kTmaThreads, 6 * tma_stage_bytes<true, 2048>()>>>(g, n, 1024.f, c, th, d, m, nullptr, st); }},
