@@ -144,5 +144,5 @@ def test_no_oracle_in_product_path():
 
 def test_no_undefined_library_symbols():
     out = subprocess.run(["nm", "-D", "--undefined-only", L.LIB_PATH], capture_output=True, text=True).stdout
-    bad = [ln for ln in out.splitlines() if "@" not in ln and ln.strip()]
+    bad = [ln for ln in out.splitlines() if " U " in ln and "@" not in ln]   # weak (w) refs are fine
     assert not bad, bad
