@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="do not record per-kernel events")
+    p.add_argument("--trace", action="store_true", help="N>1: %%globaltimer trace of the profile pass")
     return p.parse_args()
 
 
@@ -302,7 +303,22 @@ def main():
     # 2) the same K steps again with CUDA events around every kernel (per-kernel roofline)
     prof = {}
     if not args.no_profile:
+        if args.trace and world > 1:
+            L.lmsgd_trace_enable(ctx, args.steps)
         ms_prof, prof = timed(True)
+    trace = None
+    if args.trace and world > 1 and not args.no_profile:
+        import statistics
+        tr = L.lmsgd_trace_read(ctx, args.steps)
+        segs = {"pack": ("pack_start", "pack_end"), "wait_A": ("reduce_start", "reduce_go"),
+                "reduce": ("reduce_go", "reduce_end"), "reduce_to_update": ("reduce_end", "update_start"),
+                "wait_B": ("update_start", "update_go"), "update": ("update_go", "update_end"),
+                "step": ("pack_start", "update_end")}
+        mine = {k: statistics.median((t[b] - t[a]) / 1e3 for t in tr[len(tr) // 4:]) for k, (a, b) in segs.items()}
+        allr = [None] * world
+        dist.all_gather_object(allr, mine)
+        trace = {"us_median_per_rank": allr}
+        L.lmsgd_trace_enable(ctx, 0)
     ms_per_step = ms / args.steps
     global_steps_per_s = 1e3 / ms_per_step
     value = global_steps_per_s * world
@@ -404,6 +420,7 @@ def main():
             "roofline": roofline, "phases": phases, "nvlink": nvlink, "cpu_baseline": cpu, "e2e": e2e,
             "clocks": ck, "gpu_launches": kernels_per_step * args.steps,
             "profile_pass_ms_per_step": (ms_prof / args.steps) if prof else None,
+            "trace": trace,
         }
         print(json.dumps(line), flush=True)
     L.lmsgd_finalize(ctx)

@@ -40,6 +40,9 @@ struct lmsgd_ctx {
     std::vector<cudaEvent_t> pool;
     std::vector<Rec> recs;
     size_t prof_cap = 0;
+    // tracing (lmsgd_trace_enable): TR_WORDS stamps per step, ring of trace_cap steps
+    int64_t* d_trace = nullptr;
+    int64_t trace_cap = 0, trace_steps = 0;
 };
 
 namespace {
@@ -147,6 +150,11 @@ lmsgd::XArgs xargs(lmsgd_ctx* c, uint32_t epoch) {
     x.n = c->n;
     x.timeout_ns = c->timeout_ns;
     x.ticket = c->tickets;
+    x.trace = nullptr;
+    if (c->d_trace) {
+        x.trace = c->d_trace + (c->trace_steps % c->trace_cap) * lmsgd::TR_WORDS;
+        ++c->trace_steps;
+    }
     return x;
 }
 
@@ -307,6 +315,7 @@ lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
         if (c->tickets) cudaFree(c->tickets);
         if (c->last) cudaFree(c->last);
         if (c->d_grads) cudaFree(c->d_grads);
+        if (c->d_trace) cudaFree(c->d_trace);
         for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
         for (auto e : c->pool) cudaEventDestroy(e);
     }
@@ -387,7 +396,8 @@ lmsgd_status lmsgd_bn_stats_allreduce(lmsgd_ctx* c, void* stream, float* mean, f
     if (c->world == 1) return LMSGD_OK;  // the average of one worker is itself
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const lmsgd::XArgs x = xargs(c, ++c->bn_calls);
+    lmsgd::XArgs x = xargs(c, ++c->bn_calls);
+    if (x.trace) { x.trace = nullptr; --c->trace_steps; }
     CK(c, lmsgd::launch_bn_stage(s, x, mean, var, C));
     CK(c, lmsgd::launch_bn_reduce(s, x, mean, var, C));
     return LMSGD_OK;
@@ -423,6 +433,32 @@ lmsgd_status lmsgd_profile_read(lmsgd_ctx* c, double* ms, int64_t* launches) {
         c->pool.push_back(r.b);
     }
     c->recs.clear();
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_trace_enable(lmsgd_ctx* c, int64_t max_steps) {
+    if (!c || max_steps < 0 || max_steps > (int64_t(1) << 20))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "trace_enable: bad argument");
+    DeviceGuard g(c->device);
+    CK(c, cudaDeviceSynchronize());
+    if (c->d_trace) { cudaFree(c->d_trace); c->d_trace = nullptr; }
+    c->trace_cap = max_steps;
+    c->trace_steps = 0;
+    if (max_steps > 0) {
+        CK(c, cudaMalloc(&c->d_trace, max_steps * lmsgd::TR_WORDS * sizeof(int64_t)));
+        CK(c, cudaMemset(c->d_trace, 0, max_steps * lmsgd::TR_WORDS * sizeof(int64_t)));
+    }
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_trace_read(lmsgd_ctx* c, int64_t* out, int64_t max_steps, int64_t* steps) {
+    if (!c || !out || !steps || max_steps < 0) return fail(c, LMSGD_ERR_INVALID_ARG, "trace_read: bad argument");
+    DeviceGuard g(c->device);
+    CK(c, cudaDeviceSynchronize());
+    const int64_t have = c->trace_steps < c->trace_cap ? c->trace_steps : c->trace_cap;
+    *steps = have < max_steps ? have : max_steps;
+    if (*steps > 0)
+        CK(c, cudaMemcpy(out, c->d_trace, *steps * lmsgd::TR_WORDS * sizeof(int64_t), cudaMemcpyDeviceToHost));
     return LMSGD_OK;
 }
 

@@ -291,6 +291,10 @@ __device__ __forceinline__ int64_t* status_of(const XArgs& x, int owner) {
     return reinterpret_cast<int64_t*>(x.peers.base[owner] + x.lay.off_status) + x.parity * ST_WORDS;
 }
 
+__device__ __forceinline__ void stamp(const XArgs& x, int which) {
+    if (x.trace) x.trace[which] = (int64_t)globaltimer();
+}
+
 // Every block: wait until all ranks have published `which` for this epoch.
 // Returns false (and records LMSGD_ERR_TIMEOUT locally) on timeout.
 __device__ bool block_wait(const XArgs& x, int which) {
@@ -357,6 +361,7 @@ __device__ __forceinline__ bool map_unit(const XArgs& x, int64_t u, int& owner, 
 // Pack this rank's gradient and push each shard straight into its owner's receive
 // slot (peer stores over NVLink), interleaved over owners.
 __global__ void __launch_bounds__(kThreads) k_pack_push(XArgs x, const float* __restrict__ g, float s) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_PACK_START);
     int64_t first = kNone;
     unsigned sat = 0;
     const int64_t gsh = x.lay.shard >> 3;
@@ -374,13 +379,18 @@ __global__ void __launch_bounds__(kThreads) k_pack_push(XArgs x, const float* __
         *reinterpret_cast<uint4*>(dst) = pack8(xv, s, j0, first, sat);
     }
     flush_status(first, sat, status_of(x, x.rank), ST_PACK_SAT);
-    grid_signal(x, FLAG_A);
+    if (grid_last(x, FLAG_A)) {
+        stamp(x, TR_PACK_END);
+        publish(x, FLAG_A);
+    }
 }
 
 // Owner-computes reduce of this rank's shard: exact fp64 sum of the world slots in
 // rank order, one saturating RNE rounding (the fp16 all-reduce SUM, R9/R10).
 __global__ void __launch_bounds__(kThreads) k_reduce_shard(XArgs x) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_RED_START);
     if (!block_wait(x, FLAG_A)) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_RED_GO);
     const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
     uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
     unsigned sat = 0;
@@ -418,6 +428,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_shard(XArgs x) {
         mine[ST_G_PACK_SAT] = psat;
         mine[ST_G_ERROR] = err;
         __threadfence_system();
+        stamp(x, TR_RED_END);
         publish(x, FLAG_B);
     }
 }
@@ -428,10 +439,12 @@ template <bool RMS>
 __global__ void __launch_bounds__(kThreads) k_update_gather(XArgs x, UpdConst c, float* __restrict__ th,
                                                             float* __restrict__ d, float* __restrict__ m,
                                                             int64_t* last) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_UPD_START);
     if (!block_wait(x, FLAG_B)) {
         write_last(last, kNone, 0, 0, (int64_t)LMSGD_ERR_TIMEOUT, 1);
         return;
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_UPD_GO);
     const volatile int64_t* mine = status_of(x, x.rank);  // decision written by this rank's reduce
     const int64_t g_first = mine[ST_G_FIRST], g_err = mine[ST_G_ERROR];
     const bool skip = g_first != kNone || g_err != 0;
@@ -457,6 +470,14 @@ __global__ void __launch_bounds__(kThreads) k_update_gather(XArgs x, UpdConst c,
         const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
         const uint4 r = *reinterpret_cast<const uint4*>(Rp);
         update8<RMS>(r, j0, x.n, c, th, d, m);
+    }
+    if (x.trace) {  // end stamp: last block (ticket 3), trace mode only
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0 && atomicAdd(x.ticket + 3, 1u) == gridDim.x - 1) {
+            x.ticket[3] = 0;
+            stamp(x, TR_UPD_END);
+        }
     }
 }
 

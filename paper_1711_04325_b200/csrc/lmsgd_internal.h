@@ -75,7 +75,12 @@ struct XArgs {
     int64_t n;
     int64_t timeout_ns;
     unsigned int* ticket;
+    int64_t* trace;      // NULL, or this step's TR_WORDS %globaltimer stamps (lmsgd_trace_enable)
 };
+
+// Trace stamps of one world > 1 step (ns, this GPU's %globaltimer).
+enum { TR_PACK_START = 0, TR_PACK_END, TR_RED_START, TR_RED_GO, TR_RED_END, TR_UPD_START, TR_UPD_GO,
+       TR_UPD_END, TR_WORDS };
 cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,
                              float scale);
 cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x);

@@ -81,6 +81,8 @@ def _load() -> ctypes.CDLL:
         "lmsgd_query_status": (I32, [P, ctypes.POINTER(StepStatus)]),
         "lmsgd_profile_enable": (I32, [P, I64]),
         "lmsgd_profile_read": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]),
+        "lmsgd_trace_enable": (I32, [P, I64]),
+        "lmsgd_trace_read": (I32, [P, ctypes.POINTER(I64), I64, ctypes.POINTER(I64)]),
         "lmsgd_status_reset": (I32, [P, P]),
         "lmsgd_pack": (I32, [P, P, I64, I64, F32, P, P]),
         "lmsgd_reduce_local": (I32, [P, P, I32, I64, P, P]),
@@ -291,6 +293,22 @@ def lmsgd_profile_read(ctx: Context) -> dict:
     n = (ctypes.c_int64 * 3)()
     _check(_lib.lmsgd_profile_read(ctx.ptr, ms, n), ctx)
     return {PHASES[i]: (ms[i], n[i]) for i in range(3)}
+
+
+TRACE_FIELDS = ("pack_start", "pack_end", "reduce_start", "reduce_go", "reduce_end",
+                "update_start", "update_go", "update_end")
+
+
+def lmsgd_trace_enable(ctx: Context, max_steps: int):
+    _check(_lib.lmsgd_trace_enable(ctx.ptr, int(max_steps)), ctx)
+
+
+def lmsgd_trace_read(ctx: Context, max_steps: int):
+    """List of per-step dicts {field: ns} (world > 1 steps only)."""
+    buf = (ctypes.c_int64 * (8 * max_steps))()
+    got = ctypes.c_int64()
+    _check(_lib.lmsgd_trace_read(ctx.ptr, buf, int(max_steps), ctypes.byref(got)), ctx)
+    return [dict(zip(TRACE_FIELDS, buf[8 * i:8 * i + 8])) for i in range(got.value)]
 
 
 # ------------------------------------------------------------------ sub-steps
