@@ -310,10 +310,12 @@ def main():
     if args.trace and world > 1 and not args.no_profile:
         import statistics
         tr = L.lmsgd_trace_read(ctx, args.steps)
-        segs = {"pack": ("pack_start", "pack_end"), "wait_A": ("reduce_start", "reduce_go"),
-                "reduce": ("reduce_go", "reduce_end"), "reduce_to_update": ("reduce_end", "update_start"),
-                "wait_B": ("update_start", "update_go"), "update": ("update_go", "update_end"),
-                "step": ("pack_start", "update_end")}
+        # stamps: pack_start, pack_end, (all packs seen), reduce start, reduce end,
+        # (all reduces seen), update start, update end -- see lmsgd_trace_enable
+        segs = {"pack": ("pack_start", "pack_end"), "wait_A": ("pack_end", "reduce_start"),
+                "gap_A": ("reduce_start", "reduce_go"), "reduce": ("reduce_go", "reduce_end"),
+                "wait_B": ("reduce_end", "update_start"), "gap_B": ("update_start", "update_go"),
+                "update": ("update_go", "update_end"), "step": ("pack_start", "update_end")}
         mine = {k: statistics.median((t[b] - t[a]) / 1e3 for t in tr[len(tr) // 4:]) for k, (a, b) in segs.items()}
         allr = [None] * world
         dist.all_gather_object(allr, mine)

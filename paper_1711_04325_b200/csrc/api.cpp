@@ -85,6 +85,7 @@ lmsgd::Launch launch_for_current_device() {
     cudaDeviceGetAttribute(&L.sm_count, cudaDevAttrMultiProcessorCount, dev);
     L.grid_cap_stream = L.sm_count * lmsgd::stream_blocks_per_sm();
     L.grid_cap_push = L.sm_count * lmsgd::push_blocks_per_sm();
+    L.grid_cap_reduce = L.sm_count * lmsgd::reduce_blocks_per_sm();
     if (dev >= 0 && dev < 64) { cache[dev] = L; have[dev] = true; }
     return L;
 }

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "lmsgd_internal.h"
 
 namespace lmsgd {
@@ -46,6 +48,15 @@ __device__ __forceinline__ unsigned short sat16_f64(double a, unsigned& sat) {
     if (fabs(a) > 65504.0) ++sat;
     a = fmin(fmax(a, -65504.0), 65504.0);
     return __half_as_ushort(__double2half(a));
+}
+
+// Programmatic dependent launch (sm_90+): every product kernel lets the next kernel
+// in the stream be scheduled immediately and waits for its own predecessors to
+// complete (and their memory to be visible) before touching any data.  This hides
+// the launch latency between the step's kernels without changing their ordering.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {
@@ -200,6 +211,7 @@ __global__ void k_status_reset(int64_t* st, int words) {
 __global__ void __launch_bounds__(kThreads) k_pack(const float* __restrict__ g, int64_t n,
                                                    int64_t n_pad, float s, uint16_t* __restrict__ h,
                                                    int64_t* st) {
+    pdl_enter();
     int64_t first = kNone;
     unsigned sat = 0;
     const int64_t nv = n_pad >> 3;
@@ -215,6 +227,7 @@ __global__ void __launch_bounds__(kThreads) k_pack(const float* __restrict__ g, 
 __global__ void __launch_bounds__(kThreads) k_reduce_local(const uint16_t* __restrict__ h, int k,
                                                            int64_t n_pad, uint16_t* __restrict__ R,
                                                            int64_t* st) {
+    pdl_enter();
     unsigned sat = 0;
     const int64_t nv = n_pad >> 3;
     for (int64_t v = gtid(); v < nv; v += gstride()) {
@@ -241,6 +254,7 @@ __global__ void __launch_bounds__(kThreads) k_update(const uint16_t* __restrict_
                                                      float* __restrict__ th, float* __restrict__ d,
                                                      float* __restrict__ m, const int64_t* st,
                                                      int64_t* st_reset, int64_t* last) {
+    pdl_enter();
     int64_t first = kNone, psat = 0, ssat = 0, err = 0;
     if (st) { first = st[ST_FIRST]; psat = st[ST_PACK_SAT]; ssat = st[ST_SUM_SAT]; err = st[ST_ERROR]; }
     const bool skip = first != kNone || err != 0;
@@ -262,6 +276,7 @@ __global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g
                                                      UpdConst c, float* __restrict__ th,
                                                      float* __restrict__ d, float* __restrict__ m,
                                                      int64_t* st, int64_t* st_reset) {
+    pdl_enter();
     reset_status(st_reset);
     int64_t first = kNone;
     unsigned sat = 0;
@@ -279,6 +294,7 @@ __global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g
 // Publishes the fused step's status (never skipped) into the public `last` record.
 // A separate 1-warp launch: a per-block fence + ticket in k_fused1 cost 16% of it.
 __global__ void k_finalize_fused(const int64_t* st, int64_t* last) {
+    pdl_enter();
     if (threadIdx.x == 0) store_last(last, st[ST_FIRST], st[ST_PACK_SAT], st[ST_SUM_SAT], st[ST_ERROR], 0);
 }
 
@@ -344,6 +360,34 @@ __device__ void grid_signal(const XArgs& x, int which) {
     if (grid_last(x, which)) publish(x, which);
 }
 
+// One thread: wait until every rank has published `which` for this epoch (bounded
+// spin; on timeout record LMSGD_ERR_TIMEOUT in this rank's words and return false).
+__device__ bool thread_wait_all(const XArgs& x, int which) {
+    const uint64_t t0 = globaltimer();
+    for (int p = 0; p < x.world; ++p) {
+        const uint32_t* f = flag_slot(x, x.rank, which) + p;
+        while ((int32_t)(ld_acquire_sys(f) - x.epoch) < 0) {
+            __nanosleep(64);
+            if ((int64_t)(globaltimer() - t0) > x.timeout_ns) {
+                int64_t* mine = status_of(x, x.rank);
+                mine[ST_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+                mine[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+                __threadfence_system();
+                return false;
+            }
+        }
+    }
+    __threadfence_system();
+    return true;
+}
+
+// Cross-GPU ordering of the three exchange kernels.  Each kernel's last block
+// (ticket) releases its flag to every rank and then waits until every rank has
+// released the same flag; only then does the kernel end.  The next kernel in the
+// stream therefore starts after all ranks finished the previous phase, with no
+// per-block waits: kernel completion orders the acquired peer writes before every
+// later access on this GPU (L1 is invalidated at each launch; peer loads bypass L2).
+
 // Work units of the exchange kernels: a unit is kThreads consecutive 8-element groups
 // of one shard.  Units are interleaved over owners -- unit u belongs to owner
 // (u + rank) % world -- so that the blocks in flight on every rank touch all owners
@@ -359,8 +403,11 @@ __device__ __forceinline__ bool map_unit(const XArgs& x, int64_t u, int& owner, 
 }
 
 // Pack this rank's gradient and push each shard straight into its owner's receive
-// slot (peer stores over NVLink), interleaved over owners.
+// slot (peer stores over NVLink), interleaved over owners.  Persistent grid: one
+// system-scope fence per resident block.  The last block also computes the global
+// skip decision once every rank's pack status is final.
 __global__ void __launch_bounds__(kThreads) k_pack_push(XArgs x, const float* __restrict__ g, float s) {
+    pdl_enter();
     if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_PACK_START);
     int64_t first = kNone;
     unsigned sat = 0;
@@ -382,14 +429,32 @@ __global__ void __launch_bounds__(kThreads) k_pack_push(XArgs x, const float* __
     if (grid_last(x, FLAG_A)) {
         stamp(x, TR_PACK_END);
         publish(x, FLAG_A);
+        if (thread_wait_all(x, FLAG_A)) {
+            // Global skip decision from every rank's (final) pack status; identical
+            // inputs on every rank -> identical decision.
+            int64_t gfirst = kNone, psat = 0, err = 0;
+            for (int p = 0; p < x.world; ++p) {
+                const volatile int64_t* sp = status_of(x, p);
+                const int64_t f = sp[ST_FIRST];
+                gfirst = f < gfirst ? f : gfirst;
+                psat += sp[ST_PACK_SAT];
+                err = err ? err : sp[ST_ERROR];
+            }
+            int64_t* mine = status_of(x, x.rank);
+            mine[ST_G_FIRST] = gfirst;
+            mine[ST_G_PACK_SAT] = psat;
+            mine[ST_G_ERROR] = err;
+        }
+        stamp(x, TR_RED_START);   // = all ranks' packs observed
     }
 }
 
 // Owner-computes reduce of this rank's shard: exact fp64 sum of the world slots in
 // rank order, one saturating RNE rounding (the fp16 all-reduce SUM, R9/R10).
+// Persistent grid (one fence per resident block); the last block releases B, waits
+// for every rank's B and totals the wire-2 saturation counts.
 __global__ void __launch_bounds__(kThreads) k_reduce_shard(XArgs x) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_RED_START);
-    if (!block_wait(x, FLAG_A)) return;
+    pdl_enter();
     if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_RED_GO);
     const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
     uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
@@ -413,45 +478,31 @@ __global__ void __launch_bounds__(kThreads) k_reduce_shard(XArgs x) {
     }
     flush_status(kNone, sat, status_of(x, x.rank), ST_SUM_SAT);
     if (grid_last(x, FLAG_B)) {
-        // Global skip decision from every rank's pack status (final: all ranks have
-        // published FLAG_A).  Identical inputs on every rank -> identical decision.
-        int64_t first = kNone, psat = 0, err = 0;
-        for (int p = 0; p < x.world; ++p) {
-            const volatile int64_t* sp = status_of(x, p);
-            const int64_t f = sp[ST_FIRST];
-            first = f < first ? f : first;
-            psat += sp[ST_PACK_SAT];
-            err = err ? err : sp[ST_ERROR];
-        }
-        int64_t* mine = status_of(x, x.rank);
-        mine[ST_G_FIRST] = first;
-        mine[ST_G_PACK_SAT] = psat;
-        mine[ST_G_ERROR] = err;
-        __threadfence_system();
         stamp(x, TR_RED_END);
         publish(x, FLAG_B);
+        if (thread_wait_all(x, FLAG_B)) {
+            int64_t ssat = 0;
+            for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, p))[ST_SUM_SAT];
+            status_of(x, x.rank)[ST_G_SUM_SAT] = ssat;
+        }
+        stamp(x, TR_UPD_START);   // = all ranks' reduces observed
     }
 }
 
 // Update with the all-gather fused in: each element's R is loaded from its owner's
-// shard (peer loads over NVLink for remote shards), rotated per rank.
+// shard (peer loads over NVLink for remote shards), owner-interleaved units.  Flat
+// grid, no waits: the previous kernel ended only after every rank's reduce.
 template <bool RMS>
 __global__ void __launch_bounds__(kThreads) k_update_gather(XArgs x, UpdConst c, float* __restrict__ th,
                                                             float* __restrict__ d, float* __restrict__ m,
                                                             int64_t* last) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_UPD_START);
-    if (!block_wait(x, FLAG_B)) {
-        write_last(last, kNone, 0, 0, (int64_t)LMSGD_ERR_TIMEOUT, 1);
-        return;
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_UPD_GO);
-    const volatile int64_t* mine = status_of(x, x.rank);  // decision written by this rank's reduce
+    pdl_enter();
+    const int64_t* mine = status_of(x, x.rank);  // decision written by this rank's pack / reduce
     const int64_t g_first = mine[ST_G_FIRST], g_err = mine[ST_G_ERROR];
     const bool skip = g_first != kNone || g_err != 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && last) {
-        int64_t ssat = 0;
-        for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, p))[ST_SUM_SAT];
-        store_last(last, g_first, mine[ST_G_PACK_SAT], ssat, g_err, skip);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        stamp(x, TR_UPD_GO);
+        if (last) store_last(last, g_first, mine[ST_G_PACK_SAT], mine[ST_G_SUM_SAT], g_err, skip);
     }
     if (blockIdx.x == 0 && threadIdx.x < ST_WORDS) {  // next step's status slot
         int64_t* nxt = reinterpret_cast<int64_t*>(x.peers.base[x.rank] + x.lay.off_status) +
@@ -520,9 +571,31 @@ int grid_for(const Launch&, int64_t work_items) {
 
 // ------------------------------------------------------------------ launchers
 
+// Launch with the programmatic-stream-serialization attribute (see pdl_enter).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3((unsigned)block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 int push_blocks_per_sm() {
     int b = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pack_push, kThreads, 0);
+    return b > 0 ? b : 1;
+}
+
+int reduce_blocks_per_sm() {
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_reduce_shard, kThreads, 0);
     return b > 0 ? b : 1;
 }
 
@@ -544,14 +617,12 @@ cudaError_t launch_status_reset(cudaStream_t s, int64_t* st) {
 
 cudaError_t launch_pack(cudaStream_t s, const Launch& L, const float* g, int64_t n, int64_t n_pad,
                         float scale, uint16_t* h, int64_t* st) {
-    k_pack<<<grid_for(L, n_pad >> 3), kThreads, 0, s>>>(g, n, n_pad, scale, h, st);
-    return cudaGetLastError();
+    return launch_pdl(k_pack, grid_for(L, n_pad >> 3), kThreads, s, g, n, n_pad, scale, h, st);
 }
 
 cudaError_t launch_reduce_local(cudaStream_t s, const Launch& L, const uint16_t* h, int k,
                                 int64_t n_pad, uint16_t* R, int64_t* st) {
-    k_reduce_local<<<grid_for(L, n_pad >> 3), kThreads, 0, s>>>(h, k, n_pad, R, st);
-    return cudaGetLastError();
+    return launch_pdl(k_reduce_local, grid_for(L, n_pad >> 3), kThreads, s, h, k, n_pad, R, st);
 }
 
 cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, int64_t n,
@@ -559,22 +630,19 @@ cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, in
                           int64_t* st_reset, int64_t* last) {
     const int grid = grid_for(L, (n + 7) >> 3);
     if (c.a_rms != 0.0f)
-        k_update<true><<<grid, kThreads, 0, s>>>(R, n, c, th, d, m, st, st_reset, last);
+        return launch_pdl(k_update<true>, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last);
     else
-        k_update<false><<<grid, kThreads, 0, s>>>(R, n, c, th, d, m, st, st_reset, last);
-    return cudaGetLastError();
+        return launch_pdl(k_update<false>, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last);
 }
 
 cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                           const UpdConst& c, float* th, float* d, float* m, int64_t* st,
-                          int64_t* st_reset, int64_t* last) {
+                          int64_t* st_reset, int64_t* /*last: see launch_finalize_fused*/) {
     const int grid = grid_for(L, (n + 7) >> 3);
     if (c.a_rms != 0.0f)
-        k_fused1<true><<<grid, kThreads, 0, s>>>(g, n, scale, c, th, d, m, st, st_reset);
+        return launch_pdl(k_fused1<true>, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset);
     else
-        k_fused1<false><<<grid, kThreads, 0, s>>>(g, n, scale, c, th, d, m, st, st_reset);
-    (void)last;
-    return cudaGetLastError();
+        return launch_pdl(k_fused1<false>, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset);
 }
 
 // Persistent grid for the push: the system-scope fence each block issues before the
@@ -587,31 +655,29 @@ int64_t host_units(const XArgs& x) {
 }
 
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last) {
-    k_finalize_fused<<<1, 32, 0, s>>>(st, last);
-    return cudaGetLastError();
+    return launch_pdl(k_finalize_fused, 1, 32, s, st, last);
 }
 
 cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,
                              float scale) {
     int64_t blocks = host_units(x);
     if (blocks > L.grid_cap_push) blocks = L.grid_cap_push;
-    k_pack_push<<<(int)blocks, kThreads, 0, s>>>(x, g, scale);
-    return cudaGetLastError();
+    return launch_pdl(k_pack_push, (int)blocks, kThreads, s, x, g, scale);
 }
 
 cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x) {
-    k_reduce_shard<<<grid_for(L, x.lay.shard >> 3), kThreads, 0, s>>>(x);
-    return cudaGetLastError();
+    int64_t blocks = ((x.lay.shard >> 3) + kThreads - 1) / kThreads;
+    if (blocks > L.grid_cap_reduce) blocks = L.grid_cap_reduce;   // persistent: one fence per block
+    return launch_pdl(k_reduce_shard, (int)blocks, kThreads, s, x);
 }
 
 cudaError_t launch_update_gather(cudaStream_t s, const Launch& L, const XArgs& x, const UpdConst& c,
                                  float* th, float* d, float* m, int64_t* last) {
     const int grid = (int)host_units(x);  // flat: one unit per block
     if (c.a_rms != 0.0f)
-        k_update_gather<true><<<grid, kThreads, 0, s>>>(x, c, th, d, m, last);
+        return launch_pdl(k_update_gather<true>, grid, kThreads, s, x, c, th, d, m, last);
     else
-        k_update_gather<false><<<grid, kThreads, 0, s>>>(x, c, th, d, m, last);
-    return cudaGetLastError();
+        return launch_pdl(k_update_gather<false>, grid, kThreads, s, x, c, th, d, m, last);
 }
 
 cudaError_t launch_bn_stage(cudaStream_t s, const XArgs& x, const float* mean, const float* var,

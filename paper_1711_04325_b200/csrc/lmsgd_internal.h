@@ -15,7 +15,7 @@ constexpr int64_t kNone = INT64_MAX;  // "no non-finite index" in device status 
 // error} that the rank's reduce computes from every rank's words.  The public
 // sub-step status (lmsgd_status_reset) is the first four words.
 enum { ST_FIRST = 0, ST_PACK_SAT = 1, ST_SUM_SAT = 2, ST_ERROR = 3,
-       ST_G_FIRST = 4, ST_G_PACK_SAT = 5, ST_G_ERROR = 6, ST_WORDS = 8 };
+       ST_G_FIRST = 4, ST_G_PACK_SAT = 5, ST_G_ERROR = 6, ST_G_SUM_SAT = 7, ST_WORDS = 8 };
 
 // fp32 constants of the update, each rounded once from double (R15).
 struct UpdConst {
@@ -47,6 +47,7 @@ struct Launch {
     int sm_count;
     int grid_cap_stream;   // SMs x resident blocks of the streaming kernels (informational)
     int grid_cap_push;     // SMs x resident blocks of k_pack_push (persistent grid)
+    int grid_cap_reduce;   // SMs x resident blocks of k_reduce_shard (persistent grid)
 };
 
 // ---- single-GPU building blocks (sub-step ABI and world == 1)
@@ -64,6 +65,7 @@ cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last);
 int stream_blocks_per_sm();
 int push_blocks_per_sm();
+int reduce_blocks_per_sm();
 
 // ---- world > 1 exchange over peer memory (NVLink / NVSwitch)
 struct XArgs {
@@ -78,7 +80,9 @@ struct XArgs {
     int64_t* trace;      // NULL, or this step's TR_WORDS %globaltimer stamps (lmsgd_trace_enable)
 };
 
-// Trace stamps of one world > 1 step (ns, this GPU's %globaltimer).
+// Trace stamps of one world > 1 step (ns, this GPU's %globaltimer): pack start,
+// pack end (its last block), all ranks' packs observed, reduce start, reduce end,
+// all ranks' reduces observed, update start, update end.
 enum { TR_PACK_START = 0, TR_PACK_END, TR_RED_START, TR_RED_GO, TR_RED_END, TR_UPD_START, TR_UPD_GO,
        TR_UPD_END, TR_WORDS };
 cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,

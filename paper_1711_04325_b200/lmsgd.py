@@ -295,6 +295,9 @@ def lmsgd_profile_read(ctx: Context) -> dict:
     return {PHASES[i]: (ms[i], n[i]) for i in range(3)}
 
 
+# pack start, pack end, all ranks' packs observed (reduce_start), reduce kernel start
+# (reduce_go), reduce end, all ranks' reduces observed (update_start), update kernel
+# start (update_go), update end
 TRACE_FIELDS = ("pack_start", "pack_end", "reduce_start", "reduce_go", "reduce_end",
                 "update_start", "update_go", "update_end")
 

@@ -1,0 +1,150 @@
+// Multi-GPU exchange-kernel micro-benchmark (development tool): one process drives
+// every visible GPU (<= 8) with peer access; data is static, so no flags are needed.
+// Measures the phases of the world > 1 step in isolation, all GPUs concurrently.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I include \
+//        -I paper_1711_04325_b200/csrc tools/xbench.cu -o tools/xbench
+#include "../paper_1711_04325_b200/csrc/kernels.cu"
+
+#include <cstdio>
+#include <cstdlib>
+#include <functional>
+#include <vector>
+
+using namespace lmsgd;
+
+#define CKE(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("CUDA %s at %d\n", cudaGetErrorString(e), __LINE__); exit(1);} } while (0)
+
+namespace xb {
+
+// exact reduce with integer accumulation: fp16 -> fixed point (units of 2^-24)
+__device__ __forceinline__ long long h2fix(uint32_t b) {
+    const int e = (b >> 10) & 31;
+    const long long f = b & 1023;
+    long long v = e ? ((1024 + f) << (e - 1)) : f;
+    return (b & 0x8000) ? -v : v;
+}
+
+template <int MODE>   // 0: fp64 flat (production arithmetic), 1: int64 flat, 2: int64 persistent
+__global__ void __launch_bounds__(256) k_reduce(const uint16_t* __restrict__ recv, int k, int64_t shard,
+                                                uint16_t* __restrict__ R) {
+    const int64_t nv = shard >> 3;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv; v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j0 = v << 3;
+        unsigned short o[8];
+        unsigned sat = 0;
+        if (MODE == 0) {
+            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int p = 0; p < k; ++p) {
+                const uint4 q = *reinterpret_cast<const uint4*>(recv + (int64_t)p * shard + j0);
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
+        } else {
+            long long acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int p = 0; p < k; ++p) {
+                const uint4 q = *reinterpret_cast<const uint4*>(recv + (int64_t)p * shard + j0);
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] += h2fix((e & 1) ? (w[e >> 1] >> 16) : (w[e >> 1] & 0xffff));
+            }
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = sat16_f64((double)acc[e] * 0x1p-24, sat);
+        }
+        *reinterpret_cast<uint4*>(R + j0) = make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
+                                                      o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
+    }
+}
+
+struct Ptrs { const uint16_t* R[8]; };
+
+// update with R pulled from owners (interleaved units), like k_update_gather minus the flags
+__global__ void __launch_bounds__(256) k_upd_pull(Ptrs P, int world, int rank, int64_t shard, int64_t n, UpdConst c,
+                                                  float* __restrict__ th, float* __restrict__ d, float* __restrict__ m) {
+    const int64_t gsh = shard >> 3;
+    const int64_t ups = (gsh + 255) / 256;
+    const int64_t u = blockIdx.x;
+    const int owner = (int)((u % world + rank) % world);
+    const int64_t gi = (u / world) * 256 + threadIdx.x;
+    if (gi >= gsh) return;
+    const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+    if (j0 >= n) return;
+    (void)ups;
+    const uint4 r = *reinterpret_cast<const uint4*>(P.R[owner] + (gi << 3));
+    update8<true>(r, j0, n, c, th, d, m);
+}
+
+// all-gather push: owner writes its R shard into every rank's full-R buffer (persistent)
+__global__ void __launch_bounds__(256) k_ag_push(const uint16_t* __restrict__ Rmine, uint16_t* const* full, int world,
+                                                 int rank, int64_t shard) {
+    const int64_t nv = shard >> 3;
+    for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < nv * world; v += (int64_t)gridDim.x * blockDim.x) {
+        const int p = (int)((v / nv + rank) % world);   // rotate destinations
+        const int64_t i = v % nv;
+        const uint4 q = reinterpret_cast<const uint4*>(Rmine)[i];
+        reinterpret_cast<uint4*>(full[p] + (int64_t)rank * shard)[i] = q;
+    }
+    __threadfence_system();
+}
+
+}  // namespace xb
+
+int main(int argc, char** argv) {
+    int ndev; CKE(cudaGetDeviceCount(&ndev));
+    const int W = ndev > 8 ? 8 : ndev;
+    const int64_t n = 25557032;
+    int64_t shard = ((n + W - 1) / W + 63) / 64 * 64;
+    const int64_t n_pad = shard * W;
+    printf("world=%d n=%lld shard=%lld\n", W, (long long)n, (long long)shard);
+    std::vector<float*> th(W), d(W), m(W), g(W);
+    std::vector<uint16_t*> recv(W), R(W), full(W);
+    std::vector<uint16_t**> fullp(W);
+    std::vector<cudaStream_t> st(W);
+    std::vector<cudaEvent_t> e0(W), e1(W);
+    for (int i = 0; i < W; ++i) {
+        CKE(cudaSetDevice(i));
+        for (int j = 0; j < W; ++j) if (j != i) CKE(cudaDeviceEnablePeerAccess(j, 0));
+        CKE(cudaMalloc(&th[i], n * 4)); CKE(cudaMalloc(&d[i], n * 4)); CKE(cudaMalloc(&m[i], n * 4)); CKE(cudaMalloc(&g[i], n * 4));
+        CKE(cudaMemset(th[i], 0, n * 4)); CKE(cudaMemset(d[i], 0, n * 4)); CKE(cudaMemset(m[i], 0, n * 4)); CKE(cudaMemset(g[i], 0, n * 4));
+        CKE(cudaMalloc(&recv[i], n_pad * 2)); CKE(cudaMalloc(&R[i], shard * 2)); CKE(cudaMalloc(&full[i], n_pad * 2));
+        CKE(cudaMemset(recv[i], 0x11, n_pad * 2)); CKE(cudaMemset(R[i], 0x22, shard * 2)); CKE(cudaMemset(full[i], 0x22, n_pad * 2));
+        CKE(cudaStreamCreate(&st[i])); cudaEventCreate(&e0[i]); cudaEventCreate(&e1[i]);
+    }
+    for (int i = 0; i < W; ++i) {
+        CKE(cudaSetDevice(i));
+        CKE(cudaMalloc(&fullp[i], 8 * sizeof(uint16_t*)));
+        CKE(cudaMemcpy(fullp[i], full.data(), W * sizeof(uint16_t*), cudaMemcpyHostToDevice));
+    }
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    UpdConst c{0.9f, 0.99f, (float)(1.0 - 0.99), 1e-8f, 6.4f, 0.0091578f, 4.64e-05f, 1.0f / 4096};
+    xb::Ptrs P{};
+    for (int i = 0; i < W; ++i) P.R[i] = R[i];
+    auto run = [&](const char* name, double bytes, const std::function<void(int)>& f) {
+        for (int it = 0; it < 3; ++it) for (int i = 0; i < W; ++i) { cudaSetDevice(i); f(i); }
+        for (int i = 0; i < W; ++i) { cudaSetDevice(i); CKE(cudaDeviceSynchronize()); }
+        const int iters = 30;
+        for (int i = 0; i < W; ++i) { cudaSetDevice(i); cudaEventRecord(e0[i], st[i]); }
+        for (int it = 0; it < iters; ++it) for (int i = 0; i < W; ++i) { cudaSetDevice(i); f(i); }
+        float worst = 0;
+        for (int i = 0; i < W; ++i) { cudaSetDevice(i); cudaEventRecord(e1[i], st[i]); CKE(cudaEventSynchronize(e1[i])); float ms; cudaEventElapsedTime(&ms, e0[i], e1[i]); worst = ms > worst ? ms : worst; }
+        CKE(cudaGetLastError());
+        const double us = worst / iters * 1e3;
+        printf("%-46s %9.2f us  %8.1f GB/s\n", name, us, bytes / us / 1e3);
+    };
+    const Launch L{sms, 0, 0, 0};
+    const int ups = (int)(((shard >> 3) + 255) / 256);
+    // pack (local only) for reference
+    int64_t* dst; CKE(cudaSetDevice(0));
+    run("reduce fp64 flat", 2.0 * n_pad, [&](int i) { xb::k_reduce<0><<<(int)((shard / 8 + 255) / 256), 256, 0, st[i]>>>(recv[i], W, shard, R[i]); });
+    run("reduce int64 flat", 2.0 * n_pad, [&](int i) { xb::k_reduce<1><<<(int)((shard / 8 + 255) / 256), 256, 0, st[i]>>>(recv[i], W, shard, R[i]); });
+    run("reduce int64 persistent 148x8", 2.0 * n_pad, [&](int i) { xb::k_reduce<1><<<sms * 8, 256, 0, st[i]>>>(recv[i], W, shard, R[i]); });
+    run("reduce fp64 persistent 148x8", 2.0 * n_pad, [&](int i) { xb::k_reduce<0><<<sms * 8, 256, 0, st[i]>>>(recv[i], W, shard, R[i]); });
+    run("update pull from owners (flat, interleaved)", 26.0 * n, [&](int i) { xb::k_upd_pull<<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
+    run("update local full R (k_update flat)", 26.0 * n, [&](int i) { launch_update(st[i], L, full[i], n, c, th[i], d[i], m[i], nullptr, nullptr, nullptr); });
+    run("AG push R shard to all (persistent 148x8)", 2.0 * shard * (W - 1), [&](int i) { xb::k_ag_push<<<sms * 8, 256, 0, st[i]>>>(R[i], fullp[i], W, i, shard); });
+    run("AG push + local update", 26.0 * n, [&](int i) { xb::k_ag_push<<<sms * 8, 256, 0, st[i]>>>(R[i], fullp[i], W, i, shard);
+                                                          launch_update(st[i], L, full[i], n, c, th[i], d[i], m[i], nullptr, nullptr, nullptr); });
+    return 0;
+}
