@@ -69,11 +69,17 @@ def measured_peaks():
 
 
 def committed_traffic(kernel: str):
+    """DRAM bytes (read + write) per launch of `kernel` from the committed ncu
+    capture (profiles/traffic.json, written by tools/ncu_summary.py), else None."""
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            return json.load(f).get(kernel)
+            t = json.load(f)
     except Exception:
         return None
+    for name, v in t.items():
+        if name == kernel or name.startswith(kernel + "<"):
+            return v
+    return None
 
 
 # ------------------------------------------------------------------ clocks (NVML)
@@ -371,6 +377,37 @@ def main():
         nvlink["nccl_fp16_allreduce_bus_gbs"] = bus_bytes / (nccl_ms * 1e-3) / 1e9
         del buf
 
+    # config C4: BN last-minibatch statistics average over the ranks (53 layers, 26,560
+    # channels for ResNet-50), latency-bound; device time per call, max over ranks
+    bn = None
+    if world > 1:
+        C = sum(synth.resnet_bn_channels(args.depth))
+        mean = torch.randn(C, device=devc)
+        var = torch.rand(C, device=devc) + 0.1
+        for _ in range(20):
+            L.lmsgd_bn_stats_allreduce(ctx, mean, var)
+        torch.cuda.synchronize()
+        barrier()
+        nb = 1000
+        e0.record(stream)
+        for _ in range(nb):
+            L.lmsgd_bn_stats_allreduce(ctx, mean, var)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bn_us = max_over_ranks(e0.elapsed_time(e1) / nb * 1e3)
+        y = torch.cat([mean, var])
+        for _ in range(20):
+            dist.all_reduce(y)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(200):
+            dist.all_reduce(y)
+            y.mul_(1.0 / world)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        bn = {"channels": C, "bytes": 8 * C, "us_per_call": bn_us,
+              "nccl_fp32_allreduce_plus_scale_us": max_over_ranks(e0.elapsed_time(e1) / 200 * 1e3)}
+
     # e2e through the public host-buffer entry point: H2D of this step's gradient from
     # pinned memory + the whole step + D2H of the step status, every step
     g_host = grads.cpu().pin_memory()
@@ -419,7 +456,8 @@ def main():
                        "l2": f"inputs {inputs_bytes / 1e9:.2f} GB > 126 MB L2 (no flush needed)",
                        "global_steps_per_s": global_steps_per_s,
                        "grad_elems_per_s": global_steps_per_s * world * n},
-            "roofline": roofline, "phases": phases, "nvlink": nvlink, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roofline, "phases": phases, "nvlink": nvlink, "bn_stats_allreduce": bn,
+            "cpu_baseline": cpu, "e2e": e2e,
             "clocks": ck, "gpu_launches": kernels_per_step * args.steps,
             "profile_pass_ms_per_step": (ms_prof / args.steps) if prof else None,
             "trace": trace,

@@ -86,6 +86,10 @@ lmsgd::Launch launch_for_current_device() {
     L.grid_cap_stream = L.sm_count * lmsgd::stream_blocks_per_sm();
     L.grid_cap_push = L.sm_count * lmsgd::push_blocks_per_sm();
     L.grid_cap_reduce = L.sm_count * lmsgd::reduce_blocks_per_sm();
+    // PDL helps the k = 1 pair (128.7 vs 132.3 us) but costs 5-11 us on the world > 1
+    // kernels at k = 4 (early-resident dependents steal SM slots; A/B in DESIGN.md).
+    L.pdl_mask = 0x1;
+    if (const char* m = std::getenv("LMSGD_PDL_MASK")) L.pdl_mask = std::atoi(m);  // diagnostics
     if (dev >= 0 && dev < 64) { cache[dev] = L; have[dev] = true; }
     return L;
 }

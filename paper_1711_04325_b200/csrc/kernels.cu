@@ -573,7 +573,8 @@ int grid_for(const Launch&, int64_t work_items) {
 
 // Launch with the programmatic-stream-serialization attribute (see pdl_enter).
 template <typename... KArgs, typename... Args>
-cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream_t s, Args&&... args) {
+cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), int grid, int block, cudaStream_t s,
+                          Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3((unsigned)block);
@@ -583,9 +584,10 @@ cudaError_t launch_pdl(void (*kernel)(KArgs...), int grid, int block, cudaStream
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = pdl ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+#define launch_pdl(...) launch_pdl_if((L.pdl_mask & 1) != 0, __VA_ARGS__)
 
 int push_blocks_per_sm() {
     int b = 0;
@@ -655,29 +657,29 @@ int64_t host_units(const XArgs& x) {
 }
 
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last) {
-    return launch_pdl(k_finalize_fused, 1, 32, s, st, last);
+    return launch_pdl_if(true, k_finalize_fused, 1, 32, s, st, last);
 }
 
 cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,
                              float scale) {
     int64_t blocks = host_units(x);
     if (blocks > L.grid_cap_push) blocks = L.grid_cap_push;
-    return launch_pdl(k_pack_push, (int)blocks, kThreads, s, x, g, scale);
+    return launch_pdl_if((L.pdl_mask & 2) != 0, k_pack_push, (int)blocks, kThreads, s, x, g, scale);
 }
 
 cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x) {
     int64_t blocks = ((x.lay.shard >> 3) + kThreads - 1) / kThreads;
     if (blocks > L.grid_cap_reduce) blocks = L.grid_cap_reduce;   // persistent: one fence per block
-    return launch_pdl(k_reduce_shard, (int)blocks, kThreads, s, x);
+    return launch_pdl_if((L.pdl_mask & 4) != 0, k_reduce_shard, (int)blocks, kThreads, s, x);
 }
 
 cudaError_t launch_update_gather(cudaStream_t s, const Launch& L, const XArgs& x, const UpdConst& c,
                                  float* th, float* d, float* m, int64_t* last) {
     const int grid = (int)host_units(x);  // flat: one unit per block
     if (c.a_rms != 0.0f)
-        return launch_pdl(k_update_gather<true>, grid, kThreads, s, x, c, th, d, m, last);
+        return launch_pdl_if((L.pdl_mask & 8) != 0, k_update_gather<true>, grid, kThreads, s, x, c, th, d, m, last);
     else
-        return launch_pdl(k_update_gather<false>, grid, kThreads, s, x, c, th, d, m, last);
+        return launch_pdl_if((L.pdl_mask & 8) != 0, k_update_gather<false>, grid, kThreads, s, x, c, th, d, m, last);
 }
 
 cudaError_t launch_bn_stage(cudaStream_t s, const XArgs& x, const float* mean, const float* var,

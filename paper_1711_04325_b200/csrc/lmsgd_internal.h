@@ -48,6 +48,8 @@ struct Launch {
     int grid_cap_stream;   // SMs x resident blocks of the streaming kernels (informational)
     int grid_cap_push;     // SMs x resident blocks of k_pack_push (persistent grid)
     int grid_cap_reduce;   // SMs x resident blocks of k_reduce_shard (persistent grid)
+    int pdl_mask;          // programmatic dependent launch per kernel group: 1 = k = 1 kernels,
+                           // 2 = k_pack_push, 4 = k_reduce_shard, 8 = k_update_gather
 };
 
 // ---- single-GPU building blocks (sub-step ABI and world == 1)
