@@ -28,11 +28,13 @@ struct lmsgd_ctx {
     lmsgd::Peers peers{};
     bool connected = false;
     unsigned int* tickets = nullptr;  // device [4]
+    unsigned int* xctr = nullptr;     // device [2 + nchunks] monotonic counters of k_xstep
     int64_t* last = nullptr;          // device lmsgd_step_status of the last step
     float* d_grads = nullptr;         // device staging for lmsgd_step_host (lazy)
     uint32_t step = 0, bn_calls = 0;
     cudaStream_t last_stream = nullptr;
     lmsgd::Launch L{};
+    bool three_kernel = false;     // diagnostics: LMSGD_XSTEP=0 runs the 3-kernel exchange
     int64_t timeout_ns = 10'000'000'000LL;
     std::string err;
     // profiling (lmsgd_profile_enable): event pairs around each kernel launch
@@ -86,6 +88,7 @@ lmsgd::Launch launch_for_current_device() {
     L.grid_cap_stream = L.sm_count * lmsgd::stream_blocks_per_sm();
     L.grid_cap_push = L.sm_count * lmsgd::push_blocks_per_sm();
     L.grid_cap_reduce = L.sm_count * lmsgd::reduce_blocks_per_sm();
+    L.grid_xstep = L.sm_count * lmsgd::xstep_blocks_per_sm();
     // PDL helps the k = 1 pair (128.7 vs 132.3 us) but costs 5-11 us on the world > 1
     // kernels at k = 4 (early-resident dependents steal SM slots; A/B in DESIGN.md).
     L.pdl_mask = 0x1;
@@ -136,6 +139,12 @@ Layout make_layout(int world, int64_t n) {
     off = align_up(off + 3 * 128, 256);
     L.off_bn = off;
     if (world > 1) off = align_up(off + int64_t(2) * 2 * LMSGD_MAX_BN_CHANNELS * 4, 256);
+    // reduce chunks: 32 units of 2048 elements (64K elements) of the shard each
+    const int64_t units_per_shard = (L.shard / 8 + 255) / 256;
+    L.cu = 32;
+    L.nchunks = static_cast<int32_t>((units_per_shard + L.cu - 1) / L.cu);
+    L.off_cflags = off;
+    if (world > 1) off = align_up(off + int64_t(L.nchunks) * LMSGD_MAX_WORLD * 4, 256);
     L.bytes = off;
     return L;
 }
@@ -253,6 +262,7 @@ lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_
     c->lay = make_layout(world, n_params);
     c->n_pad = c->lay.shard * world;
     if (const char* t = std::getenv("LMSGD_TIMEOUT_MS")) c->timeout_ns = std::atoll(t) * 1000000LL;
+    if (const char* t = std::getenv("LMSGD_XSTEP")) c->three_kernel = (t[0] == '0');
     DeviceGuard g(device);
     auto bail = [&](lmsgd_status s) { c->connected = false; lmsgd_finalize(c); return s; };
     if ((e = cudaMalloc(&c->buf, c->lay.bytes)) != cudaSuccess) { g_err = "cudaMalloc exchange buffer"; return bail(LMSGD_ERR_CUDA); }
@@ -267,6 +277,8 @@ lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_
     }
     if ((e = cudaMalloc(&c->tickets, 4 * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMemset(c->tickets, 0, 4 * sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMalloc(&c->xctr, (2 + c->lay.nchunks) * sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMemset(c->xctr, 0, (2 + c->lay.nchunks) * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMalloc(&c->last, sizeof(lmsgd_step_status))) != cudaSuccess ||
         (e = cudaMemset(c->last, 0, sizeof(lmsgd_step_status))) != cudaSuccess) {
         g_err = std::string("context allocations: ") + cudaGetErrorString(e);
@@ -318,6 +330,7 @@ lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
             if (p != c->rank && c->peers.base[p]) cudaIpcCloseMemHandle(c->peers.base[p]);
         if (c->buf) cudaFree(c->buf);
         if (c->tickets) cudaFree(c->tickets);
+        if (c->xctr) cudaFree(c->xctr);
         if (c->last) cudaFree(c->last);
         if (c->d_grads) cudaFree(c->d_grads);
         if (c->d_trace) cudaFree(c->d_trace);
@@ -362,6 +375,11 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
         return LMSGD_OK;
     }
     const lmsgd::XArgs x = xargs(c, epoch);
+    if (!c->three_kernel) {
+        lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr};
+        CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, c->L, a); }));
+        return LMSGD_OK;
+    }
     CK(c, timed(c, s, 0, [&] { return lmsgd::launch_pack_push(s, c->L, x, grads, c->scale); }));
     CK(c, timed(c, s, 1, [&] { return lmsgd::launch_reduce_shard(s, c->L, x); }));
     CK(c, timed(c, s, 2, [&] { return lmsgd::launch_update_gather(s, c->L, x, u, params, delta, m, c->last); }));

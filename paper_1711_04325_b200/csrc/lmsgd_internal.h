@@ -32,6 +32,9 @@ struct Layout {
     int64_t off_status;   // int64 [2 parity][ST_WORDS]
     int64_t off_flags;    // uint32: A at +0, B at +128 B, C at +256 B, each [LMSGD_MAX_WORLD]
     int64_t off_bn;       // float [2 parity][2 * LMSGD_MAX_BN_CHANNELS]
+    int64_t off_cflags;   // uint32 [nchunks][LMSGD_MAX_WORLD]: owner o's "R chunk c ready" = epoch
+    int32_t cu;           // work units (2048 elements) per reduce chunk
+    int32_t nchunks;      // chunks per shard
     int64_t bytes;
 };
 
@@ -48,6 +51,7 @@ struct Launch {
     int grid_cap_stream;   // SMs x resident blocks of the streaming kernels (informational)
     int grid_cap_push;     // SMs x resident blocks of k_pack_push (persistent grid)
     int grid_cap_reduce;   // SMs x resident blocks of k_reduce_shard (persistent grid)
+    int grid_xstep;        // SMs x resident blocks of k_xstep (cooperative, all co-resident)
     int pdl_mask;          // programmatic dependent launch per kernel group: 1 = k = 1 kernels,
                            // 2 = k_pack_push, 4 = k_reduce_shard, 8 = k_update_gather
 };
@@ -92,6 +96,21 @@ cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, co
 cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x);
 cudaError_t launch_update_gather(cudaStream_t s, const Launch& L, const XArgs& x, const UpdConst& c,
                                  float* th, float* d, float* m, int64_t* last);
+// One persistent cooperative kernel for the whole world > 1 step (pack+push, exact
+// reduce of the own shard with per-chunk release, update with the all-gather fused).
+struct XStep {
+    XArgs x;
+    const float* g;
+    float scale;
+    UpdConst c;
+    float *th, *d, *m;
+    int64_t* last;
+    unsigned int* ctr;   // local counters, monotonic across steps: [0] pack blocks done,
+                         // [1] blocks finished, [2 + c] reduce units of chunk c done
+};
+cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a);
+int xstep_blocks_per_sm();
+
 cudaError_t launch_bn_stage(cudaStream_t s, const XArgs& x, const float* mean, const float* var,
                             int64_t C);
 cudaError_t launch_bn_reduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C);
