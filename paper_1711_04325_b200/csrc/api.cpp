@@ -136,7 +136,7 @@ Layout make_layout(int world, int64_t n) {
     L.off_status = off;
     off = align_up(off + 2 * lmsgd::ST_WORDS * 8, 256);
     L.off_flags = off;
-    off = align_up(off + 3 * 128, 256);
+    off = align_up(off + 4 * 128, 256);
     L.off_bn = off;
     if (world > 1) off = align_up(off + int64_t(2) * 2 * LMSGD_MAX_BN_CHANNELS * 4, 256);
     // reduce chunks: 32 units of 2048 elements (64K elements) of the shard each

@@ -23,7 +23,8 @@ namespace lmsgd {
 namespace {
 
 constexpr int kThreads = 256;
-enum { FLAG_A = 0, FLAG_B = 1, FLAG_C = 2 };  // pack done, reduce done, BN staged
+enum { FLAG_A = 0, FLAG_B = 1, FLAG_C = 2, FLAG_D = 3 };  // pack done, reduce done, BN staged,
+                                                         // local: this step's decision stored
 
 // ------------------------------------------------------------------ helpers
 
@@ -547,25 +548,28 @@ __device__ __forceinline__ bool spin_flag(const XArgs& x, const uint32_t* f) {
     return true;
 }
 
-// The whole world > 1 step in one persistent, cooperatively launched kernel (all
-// blocks co-resident, so blocks may wait on each other and on other GPUs):
+// The world > 1 step in two kernels.
+//
+// k_xstep1 -- persistent, cooperatively launched (all blocks co-resident, so blocks
+// may wait on each other and on other GPUs):
 //   1. pack + push: fp16 payload written straight into every owner's receive slot;
-//      one system fence per block, the last block releases flag A to every rank;
-//   2. every block acquires A of all ranks and computes the global skip decision
-//      from the (now final) pack status words of all ranks;
-//   3. exact reduce of this rank's shard; each 64K-element chunk is released to every
-//      rank (flag cflag[c][rank] = epoch) as soon as its units are done;
-//   4. update of all N elements with the all-gather fused in: units in chunk order,
-//      owner-interleaved; a unit waits only for its owner's chunk flag, so the
-//      update of early chunks overlaps the reduce of later ones;
-//   5. the last block to finish writes the public status record.
-// Counters in a.ctr are monotonic across steps (targets = epoch x count, mod 2^32).
-template <bool RMS>
-__global__ void __launch_bounds__(kThreads) k_xstep(XStep a) {
-    pdl_enter();
+//      one system fence per block; the last block releases flag A to every rank;
+//   2. every block acquires A of all ranks; block 0 computes the global skip
+//      decision from the (now final) pack status words of all ranks, stores it and
+//      releases the local flag D;
+//   3. exact reduce of this rank's shard over contiguous unit ranges per block; a
+//      64K-element chunk is released to every rank (cflag[c][rank] = epoch) as soon
+//      as all its units are reduced.
+// k_xupdate -- flat grid, launched with programmatic dependent launch so its blocks
+// take SMs as soon as k_xstep1's blocks retire: one unit per block, chunk-major and
+// owner-interleaved; a block waits only for D and for its owner's chunk flag, so
+// the update of early chunks overlaps the reduce of later ones.
+// k_xfinalize -- one warp: the step's public status record.
+// Chunk counters in a.ctr are reset by the block that completes them.
+__global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // let k_xupdate queue up
     const XArgs& x = a.x;
-    __shared__ int64_t s_st[3 * LMSGD_MAX_WORLD];
-    __shared__ int s_ok[2];
+    __shared__ int s_ok;
     const bool t0 = threadIdx.x == 0;
     if (blockIdx.x == 0 && t0) stamp(x, TR_PACK_START);
     const int64_t gsh = x.lay.shard >> 3;
@@ -592,122 +596,154 @@ __global__ void __launch_bounds__(kThreads) k_xstep(XStep a) {
     }
     __threadfence_system();
     __syncthreads();
-    if (t0 && atomicAdd(a.ctr + 0, 1u) + 1u == x.epoch * gridDim.x) {
+    if (t0 && atomicAdd(a.ctr + 0, 1u) + 1u == gridDim.x) {
+        a.ctr[0] = 0;
         stamp(x, TR_PACK_END);
         publish(x, FLAG_A);
     }
 
     // ---- 2. all ranks packed -> global decision (identical on every rank)
-    if (t0) s_ok[0] = thread_wait_all(x, FLAG_A) ? 1 : 0;
+    __shared__ int64_t s_st[3 * LMSGD_MAX_WORLD];
+    __shared__ int s_skip;
+    if (t0) s_ok = thread_wait_all(x, FLAG_A) ? 1 : 0;
     __syncthreads();
-    if (threadIdx.x < x.world) {
+    if (threadIdx.x < x.world) {   // every rank's final pack words, read in parallel
         const volatile int64_t* sp = status_of(x, threadIdx.x);
         s_st[3 * threadIdx.x] = sp[ST_FIRST];
         s_st[3 * threadIdx.x + 1] = sp[ST_PACK_SAT];
         s_st[3 * threadIdx.x + 2] = sp[ST_ERROR];
     }
     __syncthreads();
-    int64_t gfirst = kNone, psat = 0, err = s_ok[0] ? 0 : (int64_t)LMSGD_ERR_TIMEOUT;
-    for (int p = 0; p < x.world; ++p) {
-        gfirst = s_st[3 * p] < gfirst ? s_st[3 * p] : gfirst;
-        psat += s_st[3 * p + 1];
-        err = err ? err : s_st[3 * p + 2];
-    }
-    const bool skip = gfirst != kNone || err != 0;
-    if (blockIdx.x == 0) {
-        if (t0) {
+    if (t0) {
+        int64_t gfirst = kNone, psat = 0, err = s_ok ? 0 : (int64_t)LMSGD_ERR_TIMEOUT;
+        for (int p = 0; p < x.world; ++p) {
+            gfirst = s_st[3 * p] < gfirst ? s_st[3 * p] : gfirst;
+            psat += s_st[3 * p + 1];
+            err = err ? err : s_st[3 * p + 2];
+        }
+        s_skip = gfirst != kNone || err != 0;
+        if (blockIdx.x == 0) {
             stamp(x, TR_RED_START);
             mine[ST_G_FIRST] = gfirst;
             mine[ST_G_PACK_SAT] = psat;
             mine[ST_G_ERROR] = err;
-        }
-        if (threadIdx.x < ST_WORDS) {  // next step's status slot (every rank has read it by now)
             int64_t* nxt = reinterpret_cast<int64_t*>(x.peers.base[x.rank] + x.lay.off_status) +
-                           (x.parity ^ 1) * ST_WORDS;
-            nxt[threadIdx.x] = (threadIdx.x == ST_FIRST || threadIdx.x == ST_G_FIRST) ? kNone : 0;
+                           (x.parity ^ 1) * ST_WORDS;   // next step's slot: every rank has read it
+            for (int w = 0; w < ST_WORDS; ++w) nxt[w] = (w == ST_FIRST || w == ST_G_FIRST) ? kNone : 0;
+            __threadfence();
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag_slot(x, x.rank, FLAG_D)), "r"(x.epoch)
+                         : "memory");
         }
     }
-
-    bool ok = true;
-    if (!skip) {
-        // ---- 3. exact reduce of this rank's shard, released per chunk
-        if (blockIdx.x == 0 && t0) stamp(x, TR_RED_GO);
-        const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
-        uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
-        for (int64_t u = blockIdx.x; u < ups; u += gridDim.x) {
-            const int64_t gi = u * kThreads + threadIdx.x;
-            unsigned sat = 0;
-            if (gi < gsh) {
-                const int64_t j0 = gi << 3;
-                double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (int p = 0; p < x.world; ++p) {
-                    const uint4 q = *reinterpret_cast<const uint4*>(recv + (int64_t)p * x.lay.shard + j0);
-                    const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
-                }
-                unsigned short o[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
-                *reinterpret_cast<uint4*>(R + j0) =
-                    make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
-                               o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
-            }
-            flush_status(kNone, sat, mine, ST_SUM_SAT);
-            __threadfence_system();
-            __syncthreads();
-            if (t0) {
-                const int c = (int)(u / x.lay.cu);
-                const int64_t rem = ups - (int64_t)c * x.lay.cu;
-                const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
-                if (atomicAdd(a.ctr + 2 + c, 1u) + 1u == x.epoch * cnt)
-                    for (int p = 0; p < x.world; ++p) st_release_sys(cflag(x, p, c, x.rank), x.epoch);
-            }
-        }
-        if (blockIdx.x == 0 && t0) stamp(x, TR_RED_END);
-
-        // ---- 4. update with the all-gather fused in
-        if (blockIdx.x == 0 && t0) stamp(x, TR_UPD_START);
-        const int64_t kcu = (int64_t)x.world * x.lay.cu;
-        const int64_t nu = (int64_t)x.lay.nchunks * kcu;
-        int it = 0;
-        for (int64_t i = blockIdx.x; i < nu; i += gridDim.x, ++it) {
-            const int c = (int)(i / kcu);
-            const int64_t r = i - (int64_t)c * kcu;
-            const int owner = (int)((r % x.world + x.rank) % x.world);
-            const int64_t us = (int64_t)c * x.lay.cu + r / x.world;
-            if (us >= ups) continue;  // block-uniform
-            if (t0) s_ok[it & 1] = spin_flag(x, cflag(x, x.rank, c, owner)) ? 1 : 0;
-            __syncthreads();
-            if (!s_ok[it & 1]) { ok = false; break; }
-            const int64_t gi = us * kThreads + threadIdx.x;
-            if (gi < gsh) {
-                const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
-                if (j0 < x.n) {
-                    const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
-                    update8<RMS>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, a.c, a.th, a.d, a.m);
-                }
-            }
-        }
-        if (!ok && t0) {
-            mine[ST_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-            mine[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-        }
-    }
-
-    // ---- 5. the last block publishes the status record
-    __threadfence();
     __syncthreads();
-    if (t0 && atomicAdd(a.ctr + 1, 1u) + 1u == x.epoch * gridDim.x) {
-        int64_t ssat = 0;
-        if (!skip)
-            for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, p))[ST_SUM_SAT];
-        const volatile int64_t* vm = mine;
-        const int64_t e2 = vm[ST_G_ERROR];
-        store_last(a.last, gfirst, psat, ssat, e2 ? e2 : err, skip || e2 != 0);
-        stamp(x, TR_UPD_GO);
-        stamp(x, TR_UPD_END);
+    if (s_skip) return;
+
+    // ---- 3. exact reduce of this rank's shard, released per chunk
+    if (blockIdx.x == 0 && t0) stamp(x, TR_RED_GO);
+    const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
+    uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
+    const int64_t per = (ups + gridDim.x - 1) / gridDim.x;
+    const int64_t lo = (int64_t)blockIdx.x * per;
+    const int64_t hi = lo + per < ups ? lo + per : ups;
+    int cur = -1;
+    unsigned n_in = 0;
+    auto commit = [&](int c, unsigned n) {
+        __threadfence_system();
+        __syncthreads();
+        if (t0) {
+            const int64_t rem = ups - (int64_t)c * x.lay.cu;
+            const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
+            if (atomicAdd(a.ctr + 2 + c, n) + n == cnt) {
+                a.ctr[2 + c] = 0;
+                for (int p = 0; p < x.world; ++p) st_release_sys(cflag(x, p, c, x.rank), x.epoch);
+            }
+        }
+    };
+    for (int64_t u = lo; u < hi; ++u) {
+        const int c = (int)(u / x.lay.cu);
+        if (c != cur) {
+            if (cur >= 0) commit(cur, n_in);
+            cur = c;
+            n_in = 0;
+        }
+        const int64_t gi = u * kThreads + threadIdx.x;
+        unsigned sat = 0;
+        if (gi < gsh) {
+            const int64_t j0 = gi << 3;
+            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int p = 0; p < x.world; ++p) {
+                const uint4 q = *reinterpret_cast<const uint4*>(recv + (int64_t)p * x.lay.shard + j0);
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
+            }
+            unsigned short o[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
+            *reinterpret_cast<uint4*>(R + j0) =
+                make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
+                           o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
+        }
+        flush_status(kNone, sat, mine, ST_SUM_SAT);
+        ++n_in;
     }
+    if (cur >= 0) commit(cur, n_in);
+    if (blockIdx.x == 0 && t0) stamp(x, TR_RED_END);
+}
+
+template <bool RMS>
+__global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
+    // no griddepcontrol.wait: ordering with k_xstep1 is by flags D and cflag
+    const XArgs& x = a.x;
+    __shared__ int s_go;
+    const int64_t gsh = x.lay.shard >> 3;
+    const int64_t ups = (gsh + kThreads - 1) / kThreads;
+    const int64_t kcu = (int64_t)x.world * x.lay.cu;
+    const int64_t i = blockIdx.x;
+    const int c = (int)(i / kcu);
+    const int64_t r = i - (int64_t)c * kcu;
+    const int owner = (int)((r % x.world + x.rank) % x.world);
+    const int64_t us = (int64_t)c * x.lay.cu + r / x.world;
+    if (threadIdx.x == 0) {
+        if (i == 0) stamp(x, TR_UPD_START);
+        int go = spin_flag(x, flag_slot(x, x.rank, FLAG_D)) ? 1 : 0;
+        if (go) {
+            const int64_t* mine = status_of(x, x.rank);
+            const volatile int64_t* vm = mine;
+            if (vm[ST_G_FIRST] != kNone || vm[ST_G_ERROR] != 0) go = 0;   // skipped step
+            else if (us < ups && !spin_flag(x, cflag(x, x.rank, c, owner))) {
+                go = 0;
+                int64_t* mw = status_of(x, x.rank);
+                mw[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+            }
+        }
+        if (i == 0) stamp(x, TR_UPD_GO);
+        s_go = go;
+    }
+    __syncthreads();
+    if (!s_go || us >= ups) return;
+    const int64_t gi = us * kThreads + threadIdx.x;
+    if (gi >= gsh) return;
+    const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+    if (j0 >= x.n) return;
+    const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
+    update8<RMS>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, a.c, a.th, a.d, a.m);
+}
+
+// The step's public status record; runs after k_xupdate (every owner's reduce has
+// been observed by then, so every rank's sum saturation count is final).
+__global__ void k_xfinalize(XStep a) {
+    pdl_enter();
+    const XArgs& x = a.x;
+    if (threadIdx.x != 0) return;
+    const volatile int64_t* mine = status_of(x, x.rank);
+    const int64_t gfirst = mine[ST_G_FIRST], err = mine[ST_G_ERROR];
+    const bool skip = gfirst != kNone || err != 0;
+    int64_t ssat = 0;
+    if (!skip)
+        for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, p))[ST_SUM_SAT];
+    store_last(a.last, gfirst, mine[ST_G_PACK_SAT], ssat, err, skip);
+    stamp(x, TR_UPD_END);
 }
 
 // BN statistics: stage [mean | var] in this rank's buffer, publish.
@@ -780,18 +816,26 @@ int reduce_blocks_per_sm() {
 }
 
 int xstep_blocks_per_sm() {
-    int b = 0, b2 = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_xstep<true>, kThreads, 0);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_xstep<false>, kThreads, 0);
-    b = b2 < b ? b2 : b;
+    int b = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_xstep1, kThreads, 0);
     return b > 0 ? b : 1;
 }
 
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
     XStep arg = a;
     void* params[] = {&arg};
-    const void* fn = a.c.a_rms != 0.0f ? (const void*)k_xstep<true> : (const void*)k_xstep<false>;
-    return cudaLaunchCooperativeKernel(fn, dim3((unsigned)L.grid_xstep), dim3(kThreads), params, 0, s);
+    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_xstep1, dim3((unsigned)L.grid_xstep), dim3(kThreads),
+                                                params, 0, s);
+    if (e != cudaSuccess) return e;
+    const int64_t gsh = a.x.lay.shard >> 3;
+    (void)gsh;
+    const int grid = (int)((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu);
+    if (a.c.a_rms != 0.0f)
+        e = launch_pdl_if(true, k_xupdate<true>, grid, kThreads, s, a);
+    else
+        e = launch_pdl_if(true, k_xupdate<false>, grid, kThreads, s, a);
+    if (e != cudaSuccess) return e;
+    return launch_pdl_if(true, k_xfinalize, 1, 32, s, a);
 }
 
 int stream_blocks_per_sm() {

@@ -30,7 +30,7 @@ struct Layout {
     int64_t off_recv;     // uint16 [world][shard]: slot p = rank p's packed values of MY shard
     int64_t off_R;        // uint16 [shard]: this rank's reduced shard (wire-2 payload)
     int64_t off_status;   // int64 [2 parity][ST_WORDS]
-    int64_t off_flags;    // uint32: A at +0, B at +128 B, C at +256 B, each [LMSGD_MAX_WORLD]
+    int64_t off_flags;    // uint32: A at +0, B at +128 B, C at +256 B, D at +384 B, each [LMSGD_MAX_WORLD]
     int64_t off_bn;       // float [2 parity][2 * LMSGD_MAX_BN_CHANNELS]
     int64_t off_cflags;   // uint32 [nchunks][LMSGD_MAX_WORLD]: owner o's "R chunk c ready" = epoch
     int32_t cu;           // work units (2048 elements) per reduce chunk
@@ -105,8 +105,8 @@ struct XStep {
     UpdConst c;
     float *th, *d, *m;
     int64_t* last;
-    unsigned int* ctr;   // local counters, monotonic across steps: [0] pack blocks done,
-                         // [1] blocks finished, [2 + c] reduce units of chunk c done
+    unsigned int* ctr;   // local counters, reset by their completer: [0] pack blocks done,
+                         // [1] unused, [2 + c] reduce units of chunk c done
 };
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a);
 int xstep_blocks_per_sm();
