@@ -321,7 +321,9 @@ def main():
         segs = {"pack": ("pack_start", "pack_end"), "wait_A": ("pack_end", "reduce_start"),
                 "gap_A": ("reduce_start", "reduce_go"), "reduce": ("reduce_go", "reduce_end"),
                 "wait_B": ("reduce_end", "update_start"), "gap_B": ("update_start", "update_go"),
-                "update": ("update_go", "update_end"), "step": ("pack_start", "update_end")}
+                "update": ("update_go", "update_end"), "step": ("pack_start", "update_end"),
+                "publish": ("pack_end", "publish_end")}
+        segs.update({f"a_seen_{p}": ("pack_end", f"a_seen_{p}") for p in range(world)})
         mine = {k: statistics.median((t[b] - t[a]) / 1e3 for t in tr[len(tr) // 4:]) for k, (a, b) in segs.items()}
         allr = [None] * world
         dist.all_gather_object(allr, mine)

@@ -204,13 +204,14 @@ lmsgd_status lmsgd_profile_enable(lmsgd_ctx* ctx, int64_t max_launches);
  * launch count of each phase (arrays of 3), and clear the record. */
 lmsgd_status lmsgd_profile_read(lmsgd_ctx* ctx, double* ms, int64_t* launches);
 
-/* Tracing of world > 1 steps: 8 %globaltimer stamps (ns, this GPU's clock) per step
- * -- pack start, pack end (last block, before its flag release), reduce start,
- * reduce go (flags of all ranks observed), reduce end, update start, update go,
- * update end -- into a ring of max_steps steps (0 disables).  Synchronous. */
+/* Tracing of world > 1 steps: 17 %globaltimer stamps (ns, this GPU's clock) per step
+ * -- pack start, pack end (last block, before its flag release), decision made
+ * (all ranks' packs observed), reduce start, reduce end, update start, update go,
+ * update end, flag release done, and the arrival of each rank's pack flag (8) --
+ * into a ring of max_steps steps (0 disables).  Synchronous. */
 lmsgd_status lmsgd_trace_enable(lmsgd_ctx* ctx, int64_t max_steps);
 
-/* Copy up to max_steps recorded steps (8 int64 each, oldest first until the ring
+/* Copy up to max_steps recorded steps (17 int64 each, oldest first until the ring
  * wraps) into host `out`; *steps = how many were copied.  Synchronizes the device. */
 lmsgd_status lmsgd_trace_read(lmsgd_ctx* ctx, int64_t* out, int64_t max_steps, int64_t* steps);
 

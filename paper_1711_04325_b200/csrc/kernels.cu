@@ -352,8 +352,16 @@ __device__ bool grid_last(const XArgs& x, int which) {
     return false;
 }
 
+__device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Release `value` into slot p of every rank: one system-scope fence, then relaxed
+// stores (= a release pattern).  k st.release.sys cost ~1.5 us each on NVLink 5
+// (tools/flagbench.cu); the single fence + relaxed stores ~1 us total.
 __device__ void publish(const XArgs& x, int which) {
-    for (int p = 0; p < x.world; ++p) st_release_sys(flag_slot(x, p, which) + x.rank, x.epoch);
+    __threadfence_system();
+    for (int p = 0; p < x.world; ++p) st_relaxed_sys(flag_slot(x, p, which) + x.rank, x.epoch);
 }
 
 // Grid-wide "done": the last block to finish publishes `which` = epoch to every rank.
@@ -363,10 +371,14 @@ __device__ void grid_signal(const XArgs& x, int which) {
 
 // One thread: wait until every rank has published `which` for this epoch (bounded
 // spin; on timeout record LMSGD_ERR_TIMEOUT in this rank's words and return false).
-__device__ bool thread_wait_all(const XArgs& x, int which) {
+__device__ bool thread_wait_all(const XArgs& x, int which, bool trace_seen = false) {
     const uint64_t t0 = globaltimer();
     for (int p = 0; p < x.world; ++p) {
         const uint32_t* f = flag_slot(x, x.rank, which) + p;
+        if (trace_seen && x.trace) {   // per-peer arrival, diagnostics only
+            while ((int32_t)(ld_acquire_sys(f) - x.epoch) < 0) {}
+            x.trace[TR_A_SEEN + p] = (int64_t)globaltimer();
+        }
         while ((int32_t)(ld_acquire_sys(f) - x.epoch) < 0) {
             __nanosleep(64);
             if ((int64_t)(globaltimer() - t0) > x.timeout_ns) {
@@ -378,7 +390,8 @@ __device__ bool thread_wait_all(const XArgs& x, int which) {
             }
         }
     }
-    __threadfence_system();
+    // no trailing fence: each ld.acquire.sys orders this thread's later accesses, and
+    // the callers' bar.sync extends that to the rest of the block
     return true;
 }
 
@@ -600,30 +613,29 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
         a.ctr[0] = 0;
         stamp(x, TR_PACK_END);
         publish(x, FLAG_A);
+        stamp(x, TR_PUB_END);
     }
 
-    // ---- 2. all ranks packed -> global decision (identical on every rank)
-    __shared__ int64_t s_st[3 * LMSGD_MAX_WORLD];
-    __shared__ int s_skip;
-    if (t0) s_ok = thread_wait_all(x, FLAG_A) ? 1 : 0;
+    // ---- 2. all ranks packed; block 0 makes the global skip decision (identical on
+    //         every rank) and releases the local flag D.  The reduce does not need it.
+    if (t0) s_ok = thread_wait_all(x, FLAG_A, blockIdx.x == 0) ? 1 : 0;
     __syncthreads();
-    if (threadIdx.x < x.world) {   // every rank's final pack words, read in parallel
-        const volatile int64_t* sp = status_of(x, threadIdx.x);
-        s_st[3 * threadIdx.x] = sp[ST_FIRST];
-        s_st[3 * threadIdx.x + 1] = sp[ST_PACK_SAT];
-        s_st[3 * threadIdx.x + 2] = sp[ST_ERROR];
-    }
-    __syncthreads();
-    if (t0) {
-        int64_t gfirst = kNone, psat = 0, err = s_ok ? 0 : (int64_t)LMSGD_ERR_TIMEOUT;
-        for (int p = 0; p < x.world; ++p) {
-            gfirst = s_st[3 * p] < gfirst ? s_st[3 * p] : gfirst;
-            psat += s_st[3 * p + 1];
-            err = err ? err : s_st[3 * p + 2];
+    if (blockIdx.x == 0) {
+        __shared__ int64_t s_st[3 * LMSGD_MAX_WORLD];
+        if (threadIdx.x < x.world) {   // every rank's final pack words, read in parallel
+            const volatile int64_t* sp = status_of(x, threadIdx.x);
+            s_st[3 * threadIdx.x] = sp[ST_FIRST];
+            s_st[3 * threadIdx.x + 1] = sp[ST_PACK_SAT];
+            s_st[3 * threadIdx.x + 2] = sp[ST_ERROR];
         }
-        s_skip = gfirst != kNone || err != 0;
-        if (blockIdx.x == 0) {
-            stamp(x, TR_RED_START);
+        __syncthreads();
+        if (t0) {
+            int64_t gfirst = kNone, psat = 0, err = s_ok ? 0 : (int64_t)LMSGD_ERR_TIMEOUT;
+            for (int p = 0; p < x.world; ++p) {
+                gfirst = s_st[3 * p] < gfirst ? s_st[3 * p] : gfirst;
+                psat += s_st[3 * p + 1];
+                err = err ? err : s_st[3 * p + 2];
+            }
             mine[ST_G_FIRST] = gfirst;
             mine[ST_G_PACK_SAT] = psat;
             mine[ST_G_ERROR] = err;
@@ -633,41 +645,20 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
             __threadfence();
             asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag_slot(x, x.rank, FLAG_D)), "r"(x.epoch)
                          : "memory");
+            stamp(x, TR_RED_START);
         }
     }
-    __syncthreads();
-    if (s_skip) return;
+    if (!s_ok) return;
 
-    // ---- 3. exact reduce of this rank's shard, released per chunk
+    // ---- 3. exact reduce of this rank's shard, chunk-major over blocks (unit u on
+    //         block u % grid), each chunk released as soon as its units are done.
+    //         Runs even for a step that will be skipped (its R is then never read).
     if (blockIdx.x == 0 && t0) stamp(x, TR_RED_GO);
     const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
     uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
-    const int64_t per = (ups + gridDim.x - 1) / gridDim.x;
-    const int64_t lo = (int64_t)blockIdx.x * per;
-    const int64_t hi = lo + per < ups ? lo + per : ups;
-    int cur = -1;
-    unsigned n_in = 0;
-    auto commit = [&](int c, unsigned n) {
-        __threadfence_system();
-        __syncthreads();
-        if (t0) {
-            const int64_t rem = ups - (int64_t)c * x.lay.cu;
-            const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
-            if (atomicAdd(a.ctr + 2 + c, n) + n == cnt) {
-                a.ctr[2 + c] = 0;
-                for (int p = 0; p < x.world; ++p) st_release_sys(cflag(x, p, c, x.rank), x.epoch);
-            }
-        }
-    };
-    for (int64_t u = lo; u < hi; ++u) {
-        const int c = (int)(u / x.lay.cu);
-        if (c != cur) {
-            if (cur >= 0) commit(cur, n_in);
-            cur = c;
-            n_in = 0;
-        }
+    unsigned sat = 0;
+    for (int64_t u = blockIdx.x; u < ups; u += gridDim.x) {
         const int64_t gi = u * kThreads + threadIdx.x;
-        unsigned sat = 0;
         if (gi < gsh) {
             const int64_t j0 = gi << 3;
             double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -684,10 +675,23 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
                 make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
                            o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
         }
-        flush_status(kNone, sat, mine, ST_SUM_SAT);
-        ++n_in;
     }
-    if (cur >= 0) commit(cur, n_in);
+    flush_status(kNone, sat, mine, ST_SUM_SAT);
+    // one system fence per block (a fence per unit stalls behind the concurrent
+    // update's peer loads), then count this block's units into their chunks
+    __threadfence_system();
+    __syncthreads();
+    if (t0) {
+        for (int64_t u = blockIdx.x; u < ups; u += gridDim.x) {
+            const int c = (int)(u / x.lay.cu);
+            const int64_t rem = ups - (int64_t)c * x.lay.cu;
+            const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
+            if (atomicAdd(a.ctr + 2 + c, 1u) + 1u == cnt) {
+                a.ctr[2 + c] = 0;
+                for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, c, x.rank), x.epoch);
+            }
+        }
+    }
     if (blockIdx.x == 0 && t0) stamp(x, TR_RED_END);
 }
 

@@ -90,7 +90,7 @@ struct XArgs {
 // pack end (its last block), all ranks' packs observed, reduce start, reduce end,
 // all ranks' reduces observed, update start, update end.
 enum { TR_PACK_START = 0, TR_PACK_END, TR_RED_START, TR_RED_GO, TR_RED_END, TR_UPD_START, TR_UPD_GO,
-       TR_UPD_END, TR_WORDS };
+       TR_UPD_END, TR_PUB_END, TR_A_SEEN /* + rank, 8 words */ = 9, TR_WORDS = 17 };
 cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,
                              float scale);
 cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x);

@@ -299,7 +299,8 @@ def lmsgd_profile_read(ctx: Context) -> dict:
 # (reduce_go), reduce end, all ranks' reduces observed (update_start), update kernel
 # start (update_go), update end
 TRACE_FIELDS = ("pack_start", "pack_end", "reduce_start", "reduce_go", "reduce_end",
-                "update_start", "update_go", "update_end")
+                "update_start", "update_go", "update_end", "publish_end") + tuple(f"a_seen_{p}" for p in range(8))
+TRACE_WORDS = len(TRACE_FIELDS)
 
 
 def lmsgd_trace_enable(ctx: Context, max_steps: int):
@@ -308,10 +309,10 @@ def lmsgd_trace_enable(ctx: Context, max_steps: int):
 
 def lmsgd_trace_read(ctx: Context, max_steps: int):
     """List of per-step dicts {field: ns} (world > 1 steps only)."""
-    buf = (ctypes.c_int64 * (8 * max_steps))()
+    buf = (ctypes.c_int64 * (TRACE_WORDS * max_steps))()
     got = ctypes.c_int64()
     _check(_lib.lmsgd_trace_read(ctx.ptr, buf, int(max_steps), ctypes.byref(got)), ctx)
-    return [dict(zip(TRACE_FIELDS, buf[8 * i:8 * i + 8])) for i in range(got.value)]
+    return [dict(zip(TRACE_FIELDS, buf[TRACE_WORDS * i:TRACE_WORDS * (i + 1)])) for i in range(got.value)]
 
 
 # ------------------------------------------------------------------ sub-steps
