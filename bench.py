@@ -51,7 +51,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="do not record per-kernel events")
-    p.add_argument("--trace", action="store_true", help="N>1: %%globaltimer trace of the profile pass")
+    p.add_argument("--trace", action="store_true", help="(kept for compatibility; N>1 always traces the profile pass)")
     return p.parse_args()
 
 
@@ -279,7 +279,9 @@ def main():
     code, st = L.lmsgd_query_status(ctx)
     assert code == 0, f"warm-up step status {code}"
 
-    kernels_per_step = 2 if flags else (2 if world == 1 else 3)   # fused: k_fused1 + 1-warp status finalize
+    # kernels launched per step: fused = k_fused1 + status finalize; guarded k=1 = k_pack
+    # + k_update; world > 1 = k_xstep1 + k_xupdate + k_xfinalize
+    kernels_per_step = 2 if flags else (2 if world == 1 else 3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     def timed(profile: bool):
@@ -307,28 +309,34 @@ def main():
     ms, _ = timed(False)
     ck = clocks.stop()
     # 2) the same K steps again with CUDA events around every kernel (per-kernel roofline)
-    prof = {}
+    # 2) per-kernel durations of the same K steps, measured in a second pass:
+    #    N = 1: CUDA events around every kernel (lmsgd_profile_enable);
+    #    N > 1: %globaltimer stamps inside the kernels (lmsgd_trace_enable) -- events
+    #    between the step's kernels would serialise their overlap.
+    prof, trace, ms_prof = {}, None, None
     if not args.no_profile:
-        if args.trace and world > 1:
+        if world == 1:
+            ms_prof, prof = timed(True)
+        else:
+            import statistics
             L.lmsgd_trace_enable(ctx, args.steps)
-        ms_prof, prof = timed(True)
-    trace = None
-    if args.trace and world > 1 and not args.no_profile:
-        import statistics
-        tr = L.lmsgd_trace_read(ctx, args.steps)
-        # stamps: pack_start, pack_end, (all packs seen), reduce start, reduce end,
-        # (all reduces seen), update start, update end -- see lmsgd_trace_enable
-        segs = {"pack": ("pack_start", "pack_end"), "wait_A": ("pack_end", "reduce_start"),
-                "gap_A": ("reduce_start", "reduce_go"), "reduce": ("reduce_go", "reduce_end"),
-                "wait_B": ("reduce_end", "update_start"), "gap_B": ("update_start", "update_go"),
-                "update": ("update_go", "update_end"), "step": ("pack_start", "update_end"),
-                "publish": ("pack_end", "publish_end")}
-        segs.update({f"a_seen_{p}": ("pack_end", f"a_seen_{p}") for p in range(world)})
-        mine = {k: statistics.median((t[b] - t[a]) / 1e3 for t in tr[len(tr) // 4:]) for k, (a, b) in segs.items()}
-        allr = [None] * world
-        dist.all_gather_object(allr, mine)
-        trace = {"us_median_per_rank": allr}
-        L.lmsgd_trace_enable(ctx, 0)
+            ms_prof, _ = timed(False)
+            tr = L.lmsgd_trace_read(ctx, args.steps)
+            L.lmsgd_trace_enable(ctx, 0)
+            # stamps: see lmsgd_trace_enable (pack start/end, decision, reduce start/end,
+            # update kernel start, first unit released, status record written)
+            segs = {"pack": ("pack_start", "pack_end"), "wait_all_packs": ("pack_end", "reduce_start"),
+                    "reduce_block0": ("reduce_go", "reduce_end"), "update_first_wait": ("update_start", "update_go"),
+                    "update": ("update_go", "update_end"), "step": ("pack_start", "update_end"),
+                    "publish": ("pack_end", "publish_end")}
+            segs.update({f"flag_A_from_{p}": ("pack_end", f"a_seen_{p}") for p in range(world)})
+            body = tr[len(tr) // 4:]
+            mine = {k: statistics.median((t[b] - t[a]) / 1e3 for t in body) for k, (a, b) in segs.items()}
+            allr = [None] * world
+            dist.all_gather_object(allr, mine)
+            trace = {"us_median_per_rank": allr}
+            worst = {k: max(r[k] for r in allr) for k in ("pack", "update", "step")}
+            prof = {"pack": (worst["pack"] * 1e-3, 1), "update": (worst["update"] * 1e-3, 1)}
     ms_per_step = ms / args.steps
     global_steps_per_s = 1e3 / ms_per_step
     value = global_steps_per_s * world
@@ -338,11 +346,13 @@ def main():
     phases = {}
     for ph, (pms, cnt) in prof.items():
         if cnt:
-            phases[ph] = {"us_per_launch": max_over_ranks(pms / cnt * 1e3), "launches": cnt}
+            phases[ph] = {"us_per_launch": (max_over_ranks(pms / cnt * 1e3) if world == 1 else pms * 1e3),
+                          "launches": cnt if world == 1 else args.steps,
+                          "source": "cuda events" if world == 1 else "in-kernel %globaltimer trace, max over ranks"}
     if flags:
         dom, dom_bytes, kname = "pack", FUSED_BYTES_PER_ELEM, "k_fused1"   # phase 0 = the fused kernel
     else:
-        dom, dom_bytes, kname = "update", UPDATE_BYTES_PER_ELEM, "k_update" if world == 1 else "k_update_gather"
+        dom, dom_bytes, kname = "update", UPDATE_BYTES_PER_ELEM, "k_update" if world == 1 else "k_xupdate"
     roofline = None
     if dom in phases:
         us = phases[dom]["us_per_launch"]
@@ -351,7 +361,7 @@ def main():
                     "frac": achieved / peak, "traffic": committed_traffic(kname),
                     "algorithmic_bytes_per_launch": dom_bytes * n, "peak_source": peak_src,
                     "share_of_step": us * 1e-3 / ms_per_step}
-    if "pack" in phases and not flags:
+    if "pack" in phases and not flags and world == 1:
         phases["pack"]["gbs_algorithmic"] = PACK_BYTES_PER_ELEM * n / (phases["pack"]["us_per_launch"] * 1e-6) / 1e9
     if "update" in phases:
         phases["update"]["gbs_algorithmic"] = UPDATE_BYTES_PER_ELEM * n / (phases["update"]["us_per_launch"] * 1e-6) / 1e9
@@ -362,6 +372,12 @@ def main():
         nvlink = {"allreduce_bus_bytes_per_step": bus_bytes,
                   "step_bus_gbs": bus_bytes / (ms_per_step * 1e-3) / 1e9, "peak_gbs_per_dir": 900.0,
                   "measured_peer_gbs_per_dir": 770.0}
+        if "pack" in phases:
+            # the pack+push phase moves 2 B x N_pad x (k-1)/k out of (and into) every GPU
+            push = 2 * n_pad * (world - 1) / world
+            nvlink["pack_push_us"] = phases["pack"]["us_per_launch"]
+            nvlink["pack_push_gbs_per_dir"] = push / (phases["pack"]["us_per_launch"] * 1e-6) / 1e9
+            nvlink["pack_push_frac_of_measured_peer"] = nvlink["pack_push_gbs_per_dir"] / 770.0
         # yardstick: NCCL fp16 all-reduce of the same payload alone (not part of our path)
         buf = torch.zeros(n_pad, dtype=torch.float16, device=devc)
         for _ in range(5):
@@ -461,7 +477,7 @@ def main():
             "roofline": roofline, "phases": phases, "nvlink": nvlink, "bn_stats_allreduce": bn,
             "cpu_baseline": cpu, "e2e": e2e,
             "clocks": ck, "gpu_launches": kernels_per_step * args.steps,
-            "profile_pass_ms_per_step": (ms_prof / args.steps) if prof else None,
+            "profile_pass_ms_per_step": (ms_prof / args.steps) if ms_prof else None,
             "trace": trace,
         }
         print(json.dumps(line), flush=True)

@@ -34,7 +34,6 @@ struct lmsgd_ctx {
     uint32_t step = 0, bn_calls = 0;
     cudaStream_t last_stream = nullptr;
     lmsgd::Launch L{};
-    bool three_kernel = false;     // diagnostics: LMSGD_XSTEP=0 runs the 3-kernel exchange
     int64_t timeout_ns = 10'000'000'000LL;
     std::string err;
     // profiling (lmsgd_profile_enable): event pairs around each kernel launch
@@ -86,11 +85,8 @@ lmsgd::Launch launch_for_current_device() {
     lmsgd::Launch L{};
     cudaDeviceGetAttribute(&L.sm_count, cudaDevAttrMultiProcessorCount, dev);
     L.grid_cap_stream = L.sm_count * lmsgd::stream_blocks_per_sm();
-    L.grid_cap_push = L.sm_count * lmsgd::push_blocks_per_sm();
-    L.grid_cap_reduce = L.sm_count * lmsgd::reduce_blocks_per_sm();
     L.grid_xstep = L.sm_count * lmsgd::xstep_blocks_per_sm();
-    // PDL helps the k = 1 pair (128.7 vs 132.3 us) but costs 5-11 us on the world > 1
-    // kernels at k = 4 (early-resident dependents steal SM slots; A/B in DESIGN.md).
+    // PDL on the k = 1 pair: 128.7 vs 132.3 us (the world > 1 step uses it internally).
     L.pdl_mask = 0x1;
     if (const char* m = std::getenv("LMSGD_PDL_MASK")) L.pdl_mask = std::atoi(m);  // diagnostics
     if (dev >= 0 && dev < 64) { cache[dev] = L; have[dev] = true; }
@@ -262,7 +258,6 @@ lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_
     c->lay = make_layout(world, n_params);
     c->n_pad = c->lay.shard * world;
     if (const char* t = std::getenv("LMSGD_TIMEOUT_MS")) c->timeout_ns = std::atoll(t) * 1000000LL;
-    if (const char* t = std::getenv("LMSGD_XSTEP")) c->three_kernel = (t[0] == '0');
     DeviceGuard g(device);
     auto bail = [&](lmsgd_status s) { c->connected = false; lmsgd_finalize(c); return s; };
     if ((e = cudaMalloc(&c->buf, c->lay.bytes)) != cudaSuccess) { g_err = "cudaMalloc exchange buffer"; return bail(LMSGD_ERR_CUDA); }
@@ -375,14 +370,8 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
         return LMSGD_OK;
     }
     const lmsgd::XArgs x = xargs(c, epoch);
-    if (!c->three_kernel) {
-        lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr};
-        CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, c->L, a); }));
-        return LMSGD_OK;
-    }
-    CK(c, timed(c, s, 0, [&] { return lmsgd::launch_pack_push(s, c->L, x, grads, c->scale); }));
-    CK(c, timed(c, s, 1, [&] { return lmsgd::launch_reduce_shard(s, c->L, x); }));
-    CK(c, timed(c, s, 2, [&] { return lmsgd::launch_update_gather(s, c->L, x, u, params, delta, m, c->last); }));
+    lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr};
+    CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, c->L, a); }));
     return LMSGD_OK;
 }
 

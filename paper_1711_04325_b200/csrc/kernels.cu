@@ -395,13 +395,6 @@ __device__ bool thread_wait_all(const XArgs& x, int which, bool trace_seen = fal
     return true;
 }
 
-// Cross-GPU ordering of the three exchange kernels.  Each kernel's last block
-// (ticket) releases its flag to every rank and then waits until every rank has
-// released the same flag; only then does the kernel end.  The next kernel in the
-// stream therefore starts after all ranks finished the previous phase, with no
-// per-block waits: kernel completion orders the acquired peer writes before every
-// later access on this GPU (L1 is invalidated at each launch; peer loads bypass L2).
-
 // Work units of the exchange kernels: a unit is kThreads consecutive 8-element groups
 // of one shard.  Units are interleaved over owners -- unit u belongs to owner
 // (u + rank) % world -- so that the blocks in flight on every rank touch all owners
@@ -414,136 +407,6 @@ __device__ __forceinline__ bool map_unit(const XArgs& x, int64_t u, int& owner, 
     owner = (int)((u % x.world + x.rank) % x.world);
     gi = (u / x.world) * kThreads + threadIdx.x;   // group index inside the owner's shard
     return gi < (x.lay.shard >> 3);
-}
-
-// Pack this rank's gradient and push each shard straight into its owner's receive
-// slot (peer stores over NVLink), interleaved over owners.  Persistent grid: one
-// system-scope fence per resident block.  The last block also computes the global
-// skip decision once every rank's pack status is final.
-__global__ void __launch_bounds__(kThreads) k_pack_push(XArgs x, const float* __restrict__ g, float s) {
-    pdl_enter();
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_PACK_START);
-    int64_t first = kNone;
-    unsigned sat = 0;
-    const int64_t gsh = x.lay.shard >> 3;
-    const int64_t units = units_of(x);
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        int owner;
-        int64_t gi;
-        if (!map_unit(x, u, owner, gi)) continue;
-        const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
-        const int64_t off = gi << 3;
-        float xv[8];
-        load8_g(g, j0, x.n, xv);
-        uint16_t* dst = reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
-                        (int64_t)x.rank * x.lay.shard + off;
-        *reinterpret_cast<uint4*>(dst) = pack8(xv, s, j0, first, sat);
-    }
-    flush_status(first, sat, status_of(x, x.rank), ST_PACK_SAT);
-    if (grid_last(x, FLAG_A)) {
-        stamp(x, TR_PACK_END);
-        publish(x, FLAG_A);
-        if (thread_wait_all(x, FLAG_A)) {
-            // Global skip decision from every rank's (final) pack status; identical
-            // inputs on every rank -> identical decision.
-            int64_t gfirst = kNone, psat = 0, err = 0;
-            for (int p = 0; p < x.world; ++p) {
-                const volatile int64_t* sp = status_of(x, p);
-                const int64_t f = sp[ST_FIRST];
-                gfirst = f < gfirst ? f : gfirst;
-                psat += sp[ST_PACK_SAT];
-                err = err ? err : sp[ST_ERROR];
-            }
-            int64_t* mine = status_of(x, x.rank);
-            mine[ST_G_FIRST] = gfirst;
-            mine[ST_G_PACK_SAT] = psat;
-            mine[ST_G_ERROR] = err;
-        }
-        stamp(x, TR_RED_START);   // = all ranks' packs observed
-    }
-}
-
-// Owner-computes reduce of this rank's shard: exact fp64 sum of the world slots in
-// rank order, one saturating RNE rounding (the fp16 all-reduce SUM, R9/R10).
-// Persistent grid (one fence per resident block); the last block releases B, waits
-// for every rank's B and totals the wire-2 saturation counts.
-__global__ void __launch_bounds__(kThreads) k_reduce_shard(XArgs x) {
-    pdl_enter();
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_RED_GO);
-    const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
-    uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
-    unsigned sat = 0;
-    const int64_t nv = x.lay.shard >> 3;
-    for (int64_t v = gtid(); v < nv; v += gstride()) {
-        const int64_t j0 = v << 3;
-        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int p = 0; p < x.world; ++p) {
-            const uint4 q = *reinterpret_cast<const uint4*>(recv + (int64_t)p * x.lay.shard + j0);
-            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
-        }
-        unsigned short o[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
-        *reinterpret_cast<uint4*>(R + j0) =
-            make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
-                       o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
-    }
-    flush_status(kNone, sat, status_of(x, x.rank), ST_SUM_SAT);
-    if (grid_last(x, FLAG_B)) {
-        stamp(x, TR_RED_END);
-        publish(x, FLAG_B);
-        if (thread_wait_all(x, FLAG_B)) {
-            int64_t ssat = 0;
-            for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, p))[ST_SUM_SAT];
-            status_of(x, x.rank)[ST_G_SUM_SAT] = ssat;
-        }
-        stamp(x, TR_UPD_START);   // = all ranks' reduces observed
-    }
-}
-
-// Update with the all-gather fused in: each element's R is loaded from its owner's
-// shard (peer loads over NVLink for remote shards), owner-interleaved units.  Flat
-// grid, no waits: the previous kernel ended only after every rank's reduce.
-template <bool RMS>
-__global__ void __launch_bounds__(kThreads) k_update_gather(XArgs x, UpdConst c, float* __restrict__ th,
-                                                            float* __restrict__ d, float* __restrict__ m,
-                                                            int64_t* last) {
-    pdl_enter();
-    const int64_t* mine = status_of(x, x.rank);  // decision written by this rank's pack / reduce
-    const int64_t g_first = mine[ST_G_FIRST], g_err = mine[ST_G_ERROR];
-    const bool skip = g_first != kNone || g_err != 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        stamp(x, TR_UPD_GO);
-        if (last) store_last(last, g_first, mine[ST_G_PACK_SAT], mine[ST_G_SUM_SAT], g_err, skip);
-    }
-    if (blockIdx.x == 0 && threadIdx.x < ST_WORDS) {  // next step's status slot
-        int64_t* nxt = reinterpret_cast<int64_t*>(x.peers.base[x.rank] + x.lay.off_status) +
-                       (x.parity ^ 1) * ST_WORDS;
-        nxt[threadIdx.x] = (threadIdx.x == ST_FIRST || threadIdx.x == ST_G_FIRST) ? kNone : 0;
-    }
-    if (skip) return;
-    const int64_t gsh = x.lay.shard >> 3;
-    const int64_t units = units_of(x);
-    for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-        int owner;
-        int64_t gi;
-        if (!map_unit(x, u, owner, gi)) continue;
-        const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
-        if (j0 >= x.n) continue;
-        const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
-        const uint4 r = *reinterpret_cast<const uint4*>(Rp);
-        update8<RMS>(r, j0, x.n, c, th, d, m);
-    }
-    if (x.trace) {  // end stamp: last block (ticket 3), trace mode only
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0 && atomicAdd(x.ticket + 3, 1u) == gridDim.x - 1) {
-            x.ticket[3] = 0;
-            stamp(x, TR_UPD_END);
-        }
-    }
 }
 
 // ------------------------------------------------------------------ world > 1, one kernel
@@ -807,17 +670,7 @@ cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), int grid, int bloc
 }
 #define launch_pdl(...) launch_pdl_if((L.pdl_mask & 1) != 0, __VA_ARGS__)
 
-int push_blocks_per_sm() {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_pack_push, kThreads, 0);
-    return b > 0 ? b : 1;
-}
 
-int reduce_blocks_per_sm() {
-    int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_reduce_shard, kThreads, 0);
-    return b > 0 ? b : 1;
-}
 
 int xstep_blocks_per_sm() {
     int b = 0;
@@ -847,8 +700,6 @@ int stream_blocks_per_sm() {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update<true>, kThreads, 0);
     worst = b < worst ? b : worst;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true>, kThreads, 0);  // NOLINT
-    worst = b < worst ? b : worst;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update_gather<true>, kThreads, 0);
     worst = b < worst ? b : worst;
     return worst > 0 ? worst : 1;
 }
@@ -888,10 +739,6 @@ cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64
         return launch_pdl(k_fused1<false>, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset);
 }
 
-// Persistent grid for the push: the system-scope fence each block issues before the
-// ticket waits for its remote stores to be acknowledged, so it is paid once per
-// resident block, not once per 2048 elements (tools/p2pbench.cu: 80.7 us vs 120 us
-// for a 51 MB push at k = 2 on NVLink 5).
 int64_t host_units(const XArgs& x) {
     const int64_t gsh = x.lay.shard >> 3;
     return (int64_t)x.world * ((gsh + kThreads - 1) / kThreads);
@@ -901,27 +748,8 @@ cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* la
     return launch_pdl_if(true, k_finalize_fused, 1, 32, s, st, last);
 }
 
-cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,
-                             float scale) {
-    int64_t blocks = host_units(x);
-    if (blocks > L.grid_cap_push) blocks = L.grid_cap_push;
-    return launch_pdl_if((L.pdl_mask & 2) != 0, k_pack_push, (int)blocks, kThreads, s, x, g, scale);
-}
 
-cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x) {
-    int64_t blocks = ((x.lay.shard >> 3) + kThreads - 1) / kThreads;
-    if (blocks > L.grid_cap_reduce) blocks = L.grid_cap_reduce;   // persistent: one fence per block
-    return launch_pdl_if((L.pdl_mask & 4) != 0, k_reduce_shard, (int)blocks, kThreads, s, x);
-}
 
-cudaError_t launch_update_gather(cudaStream_t s, const Launch& L, const XArgs& x, const UpdConst& c,
-                                 float* th, float* d, float* m, int64_t* last) {
-    const int grid = (int)host_units(x);  // flat: one unit per block
-    if (c.a_rms != 0.0f)
-        return launch_pdl_if((L.pdl_mask & 8) != 0, k_update_gather<true>, grid, kThreads, s, x, c, th, d, m, last);
-    else
-        return launch_pdl_if((L.pdl_mask & 8) != 0, k_update_gather<false>, grid, kThreads, s, x, c, th, d, m, last);
-}
 
 cudaError_t launch_bn_stage(cudaStream_t s, const XArgs& x, const float* mean, const float* var,
                             int64_t C) {

@@ -49,11 +49,8 @@ struct Ticket {
 struct Launch {
     int sm_count;
     int grid_cap_stream;   // SMs x resident blocks of the streaming kernels (informational)
-    int grid_cap_push;     // SMs x resident blocks of k_pack_push (persistent grid)
-    int grid_cap_reduce;   // SMs x resident blocks of k_reduce_shard (persistent grid)
     int grid_xstep;        // SMs x resident blocks of k_xstep (cooperative, all co-resident)
-    int pdl_mask;          // programmatic dependent launch per kernel group: 1 = k = 1 kernels,
-                           // 2 = k_pack_push, 4 = k_reduce_shard, 8 = k_update_gather
+    int pdl_mask;          // programmatic dependent launch: bit 1 = the k = 1 kernels
 };
 
 // ---- single-GPU building blocks (sub-step ABI and world == 1)
@@ -70,8 +67,6 @@ cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64
                           int64_t* st_reset, int64_t* last);
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last);
 int stream_blocks_per_sm();
-int push_blocks_per_sm();
-int reduce_blocks_per_sm();
 
 // ---- world > 1 exchange over peer memory (NVLink / NVSwitch)
 struct XArgs {
@@ -91,11 +86,6 @@ struct XArgs {
 // all ranks' reduces observed, update start, update end.
 enum { TR_PACK_START = 0, TR_PACK_END, TR_RED_START, TR_RED_GO, TR_RED_END, TR_UPD_START, TR_UPD_GO,
        TR_UPD_END, TR_PUB_END, TR_A_SEEN /* + rank, 8 words */ = 9, TR_WORDS = 17 };
-cudaError_t launch_pack_push(cudaStream_t s, const Launch& L, const XArgs& x, const float* g,
-                             float scale);
-cudaError_t launch_reduce_shard(cudaStream_t s, const Launch& L, const XArgs& x);
-cudaError_t launch_update_gather(cudaStream_t s, const Launch& L, const XArgs& x, const UpdConst& c,
-                                 float* th, float* d, float* m, int64_t* last);
 // One persistent cooperative kernel for the whole world > 1 step (pack+push, exact
 // reduce of the own shard with per-chunk release, update with the all-gather fused).
 struct XStep {

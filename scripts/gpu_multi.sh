@@ -10,7 +10,7 @@ timeout 300 python bench.py --no-cpu-baseline > gpurun_out/bench_n1.log 2>&1; ec
 timeout 300 python bench.py --mode fused --no-cpu-baseline > gpurun_out/bench_n1_fused.log 2>&1; echo "rc=$?" >> gpurun_out/bench_n1_fused.log
 timeout 300 python bench.py --depth 152 --no-cpu-baseline --steps 1000 > gpurun_out/bench_r152_n1.log 2>&1; echo "rc=$?" >> gpurun_out/bench_r152_n1.log
 if [ "$N" -gt 1 ]; then
-  timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29500 bench.py --gpus $N --trace > gpurun_out/bench_n$N.log 2>&1; echo "rc=$?" >> gpurun_out/bench_n$N.log
+  timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29500 bench.py --gpus $N > gpurun_out/bench_n$N.log 2>&1; echo "rc=$?" >> gpurun_out/bench_n$N.log
   timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29501 bench.py --gpus $N --depth 152 --steps 1000 > gpurun_out/bench_r152_n$N.log 2>&1; echo "rc=$?" >> gpurun_out/bench_r152_n$N.log
 fi
 echo done

@@ -201,7 +201,7 @@ int main(int argc, char** argv) {
     cudaMemcpy(d0, hd.data(), n * 4, cudaMemcpyHostToDevice);
     cudaMemcpy(m0, hm.data(), n * 4, cudaMemcpyHostToDevice);
     UpdConst c{0.9f, 0.99f, (float)(1.0 - 0.99), 1e-8f, 6.4f, 0.00915781944436709f, 4.644572721354529e-05f, 1.0f / 1024};
-    const Launch L{sms, sms * stream_blocks_per_sm(), sms * push_blocks_per_sm(), sms * reduce_blocks_per_sm(), 0, 0x1};  // production launchers now use flat grids
+    const Launch L{sms, sms * stream_blocks_per_sm(), 0, 0x1};  // production launchers now use flat grids
     auto reset = [&] {
         cudaMemcpy(th, th0, n * 4, cudaMemcpyDeviceToDevice);
         cudaMemcpy(d, d0, n * 4, cudaMemcpyDeviceToDevice);

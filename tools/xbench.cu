@@ -133,7 +133,7 @@ int main(int argc, char** argv) {
         const double us = worst / iters * 1e3;
         printf("%-46s %9.2f us  %8.1f GB/s\n", name, us, bytes / us / 1e3);
     };
-    const Launch L{sms, 0, 0, 0, 0, 0x1};
+    const Launch L{sms, 0, 0, 0x1};
     const int ups = (int)(((shard >> 3) + 255) / 256);
     // pack (local only) for reference
     int64_t* dst; CKE(cudaSetDevice(0));
