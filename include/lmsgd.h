@@ -193,8 +193,8 @@ lmsgd_status lmsgd_query_status(lmsgd_ctx* ctx, lmsgd_step_status* out);
 /* ---------------------------------------------------------------- profiling
  * Per-kernel device timing of lmsgd_step, measured with CUDA events recorded on
  * the step's stream around each kernel launch (used by bench.py for the roofline
- * of the dominant kernel).  Phases: 0 = pack (k_pack / k_pack_push / k_fused1),
- * 1 = reduce (k_reduce_shard), 2 = update (k_update / k_update_gather). */
+ * of the dominant kernel).  Phases: 0 = pack (k_pack / k_fused1), 2 = update
+ * (k_update; for world > 1 the whole step, whose kernels overlap -- use tracing). */
 
 /* max_launches > 0: start recording (event pool sized for that many kernel
  * launches; further launches are not timed).  0: stop and discard.  Synchronous. */
