@@ -284,14 +284,18 @@ def main():
     kernels_per_step = 2 if flags else (2 if world == 1 else 3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
+    host_s = [0.0]
+
     def timed(profile: bool):
         if profile:
             L.lmsgd_profile_enable(ctx, kernels_per_step * args.steps)
         barrier()
         torch.cuda.synchronize()
         e0.record(stream)
+        h0 = time.perf_counter()
         for i in range(args.steps):
             step(args.warmup + i)
+        host_s[0] = time.perf_counter() - h0
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -308,6 +312,7 @@ def main():
     clocks.start()
     ms, _ = timed(False)
     ck = clocks.stop()
+    host_us_per_step = host_s[0] / args.steps * 1e6   # enqueue cost; < device time => not host-bound
     # 2) the same K steps again with CUDA events around every kernel (per-kernel roofline)
     # 2) per-kernel durations of the same K steps, measured in a second pass:
     #    N = 1: CUDA events around every kernel (lmsgd_profile_enable);
@@ -478,6 +483,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e,
             "clocks": ck, "gpu_launches": kernels_per_step * args.steps,
             "profile_pass_ms_per_step": (ms_prof / args.steps) if ms_prof else None,
+            "host_enqueue_us_per_step": host_us_per_step,
             "trace": trace,
         }
         print(json.dumps(line), flush=True)

@@ -126,6 +126,27 @@ def main():
         assert np.array_equal(H(mean), om) and np.array_equal(H(var), ov), "BN average not bit-exact"
     L.lmsgd_finalize(ctx)
 
+    # ---- longer run: random schedule steps, replica bit-identity every step,
+    #      resync parity every 10th step
+    n = 333_331
+    ctx = L.lmsgd_init(world, rank, local, n, S)
+    L.connect_process_group(ctx)
+    a = synth.grad_scale(n)
+    th0 = synth.theta0(n, None)
+    th, d, m = D(th0), D(np.zeros(n, np.float32)), D(np.zeros(n, np.float32))
+    rng = np.random.default_rng(11)
+    for it in range(40):
+        t = int(rng.integers(1, 3519))
+        g = synth.grads(world, t, n, a)
+        prev = (H(th), H(d), H(m)) if it % 10 == 9 else None
+        L.lmsgd_step(ctx, th, D(g[rank]), d, m, L.lmsgd_schedule_at(None, L.make_cluster(), t))
+        if prev is not None:
+            code, st = L.lmsgd_query_status(ctx)
+            assert code == 0
+            check_state(H(th), H(d), H(m), *prev, exchange.exchange(list(g), S).ghat, schedule.coeffs_at(t))
+        replicas_identical(th, d, m)
+    L.lmsgd_finalize(ctx)
+
     # ---- full ResNet-50 buffer, sampled check
     n = synth.resnet_n_params(50)
     ctx = L.lmsgd_init(world, rank, local, n, S)
@@ -144,6 +165,20 @@ def main():
     check_state(H(th)[idx], H(d)[idx], H(m)[idx], th0[idx], z, z, ex.ghat, schedule.coeffs_at(1))
     replicas_identical(th, d, m)
     L.lmsgd_finalize(ctx)
+
+    # ---- a rank that does not step: the others time out instead of hanging
+    if os.environ.get("LMSGD_TEST_TIMEOUT") == "1":
+        n = 4096
+        ctx = L.lmsgd_init(world, rank, local, n, S)
+        L.connect_process_group(ctx)
+        th, d, m = D(np.zeros(n, np.float32)), D(np.zeros(n, np.float32)), D(np.zeros(n, np.float32))
+        if rank == 0:
+            L.lmsgd_step(ctx, th, D(np.ones(n, np.float32)), d, m, L.make_coeffs(1.0, 1.0, 0.0))
+            code, st = L.lmsgd_query_status(ctx)
+            assert code == L.LMSGD_ERR_TIMEOUT and st.skipped == 1, (code, st.skipped)
+            assert not H(th).any()
+        dist.barrier()
+        L.lmsgd_finalize(ctx)
 
     dist.barrier()
     if rank == 0:

@@ -345,3 +345,52 @@ def test_resnet50_full_size_sampled(t):
     check_state(host(th)[idx], host(d)[idx], host(m)[idx], th0[idx], d0[idx], m0[idx], ex.ghat,
                 schedule.coeffs_at(t))
     L.lmsgd_finalize(ctx)
+
+
+# ------------------------------------------------------------------ API behaviour on the GPU
+
+def test_api_errors_on_gpu():
+    n = 1000
+    ctx = L.lmsgd_init(1, 0, 0, n, 1.0)
+    th = torch.zeros(n + 1, device=DEV)
+    g = torch.zeros(n, device=DEV)
+    import ctypes
+    st = L.lib().lmsgd_step(ctx.ptr, None, ctypes.c_void_p(th.data_ptr() + 4), ctypes.c_void_p(g.data_ptr()),
+                            ctypes.c_void_p(g.data_ptr()), ctypes.c_void_p(g.data_ptr()),
+                            ctypes.byref(L.make_coeffs(0.1, 1.0, 0.0)))
+    assert st == L.LMSGD_ERR_INVALID_ARG                  # misaligned (offset 4 B) params
+    assert b"aligned" in L.lib().lmsgd_last_error(ctx.ptr)
+    for bad in (L.make_coeffs(0.0, 1.0, 0.0), L.make_coeffs(0.1, 1.5, 0.0), L.make_coeffs(0.1, 1.0, -1.0)):
+        with pytest.raises(L.LmsgdError) as e:
+            L.lmsgd_step(ctx, th[:n], g, g.clone(), g.clone(), bad)
+        assert e.value.status == L.LMSGD_ERR_INVALID_ARG
+    with pytest.raises(L.LmsgdError) as e:
+        L.lmsgd_query_status(ctx)                   # no step yet
+    assert e.value.status == L.LMSGD_ERR_STATE
+    mean, var = torch.randn(64, device=DEV), torch.rand(64, device=DEV)
+    m0, v0 = mean.clone(), var.clone()
+    L.lmsgd_bn_stats_allreduce(ctx, mean, var)     # world 1: identity
+    assert torch.equal(mean, m0) and torch.equal(var, v0)
+    L.lmsgd_finalize(ctx)
+    ctx2 = L.lmsgd_init(2, 0, 0, n, 1.0)             # world 2, never connected
+    with pytest.raises(L.LmsgdError) as e:
+        L.lmsgd_step(ctx2, th[:n], g, g.clone(), g.clone(), L.make_coeffs(0.1, 1.0, 0.0))
+    assert e.value.status == L.LMSGD_ERR_STATE
+    L.lmsgd_finalize(ctx2)
+
+
+def test_goyal_schedule_through_ctx():
+    """The Goyal et al. schedule selected in the cluster struct."""
+    n = 50_000
+    cl_c = L.make_cluster(1024, 32, 1_281_167, L.SCHEDULE_GOYAL)
+    cl_o = schedule.Cluster(schedule="goyal")
+    th0, d0, m0 = init_state(n)
+    ctx = L.lmsgd_init(1, 0, 0, n, 1024.0)
+    th, d, m = dev(th0), dev(d0), dev(m0)
+    for t in (1, 1200, 2400, 3200):
+        g = synth.grads(1, t, n)
+        prev = host(th), host(d), host(m)
+        L.lmsgd_step(ctx, th, dev(g[0]), d, m, L.lmsgd_schedule_at(None, cl_c, t))
+        check_state(host(th), host(d), host(m), *prev, exchange.exchange(list(g), 1024.0).ghat,
+                    schedule.coeffs_at(t, schedule.Hyper(), cl_o))
+    L.lmsgd_finalize(ctx)

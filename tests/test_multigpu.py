@@ -12,11 +12,30 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs >= 2 GPUs")
-def test_exchange_on_all_gpus():
-    k = torch.cuda.device_count()
+NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+
+
+def _run(k, port, extra_env=None):
     env = dict(os.environ, LMSGD_TIMEOUT_MS="20000", PYTHONPATH=ROOT)
+    env.update(extra_env or {})
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={k}",
-           "--master-addr=127.0.0.1", "--master-port=29533", os.path.join(ROOT, "tests", "mgpu_worker.py")]
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.join(ROOT, "tests", "mgpu_worker.py")]
     r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0 and f"MGPU_OK world={k}" in r.stdout, r.stdout[-4000:] + r.stderr[-4000:]
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_exchange_on_all_gpus():
+    _run(NGPU, 29533)
+
+
+@pytest.mark.skipif(NGPU < 3, reason="needs >= 3 GPUs")
+def test_exchange_three_ranks():
+    # k = 3: 1/(k s) is not a power of two, shards of a ragged size
+    _run(3, 29534)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="needs >= 2 GPUs")
+def test_exchange_two_ranks_and_timeout():
+    # a rank that never steps makes the other time out (status, no hang)
+    _run(2, 29535, {"LMSGD_TEST_TIMEOUT": "1", "LMSGD_TIMEOUT_MS": "3000"})

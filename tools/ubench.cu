@@ -298,6 +298,9 @@ int main(int argc, char** argv) {
              k_stream_tma<true, false, 2048, 6><<<sms, kTmaThreads, 6 * tma_stage_bytes<false, 2048>()>>>(h, n, 1024.f, c, th, d, m, st, nullptr); }},
         {"G4 pack flat+update flat", [&] { k_pack_flat<<<fgrid, kThreads>>>(g, n, n_pad, 1024.f, h, st);
              k_update_flat<true><<<(int)(((n >> 3) + kThreads - 1) / kThreads), kThreads>>>(h, n, c, th, d, m); }},
+        {"G5 pack evict_last+update flat", [&] { k_pack_l2<<<fgrid, kThreads>>>(g, n, n_pad, 1024.f, h, st);
+             k_update_flat<true><<<(int)(((n >> 3) + kThreads - 1) / kThreads), kThreads>>>(h, n, c, th, d, m); }},
+        {"G6 prod pack+update (PDL)", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr); }},
         {"G3 pack+update tma", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st);
              k_stream_tma<true, false, 2048, 6><<<sms, kTmaThreads, 6 * tma_stage_bytes<false, 2048>()>>>(h, n, 1024.f, c, th, d, m, st, nullptr); }},
     };
