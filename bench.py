@@ -49,6 +49,9 @@ def parse():
                         "fused = single-pass pack+update (LMSGD_FLAG_NO_SKIP)")
     p.add_argument("--t-start", type=int, default=1, help="first schedule step timed (1 = RMSprop warm-up)")
     p.add_argument("--e2e-steps", type=int, default=50)
+    p.add_argument("--full-schedule", action="store_true",
+                   help="config C5: time the whole 90-epoch schedule (T = 3,519 steps at 32k from t = 1) with the "
+                        "BN statistics average at every epoch crossing; use with --depth 152")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-profile", action="store_true", help="do not record per-kernel events")
     p.add_argument("--trace", action="store_true", help="(kept for compatibility; N>1 always traces the profile pass)")
@@ -250,7 +253,17 @@ def main():
     m = torch.zeros(n, device=devc)
     cl = L.make_cluster()
     T = L.lmsgd_schedule_steps(cl)
+    if args.full_schedule:
+        args.steps, args.t_start = T, 1
     coeffs = [L.lmsgd_schedule_at(None, cl, (args.t_start - 1 + i) % T + 1) for i in range(args.warmup + args.steps)]
+    # BN sync points of the full-schedule run: steps whose epoch crosses an integer
+    bn_at = set()
+    if args.full_schedule:
+        ep = [c.epoch for c in coeffs[args.warmup:]] + [90.0]
+        bn_at = {i for i in range(args.steps) if int(ep[i + 1]) > int(ep[i])}
+        C_bn = sum(synth.resnet_bn_channels(args.depth))
+        bn_mean = torch.randn(C_bn, device=devc)
+        bn_var = torch.rand(C_bn, device=devc) + 0.1
     stream = torch.cuda.current_stream()
     sp = ctypes.c_void_p(stream.cuda_stream)
     P = ctypes.c_void_p
@@ -295,6 +308,8 @@ def main():
         h0 = time.perf_counter()
         for i in range(args.steps):
             step(args.warmup + i)
+            if i in bn_at:
+                L.lmsgd_bn_stats_allreduce(ctx, bn_mean, bn_var)
         host_s[0] = time.perf_counter() - h0
         e1.record(stream)
         torch.cuda.synchronize()
@@ -484,6 +499,9 @@ def main():
             "clocks": ck, "gpu_launches": kernels_per_step * args.steps,
             "profile_pass_ms_per_step": (ms_prof / args.steps) if ms_prof else None,
             "host_enqueue_us_per_step": host_us_per_step,
+            "full_schedule": ({"steps": args.steps, "bn_syncs": len(bn_at), "total_s": ms / 1e3,
+                               "note": "config C5: whole 90-epoch slow-start / RMSprop warm-up schedule"}
+                              if args.full_schedule else None),
             "trace": trace,
         }
         print(json.dumps(line), flush=True)
