@@ -28,10 +28,7 @@ struct lmsgd_ctx {
     lmsgd::Peers peers{};
     bool connected = false;
     unsigned int* tickets = nullptr;  // device [4]
-    unsigned int* xctr = nullptr;     // device [4 + 2 nchunks] counters of the world > 1 kernels
-    int64_t* xstage = nullptr;        // device [nchunks + 3] stage offsets of k_xflow
-    int64_t xflow_items = 0, xscan_items = 0;
-    bool flow = false;                // LMSGD_XFLOW=1: pipelined single-kernel exchange (experimental)
+    unsigned int* xctr = nullptr;     // device [4 + nchunks] counters of the world > 1 kernels
     int64_t* last = nullptr;          // device lmsgd_step_status of the last step
     float* d_grads = nullptr;         // device staging for lmsgd_step_host (lazy)
     uint32_t step = 0, bn_calls = 0;
@@ -142,11 +139,7 @@ Layout make_layout(int world, int64_t n) {
     const int64_t units_per_shard = (L.shard / 8 + 255) / 256;
     L.cu = 32;
     L.nchunks = static_cast<int32_t>((units_per_shard + L.cu - 1) / L.cu);
-    L.cu_flow = 256;
-    L.nchunks_flow = static_cast<int32_t>((units_per_shard + L.cu_flow - 1) / L.cu_flow);
     L.off_cflags = off;
-    if (world > 1) off = align_up(off + int64_t(L.nchunks) * LMSGD_MAX_WORLD * 4, 256);
-    L.off_aflags = off;
     if (world > 1) off = align_up(off + int64_t(L.nchunks) * LMSGD_MAX_WORLD * 4, 256);
     L.bytes = off;
     return L;
@@ -279,28 +272,12 @@ lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_
     }
     if ((e = cudaMalloc(&c->tickets, 4 * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMemset(c->tickets, 0, 4 * sizeof(unsigned int))) != cudaSuccess ||
-        (e = cudaMalloc(&c->xctr, (4 + 2 * c->lay.nchunks) * sizeof(unsigned int))) != cudaSuccess ||
-        (e = cudaMemset(c->xctr, 0, (4 + 2 * c->lay.nchunks) * sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMalloc(&c->xctr, (4 + c->lay.nchunks) * sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMemset(c->xctr, 0, (4 + c->lay.nchunks) * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMalloc(&c->last, sizeof(lmsgd_step_status))) != cudaSuccess ||
         (e = cudaMemset(c->last, 0, sizeof(lmsgd_step_status))) != cudaSuccess) {
         g_err = std::string("context allocations: ") + cudaGetErrorString(e);
         return bail(LMSGD_ERR_CUDA);
-    }
-    if (world > 1) {   // k_xflow stage table: stage s holds P(s) [s < C], Rd(s-1) [1 <= s <= C],
-                       // U(s-2-lag) [2+lag <= s <= C+1+lag]
-        const int64_t C = c->lay.nchunks_flow, cu = c->lay.cu_flow, lag = lmsgd::kFlowLag;
-        const int64_t S = C + 2 + lag;
-        std::vector<int64_t> off(S + 1, 0);
-        for (int64_t st = 0; st < S; ++st)
-            off[st + 1] = off[st] + (st < C ? cu : 0) + (st >= 1 && st <= C ? cu : 0) +
-                          (st >= 2 + lag ? int64_t(world) * cu : 0);
-        c->xscan_items = ((c->n + 7) / 8 + 255) / 256;   // k_xscan blocks: one unit each
-        c->xflow_items = off[S];
-        if ((e = cudaMalloc(&c->xstage, (S + 1) * sizeof(int64_t))) != cudaSuccess ||
-            (e = cudaMemcpy(c->xstage, off.data(), (S + 1) * sizeof(int64_t), cudaMemcpyHostToDevice)) != cudaSuccess) {
-            g_err = "stage table"; return bail(LMSGD_ERR_CUDA);
-        }
-        if (const char* f = std::getenv("LMSGD_XFLOW")) c->flow = (f[0] == '1');
     }
     if ((e = cudaDeviceSynchronize()) != cudaSuccess) { g_err = cudaGetErrorString(e); return bail(LMSGD_ERR_CUDA); }
     c->L = launch_for_current_device();
@@ -349,7 +326,6 @@ lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
         if (c->buf) cudaFree(c->buf);
         if (c->tickets) cudaFree(c->tickets);
         if (c->xctr) cudaFree(c->xctr);
-        if (c->xstage) cudaFree(c->xstage);
         if (c->last) cudaFree(c->last);
         if (c->d_grads) cudaFree(c->d_grads);
         if (c->d_trace) cudaFree(c->d_trace);
@@ -394,11 +370,7 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
         return LMSGD_OK;
     }
     const lmsgd::XArgs x = xargs(c, epoch);
-    lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, c->xstage, c->xscan_items};
-    if (c->flow) {
-        CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xflow(s, c->L, a, c->xflow_items); }));
-        return LMSGD_OK;
-    }
+    lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr};
     CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, c->L, a); }));
     return LMSGD_OK;
 }

@@ -590,213 +590,6 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
     update8<RMS>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, a.c, a.th, a.d, a.m);
 }
 
-// ------------------------------------------------------------------ world > 1, pipelined flow
-//
-// k_xflow: one flat kernel whose blocks take work items from a queue (an atomic
-// head; items start in queue order, and an item only ever waits for items that
-// precede it in every rank's queue, so the kernel cannot deadlock however many
-// blocks are resident).  Queue:
-//   scan items  -- non-finite / saturation statistics of this rank's gradient; the
-//                  last one releases flag A (= this rank's status is final);
-//   stage s     -- P(s): pack + push of chunk s for every owner (one fence per item,
-//                  the last item of the chunk releases aflag[s]);
-//                  Rd(s-1): exact reduce of chunk s-1 of my shard once every rank
-//                  released aflag[s-1] (the last item releases cflag[s-1]);
-//                  U(s-2): update of chunk s-2, all owners, once the skip decision
-//                  (local flag D, made by the first U item from every rank's A) and
-//                  the owner's cflag[s-2] are in.
-// So the fp16 push (NVLink), the reduce and the update (HBM) of successive chunks
-// overlap, while a non-finite gradient anywhere still skips every update.
-__device__ __forceinline__ uint32_t* aflag(const XArgs& x, int r, int c, int p) {
-    return reinterpret_cast<uint32_t*>(x.peers.base[r] + x.lay.off_aflags) + (int64_t)c * LMSGD_MAX_WORLD + p;
-}
-
-__device__ __forceinline__ void release_chunk(const XArgs& x, uint32_t* (*slot)(const XArgs&, int, int, int), int c) {
-    __threadfence_system();
-    for (int p = 0; p < x.world; ++p) st_relaxed_sys(slot(x, p, c, x.rank), x.epoch);
-}
-
-// k_xscan: non-finite / saturation statistics of this rank's gradient (flat grid,
-// one unit per block); the last block releases flag A (this rank's words are final).
-__global__ void __launch_bounds__(kThreads) k_xscan(XStep a) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // k_xflow may start now
-    const XArgs& x = a.x;
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_PACK_START);
-    int64_t first = kNone;
-    unsigned sat = 0;
-    const int64_t v = gtid();
-    if (v < ((x.n + 7) >> 3)) {
-        float xv[8];
-        load8_g(a.g, v << 3, x.n, xv);
-        (void)pack8(xv, a.scale, v << 3, first, sat);
-    }
-    flush_status(first, sat, status_of(x, x.rank), ST_PACK_SAT);
-    __threadfence();   // gpu scope per block; the last block's publish fences at system scope
-    __syncthreads();
-    if (threadIdx.x == 0 && atomicAdd(x.ticket + 0, 1u) + 1u == gridDim.x) {
-        x.ticket[0] = 0;
-        stamp(x, TR_PACK_END);
-        publish(x, FLAG_A);
-    }
-}
-
-template <bool RMS>
-__global__ void __launch_bounds__(kThreads) k_xflow(XStep a) {
-    // no griddepcontrol.wait: nothing here reads what k_xscan writes except through flag A
-    const XArgs& x = a.x;
-    __shared__ int64_t s_item;
-    __shared__ int s_ok;
-    const bool t0 = threadIdx.x == 0;
-    const int k = x.world;
-    const int cu = x.lay.cu_flow;
-    const int C = x.lay.nchunks_flow;
-    const int S = C + 2 + kFlowLag;
-    if (t0) {
-        const int64_t it = (int64_t)atomicAdd(a.ctr + 1, 1u);
-        if (it == a.stage_off[S] - 1) a.ctr[1] = 0;   // every item has been taken: reset the head
-        s_item = it;
-    }
-    __syncthreads();
-    const int64_t q = s_item;
-    const int64_t gsh = x.lay.shard >> 3;
-    const int64_t ups = (gsh + kThreads - 1) / kThreads;
-    int64_t* mine = status_of(x, x.rank);
-
-    int lo = 0, hi = S;   // stage s: [stage_off[s], stage_off[s+1])
-    while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (a.stage_off[mid] <= q) lo = mid; else hi = mid;
-    }
-    const int s = lo;
-    int64_t j = q - a.stage_off[s];
-
-    if (s < C) {
-        if (j < cu) {   // ---- P(s): pack + push unit s*cu + j to every owner
-            const int c = s;
-            const int64_t us = (int64_t)c * cu + j;
-            const int64_t gi = us * kThreads + threadIdx.x;
-            if (us < ups && gi < gsh) {
-                int64_t first = kNone;
-                unsigned sat = 0;
-                for (int qq = 0; qq < k; ++qq) {
-                    const int owner = (qq + x.rank) % k;
-                    const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
-                    float xv[8];
-                    load8_g(a.g, j0, x.n, xv);
-                    uint16_t* dst = reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
-                                    (int64_t)x.rank * x.lay.shard + (gi << 3);
-                    *reinterpret_cast<uint4*>(dst) = pack8(xv, a.scale, j0, first, sat);
-                }
-            }
-            __threadfence_system();
-            __syncthreads();
-            if (t0 && atomicAdd(a.ctr + 4 + x.lay.nchunks + c, 1u) + 1u == (unsigned)cu) {
-                a.ctr[4 + x.lay.nchunks + c] = 0;
-                release_chunk(x, aflag, c);
-            }
-            return;
-        }
-        j -= cu;
-    }
-    if (s >= 1 && s <= C) {
-        if (j < cu) {   // ---- Rd(s-1): exact reduce of unit (s-1)*cu + j of my shard
-            const int c = s - 1;
-            if (t0) {
-                int ok = 1;
-                for (int p = 0; p < k && ok; ++p) ok = spin_flag(x, aflag(x, x.rank, c, p));
-                s_ok = ok;
-            }
-            __syncthreads();
-            if (!s_ok) {
-                if (t0) mine[ST_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-                return;
-            }
-            const int64_t us = (int64_t)c * cu + j;
-            const int64_t gi = us * kThreads + threadIdx.x;
-            unsigned sat = 0;
-            if (us < ups && gi < gsh) {
-                const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
-                uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
-                const int64_t j0 = gi << 3;
-                double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-                for (int p = 0; p < k; ++p) {
-                    const uint4 qv = *reinterpret_cast<const uint4*>(recv + (int64_t)p * x.lay.shard + j0);
-                    const uint32_t w[4] = {qv.x, qv.y, qv.z, qv.w};
-#pragma unroll
-                    for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
-                }
-                unsigned short o[8];
-#pragma unroll
-                for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
-                *reinterpret_cast<uint4*>(R + j0) =
-                    make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
-                               o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
-            }
-            flush_status(kNone, sat, mine, ST_SUM_SAT);
-            __threadfence_system();
-            __syncthreads();
-            if (t0 && atomicAdd(a.ctr + 4 + c, 1u) + 1u == (unsigned)cu) {
-                a.ctr[4 + c] = 0;
-                if (c == 0) stamp(x, TR_RED_GO);
-                if (c == C - 1) stamp(x, TR_RED_END);
-                release_chunk(x, cflag, c);
-            }
-            return;
-        }
-        j -= cu;
-    }
-    // ---- U(c), c = s - 2 - lag: update unit of one owner
-    const int c = s - 2 - kFlowLag;
-    const int owner = (int)((j % k + x.rank) % k);
-    const int64_t us = (int64_t)c * cu + j / k;
-    if (t0) {
-        int ok = 1;
-        if (c == 0 && j == 0) {   // the decision maker: every rank's scan statistics
-            stamp(x, TR_UPD_START);
-            ok = thread_wait_all(x, FLAG_A) ? 1 : 0;
-            int64_t gfirst = kNone, psat = 0, err = ok ? 0 : (int64_t)LMSGD_ERR_TIMEOUT;
-            for (int p = 0; p < k; ++p) {
-                const volatile int64_t* sp = status_of(x, p);
-                const int64_t f = sp[ST_FIRST];
-                gfirst = f < gfirst ? f : gfirst;
-                psat += sp[ST_PACK_SAT];
-                err = err ? err : sp[ST_ERROR];
-            }
-            mine[ST_G_FIRST] = gfirst;
-            mine[ST_G_PACK_SAT] = psat;
-            mine[ST_G_ERROR] = err;
-            int64_t* nxt = reinterpret_cast<int64_t*>(x.peers.base[x.rank] + x.lay.off_status) +
-                           (x.parity ^ 1) * ST_WORDS;
-            for (int w = 0; w < ST_WORDS; ++w) nxt[w] = (w == ST_FIRST || w == ST_G_FIRST) ? kNone : 0;
-            __threadfence();
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag_slot(x, x.rank, FLAG_D)), "r"(x.epoch)
-                         : "memory");
-            stamp(x, TR_RED_START);
-        }
-        ok = ok && spin_flag(x, flag_slot(x, x.rank, FLAG_D));
-        if (ok) {
-            // wait for the owner's chunk even when the step is skipped: this step may
-            // end only after every owner's reduce has read its receive slots
-            if (us < ups && !spin_flag(x, cflag(x, x.rank, c, owner))) {
-                ok = 0;
-                mine[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-            }
-            const volatile int64_t* vm = mine;
-            if (vm[ST_G_FIRST] != kNone || vm[ST_G_ERROR] != 0) ok = 0;   // skipped step
-        }
-        if (c == 0 && j == 0) stamp(x, TR_UPD_GO);
-        s_ok = ok;
-    }
-    __syncthreads();
-    if (!s_ok || us >= ups) return;
-    const int64_t gi = us * kThreads + threadIdx.x;
-    if (gi >= gsh) return;
-    const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
-    if (j0 >= x.n) return;
-    const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
-    update8<RMS>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, a.c, a.th, a.d, a.m);
-}
-
 // The step's public status record; runs after k_xupdate (every owner's reduce has
 // been observed by then, so every rank's sum saturation count is final).
 __global__ void k_xfinalize(XStep a) {
@@ -895,17 +688,6 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
     return launch_pdl_if(true, k_xfinalize, 1, 32, s, a);
 }
 
-cudaError_t launch_xflow(cudaStream_t s, const Launch& L, const XStep& a, int64_t items) {
-    (void)L;
-    cudaError_t e = launch_pdl_if(false, k_xscan, (int)a.scan_items, kThreads, s, a);
-    if (e != cudaSuccess) return e;
-    if (a.c.a_rms != 0.0f)
-        e = launch_pdl_if(true, k_xflow<true>, (int)items, kThreads, s, a);
-    else
-        e = launch_pdl_if(true, k_xflow<false>, (int)items, kThreads, s, a);
-    if (e != cudaSuccess) return e;
-    return launch_pdl_if(true, k_xfinalize, 1, 32, s, a);
-}
 
 int stream_blocks_per_sm() {
     int worst = 1 << 30, b = 0;

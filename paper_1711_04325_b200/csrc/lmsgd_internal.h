@@ -33,11 +33,8 @@ struct Layout {
     int64_t off_flags;    // uint32: A at +0, B at +128 B, C at +256 B, D at +384 B, each [LMSGD_MAX_WORLD]
     int64_t off_bn;       // float [2 parity][2 * LMSGD_MAX_BN_CHANNELS]
     int64_t off_cflags;   // uint32 [nchunks][LMSGD_MAX_WORLD]: owner o's "R chunk c ready" = epoch
-    int64_t off_aflags;   // uint32 [nchunks][LMSGD_MAX_WORLD]: rank p's "payload of chunk c sent" = epoch
     int32_t cu;           // work units (2048 elements) per reduce chunk
     int32_t nchunks;      // chunks per shard
-    int32_t cu_flow;      // k_xflow: units per pipeline chunk
-    int32_t nchunks_flow; // k_xflow: pipeline chunks per shard (<= nchunks)
     int64_t bytes;
 };
 
@@ -99,14 +96,9 @@ struct XStep {
     float *th, *d, *m;
     int64_t* last;
     unsigned int* ctr;   // local counters, reset by their completer: [0] pack blocks done,
-                         // [1] work-queue head, [2] scan items done, [3] unused,
-                         // [4 + c] reduce units of chunk c, [4 + C + c] pack items of chunk c
-    const int64_t* stage_off;  // k_xflow: first item of each pipeline stage [nchunks + 3]
-    int64_t scan_items;        // k_xflow: scan items ahead of the stages
+                         // [1..3] unused, [4 + c] reduce units of chunk c
 };
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a);
-cudaError_t launch_xflow(cudaStream_t s, const Launch& L, const XStep& a, int64_t items);
-constexpr int kFlowLag = 2;   // k_xflow: U(c) runs in stage c + 2 + kFlowLag
 int xstep_blocks_per_sm();
 
 cudaError_t launch_bn_stage(cudaStream_t s, const XArgs& x, const float* mean, const float* var,
