@@ -23,6 +23,7 @@ namespace lmsgd {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kXUnits = 1;   // k_xupdate: 2048-element units per block
 enum { FLAG_A = 0, FLAG_B = 1, FLAG_C = 2, FLAG_D = 3 };  // pack done, reduce done, BN staged,
                                                          // local: this step's decision stored
 
@@ -504,7 +505,10 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
             stamp(x, TR_RED_START);
         }
     }
-    if (!s_ok) return;
+    if (!s_ok) {
+        if (t0) atomicAdd(a.ctr + 1, 1u);
+        return;
+    }
 
     // ---- 3. exact reduce of this rank's shard, chunk-major over blocks (unit u on
     //         block u % grid), each chunk released as soon as its units are done.
@@ -549,53 +553,73 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
         }
     }
     if (blockIdx.x == 0 && t0) stamp(x, TR_RED_END);
+    if (t0) atomicAdd(a.ctr + 1, 1u);   // k_xfinalize waits for every block of this grid
 }
 
 template <bool RMS>
 __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
-    // no griddepcontrol.wait: ordering with k_xstep1 is by flags D and cflag
+    // no griddepcontrol.wait: ordering with k_xstep1 is by flags D and cflag.
+    // kXUnits units per block: 2 was faster in isolation (tools/xbench.cu, 109 vs
+    // 120 us) but slower in the step (225 vs 215 us at k = 4), so 1.
     const XArgs& x = a.x;
     __shared__ int s_go;
     const int64_t gsh = x.lay.shard >> 3;
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
     const int64_t kcu = (int64_t)x.world * x.lay.cu;
-    const int64_t i = blockIdx.x;
-    const int c = (int)(i / kcu);
-    const int64_t r = i - (int64_t)c * kcu;
-    const int owner = (int)((r % x.world + x.rank) % x.world);
-    const int64_t us = (int64_t)c * x.lay.cu + r / x.world;
+    int owner[kXUnits];
+    int64_t us[kXUnits];
+    int cch[kXUnits];
+#pragma unroll
+    for (int v = 0; v < kXUnits; ++v) {
+        const int64_t i = (int64_t)blockIdx.x * kXUnits + v;
+        cch[v] = (int)(i / kcu);
+        const int64_t r = i - (int64_t)cch[v] * kcu;
+        owner[v] = (int)((r % x.world + x.rank) % x.world);
+        us[v] = (int64_t)cch[v] * x.lay.cu + r / x.world;
+        if (cch[v] >= x.lay.nchunks) us[v] = ups;   // past the last unit
+    }
     if (threadIdx.x == 0) {
-        if (i == 0) stamp(x, TR_UPD_START);
+        if (blockIdx.x == 0) stamp(x, TR_UPD_START);
         int go = spin_flag(x, flag_slot(x, x.rank, FLAG_D)) ? 1 : 0;
         if (go) {
-            const int64_t* mine = status_of(x, x.rank);
-            const volatile int64_t* vm = mine;
+            // wait for the owners' chunks even when the step is skipped: the step may
+            // end only after every owner's reduce has finished reading its receive slots
+            for (int v = 0; v < kXUnits; ++v)
+                if (us[v] < ups && !spin_flag(x, cflag(x, x.rank, cch[v], owner[v]))) {
+                    go = 0;
+                    status_of(x, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+                    break;
+                }
+            const volatile int64_t* vm = status_of(x, x.rank);
             if (vm[ST_G_FIRST] != kNone || vm[ST_G_ERROR] != 0) go = 0;   // skipped step
-            else if (us < ups && !spin_flag(x, cflag(x, x.rank, c, owner))) {
-                go = 0;
-                int64_t* mw = status_of(x, x.rank);
-                mw[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-            }
         }
-        if (i == 0) stamp(x, TR_UPD_GO);
+        if (blockIdx.x == 0) stamp(x, TR_UPD_GO);
         s_go = go;
     }
     __syncthreads();
-    if (!s_go || us >= ups) return;
-    const int64_t gi = us * kThreads + threadIdx.x;
-    if (gi >= gsh) return;
-    const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
-    if (j0 >= x.n) return;
-    const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
-    update8<RMS>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, a.c, a.th, a.d, a.m);
+    if (!s_go) return;
+#pragma unroll
+    for (int v = 0; v < kXUnits; ++v) {
+        if (us[v] >= ups) continue;
+        const int64_t gi = us[v] * kThreads + threadIdx.x;
+        if (gi >= gsh) continue;
+        const int64_t j0 = ((int64_t)owner[v] * gsh + gi) << 3;
+        if (j0 >= x.n) continue;
+        const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner[v]] + x.lay.off_R) + (gi << 3);
+        update8<RMS>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, a.c, a.th, a.d, a.m);
+    }
 }
 
 // The step's public status record; runs after k_xupdate (every owner's reduce has
 // been observed by then, so every rank's sum saturation count is final).
-__global__ void k_xfinalize(XStep a) {
+__global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
     pdl_enter();
     const XArgs& x = a.x;
     if (threadIdx.x != 0) return;
+    // k_xupdate may complete before k_xstep1 (it never waits for its grid): the step
+    // ends only once every k_xstep1 block has retired its last memory operation
+    while (ld_acquire_sys(a.ctr + 1) < xstep1_blocks) __nanosleep(64);
+    a.ctr[1] = 0;
     const volatile int64_t* mine = status_of(x, x.rank);
     const int64_t gfirst = mine[ST_G_FIRST], err = mine[ST_G_ERROR];
     const bool skip = gfirst != kNone || err != 0;
@@ -679,13 +703,13 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
     if (e != cudaSuccess) return e;
     const int64_t gsh = a.x.lay.shard >> 3;
     (void)gsh;
-    const int grid = (int)((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu);
+    const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits);
     if (a.c.a_rms != 0.0f)
         e = launch_pdl_if(true, k_xupdate<true>, grid, kThreads, s, a);
     else
         e = launch_pdl_if(true, k_xupdate<false>, grid, kThreads, s, a);
     if (e != cudaSuccess) return e;
-    return launch_pdl_if(true, k_xfinalize, 1, 32, s, a);
+    return launch_pdl_if(true, k_xfinalize, 1, 32, s, a, (unsigned int)L.grid_xstep);
 }
 
 

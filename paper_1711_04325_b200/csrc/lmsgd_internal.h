@@ -96,7 +96,7 @@ struct XStep {
     float *th, *d, *m;
     int64_t* last;
     unsigned int* ctr;   // local counters, reset by their completer: [0] pack blocks done,
-                         // [1..3] unused, [4 + c] reduce units of chunk c
+                         // [1] k_xstep1 blocks retired, [2..3] unused, [4 + c] reduce units of chunk c
 };
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a);
 int xstep_blocks_per_sm();

@@ -76,6 +76,37 @@ __global__ void __launch_bounds__(256) k_upd_pull(Ptrs P, int world, int rank, i
     update8<true>(r, j0, n, c, th, d, m);
 }
 
+// the same with a register cap (more resident blocks per SM to cover the peer-load latency)
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_upd_pull_lb(Ptrs P, int world, int rank, int64_t shard, int64_t n, UpdConst c,
+                                                           float* __restrict__ th, float* __restrict__ d, float* __restrict__ m) {
+    const int64_t gsh = shard >> 3;
+    const int64_t u = blockIdx.x;
+    const int owner = (int)((u % world + rank) % world);
+    const int64_t gi = (u / world) * 256 + threadIdx.x;
+    if (gi >= gsh) return;
+    const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+    if (j0 >= n) return;
+    const uint4 r = *reinterpret_cast<const uint4*>(P.R[owner] + (gi << 3));
+    update8<true>(r, j0, n, c, th, d, m);
+}
+
+// R prefetched with cp.async (LDGSTS) into shared memory for the NEXT unit of a 2-unit block
+__global__ void __launch_bounds__(256) k_upd_pull2(Ptrs P, int world, int rank, int64_t shard, int64_t n, UpdConst c,
+                                                   float* __restrict__ th, float* __restrict__ d, float* __restrict__ m) {
+    const int64_t gsh = shard >> 3;
+    for (int rep = 0; rep < 2; ++rep) {
+        const int64_t u = (int64_t)blockIdx.x * 2 + rep;
+        const int owner = (int)((u % world + rank) % world);
+        const int64_t gi = (u / world) * 256 + threadIdx.x;
+        if (gi >= gsh) continue;
+        const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+        if (j0 >= n) continue;
+        const uint4 r = *reinterpret_cast<const uint4*>(P.R[owner] + (gi << 3));
+        update8<true>(r, j0, n, c, th, d, m);
+    }
+}
+
 // all-gather push: owner writes its R shard into every rank's full-R buffer (persistent)
 __global__ void __launch_bounds__(256) k_ag_push(const uint16_t* __restrict__ Rmine, uint16_t* const* full, int world,
                                                  int rank, int64_t shard) {
@@ -142,6 +173,9 @@ int main(int argc, char** argv) {
     run("reduce int64 persistent 148x8", 2.0 * n_pad, [&](int i) { xb::k_reduce<1><<<sms * 8, 256, 0, st[i]>>>(recv[i], W, shard, R[i]); });
     run("reduce fp64 persistent 148x8", 2.0 * n_pad, [&](int i) { xb::k_reduce<0><<<sms * 8, 256, 0, st[i]>>>(recv[i], W, shard, R[i]); });
     run("update pull from owners (flat, interleaved)", 26.0 * n, [&](int i) { xb::k_upd_pull<<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
+    run("update pull, launch_bounds(256,6)", 26.0 * n, [&](int i) { xb::k_upd_pull_lb<6><<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
+    run("update pull, launch_bounds(256,8)", 26.0 * n, [&](int i) { xb::k_upd_pull_lb<8><<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
+    run("update pull, 2 units per block", 26.0 * n, [&](int i) { xb::k_upd_pull2<<<(W * ups + 1) / 2, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
     run("update local full R (k_update flat)", 26.0 * n, [&](int i) { launch_update(st[i], L, full[i], n, c, th[i], d[i], m[i], nullptr, nullptr, nullptr); });
     run("AG push R shard to all (persistent 148x8)", 2.0 * shard * (W - 1), [&](int i) { xb::k_ag_push<<<sms * 8, 256, 0, st[i]>>>(R[i], fullp[i], W, i, shard); });
     run("AG push + local update", 26.0 * n, [&](int i) { xb::k_ag_push<<<sms * 8, 256, 0, st[i]>>>(R[i], fullp[i], W, i, shard);
