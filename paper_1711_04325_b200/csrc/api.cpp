@@ -410,8 +410,7 @@ lmsgd_status lmsgd_bn_stats_allreduce(lmsgd_ctx* c, void* stream, float* mean, f
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     lmsgd::XArgs x = xargs(c, ++c->bn_calls);
     if (x.trace) { x.trace = nullptr; --c->trace_steps; }
-    CK(c, lmsgd::launch_bn_stage(s, x, mean, var, C));
-    CK(c, lmsgd::launch_bn_reduce(s, x, mean, var, C));
+    CK(c, lmsgd::launch_bn_allreduce(s, x, mean, var, C));
     return LMSGD_OK;
 }
 

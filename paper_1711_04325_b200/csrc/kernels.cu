@@ -310,29 +310,6 @@ __device__ __forceinline__ void stamp(const XArgs& x, int which) {
     if (x.trace) x.trace[which] = (int64_t)globaltimer();
 }
 
-// Every block: wait until all ranks have published `which` for this epoch.
-// Returns false (and records LMSGD_ERR_TIMEOUT locally) on timeout.
-__device__ bool block_wait(const XArgs& x, int which) {
-    __shared__ int timed_out;
-    if (threadIdx.x == 0) timed_out = 0;
-    __syncthreads();
-    if (threadIdx.x < x.world) {
-        const uint32_t* f = flag_slot(x, x.rank, which) + threadIdx.x;
-        const uint64_t t0 = globaltimer();
-        while ((int32_t)(ld_acquire_sys(f) - x.epoch) < 0) {
-            __nanosleep(32);
-            if ((int64_t)(globaltimer() - t0) > x.timeout_ns) { timed_out = 1; break; }
-        }
-        __threadfence();
-    }
-    __syncthreads();
-    if (timed_out) {
-        if (threadIdx.x == 0) atomicExch(reinterpret_cast<unsigned long long*>(status_of(x, x.rank) + ST_ERROR),
-                                         (unsigned long long)(int64_t)LMSGD_ERR_TIMEOUT);
-        return false;
-    }
-    return true;
-}
 
 // Grid-wide "done" ticket: returns true in exactly one thread (thread 0 of the last
 // block to finish), after all blocks' writes are fenced at system scope.
@@ -362,10 +339,6 @@ __device__ void publish(const XArgs& x, int which) {
     for (int p = 0; p < x.world; ++p) st_relaxed_sys(flag_slot(x, p, which) + x.rank, x.epoch);
 }
 
-// Grid-wide "done": the last block to finish publishes `which` = epoch to every rank.
-__device__ void grid_signal(const XArgs& x, int which) {
-    if (grid_last(x, which)) publish(x, which);
-}
 
 // One thread: wait until every rank has published `which` for this epoch (bounded
 // spin; on timeout record LMSGD_ERR_TIMEOUT in this rank's words and return false).
@@ -630,29 +603,44 @@ __global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
     stamp(x, TR_UPD_END);
 }
 
-// BN statistics: stage [mean | var] in this rank's buffer, publish.
-__global__ void k_bn_stage(XArgs x, const float* __restrict__ mean, const float* __restrict__ var, int64_t C) {
-    float* stage = reinterpret_cast<float*>(x.peers.base[x.rank] + x.lay.off_bn) +
-                   (int64_t)x.parity * 2 * LMSGD_MAX_BN_CHANNELS;
+// BN statistics without moving averages, one cooperative kernel
+// (all blocks co-resident): stage [mean | var] in this rank's exchange buffer, one
+// system fence per block, the last block releases flag C, every block acquires C of
+// all ranks, then averages its slice over the ranks' staging buffers in rank order,
+// in fp64, one rounding to fp32 (R16).  Double-buffered by call parity.
+__global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs x, float* __restrict__ mean,
+                                                           float* __restrict__ var, int64_t C) {
+    __shared__ int s_ok;
+    const int64_t Cp = (C + 3) & ~int64_t(3);   // var staged at a 16-B aligned offset
+    const int64_t off = (int64_t)x.parity * 2 * LMSGD_MAX_BN_CHANNELS;
+    float* stage = reinterpret_cast<float*>(x.peers.base[x.rank] + x.lay.off_bn) + off;
     for (int64_t i = gtid(); i < C; i += gstride()) {
         stage[i] = mean[i];
-        stage[C + i] = var[i];
+        stage[Cp + i] = var[i];
     }
-    grid_signal(x, FLAG_C);
-}
-
-// Average over ranks in rank order, fp64, one rounding to fp32 (R16).
-__global__ void k_bn_reduce(XArgs x, float* __restrict__ mean, float* __restrict__ var, int64_t C) {
-    if (!block_wait(x, FLAG_C)) return;
-    for (int64_t i = gtid(); i < 2 * C; i += gstride()) {
-        double acc = 0.0;
-        for (int p = 0; p < x.world; ++p) {
-            const float* stage = reinterpret_cast<const float*>(x.peers.base[p] + x.lay.off_bn) +
-                                 (int64_t)x.parity * 2 * LMSGD_MAX_BN_CHANNELS;
-            acc += (double)stage[i];
+    if (grid_last(x, FLAG_C)) publish(x, FLAG_C);
+    if (threadIdx.x == 0) s_ok = thread_wait_all(x, FLAG_C) ? 1 : 0;
+    __syncthreads();
+    if (!s_ok) return;
+    // one float4 of every rank per thread, all peer loads issued before the sums
+    for (int64_t f = gtid(); f < Cp / 2; f += gstride()) {
+        float4 v[LMSGD_MAX_WORLD];
+#pragma unroll
+        for (int p = 0; p < LMSGD_MAX_WORLD; ++p)
+            if (p < x.world)
+                v[p] = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x.peers.base[p] + x.lay.off_bn) + off)[f];
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+        for (int p = 0; p < LMSGD_MAX_WORLD; ++p)
+            if (p < x.world) { a0 += v[p].x; a1 += v[p].y; a2 += v[p].z; a3 += v[p].w; }
+        const double kk = (double)x.world;
+        const float o[4] = {(float)(a0 / kk), (float)(a1 / kk), (float)(a2 / kk), (float)(a3 / kk)};
+        const int64_t e0 = f * 4;
+        for (int e = 0; e < 4; ++e) {
+            const int64_t i = e0 + e;
+            if (i < C) mean[i] = o[e];
+            else if (i >= Cp && i - Cp < C) var[i - Cp] = o[e];
         }
-        const float out = (float)(acc / (double)x.world);
-        if (i < C) mean[i] = out; else var[i - C] = out;
     }
 }
 
@@ -769,19 +757,12 @@ cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* la
 
 
 
-cudaError_t launch_bn_stage(cudaStream_t s, const XArgs& x, const float* mean, const float* var,
-                            int64_t C) {
-    int grid = (int)((C + kThreads - 1) / kThreads);
-    grid = grid > 128 ? 128 : (grid < 1 ? 1 : grid);
-    k_bn_stage<<<grid, kThreads, 0, s>>>(x, mean, var, C);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_bn_reduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C) {
-    int grid = (int)((2 * C + kThreads - 1) / kThreads);
-    grid = grid > 128 ? 128 : (grid < 1 ? 1 : grid);
-    k_bn_reduce<<<grid, kThreads, 0, s>>>(x, mean, var, C);
-    return cudaGetLastError();
+cudaError_t launch_bn_allreduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C) {
+    int grid = (int)(((C + 3) / 4 * 2 + kThreads - 1) / kThreads);   // one float4 per thread
+    grid = grid > 148 ? 148 : (grid < 1 ? 1 : grid);
+    XArgs xa = x;
+    void* params[] = {&xa, &mean, &var, &C};
+    return cudaLaunchCooperativeKernel((const void*)k_bn_allreduce, dim3((unsigned)grid), dim3(kThreads), params, 0, s);
 }
 
 }  // namespace lmsgd

@@ -101,8 +101,6 @@ struct XStep {
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a);
 int xstep_blocks_per_sm();
 
-cudaError_t launch_bn_stage(cudaStream_t s, const XArgs& x, const float* mean, const float* var,
-                            int64_t C);
-cudaError_t launch_bn_reduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C);
+cudaError_t launch_bn_allreduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C);
 
 }  // namespace lmsgd
