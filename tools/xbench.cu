@@ -107,6 +107,29 @@ __global__ void __launch_bounds__(256) k_upd_pull2(Ptrs P, int world, int rank, 
     }
 }
 
+// P with a system fence after every unit (what per-chunk release needs), persistent
+__global__ void __launch_bounds__(256) k_push_fenced(const float* __restrict__ g, uint16_t* const* recv, int world,
+                                                     int rank, int64_t shard, int64_t n, int fence_every) {
+    const int64_t gsh = shard >> 3;
+    const int64_t ups = (gsh + 255) / 256;
+    int cnt = 0;
+    for (int64_t us = blockIdx.x; us < ups; us += gridDim.x) {
+        const int64_t gi = us * 256 + threadIdx.x;
+        if (gi < gsh) {
+            for (int q = 0; q < world; ++q) {
+                const int owner = (q + rank) % world;
+                const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+                float xv[8];
+                load8_g(g, j0, n, xv);
+                int64_t first = kNone; unsigned sat = 0;
+                *reinterpret_cast<uint4*>(recv[owner] + (int64_t)rank * shard + (gi << 3)) = pack8(xv, 1024.f, j0, first, sat);
+            }
+        }
+        if (fence_every && ++cnt % fence_every == 0) { __threadfence_system(); __syncthreads(); }
+    }
+    __threadfence_system();
+}
+
 // all-gather push: owner writes its R shard into every rank's full-R buffer (persistent)
 __global__ void __launch_bounds__(256) k_ag_push(const uint16_t* __restrict__ Rmine, uint16_t* const* full, int world,
                                                  int rank, int64_t shard) {
@@ -177,6 +200,27 @@ int main(int argc, char** argv) {
     run("update pull, launch_bounds(256,8)", 26.0 * n, [&](int i) { xb::k_upd_pull_lb<8><<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
     run("update pull, 2 units per block", 26.0 * n, [&](int i) { xb::k_upd_pull2<<<(W * ups + 1) / 2, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
     run("update local full R (k_update flat)", 26.0 * n, [&](int i) { launch_update(st[i], L, full[i], n, c, th[i], d[i], m[i], nullptr, nullptr, nullptr); });
+    {   // P with per-unit fences, alone and concurrently with the local update on a second stream
+        std::vector<uint16_t**> recvp(W);
+        for (int i = 0; i < W; ++i) { CKE(cudaSetDevice(i)); CKE(cudaMalloc(&recvp[i], 8 * sizeof(uint16_t*)));
+                                      CKE(cudaMemcpy(recvp[i], recv.data(), W * sizeof(uint16_t*), cudaMemcpyHostToDevice)); }
+        std::vector<cudaStream_t> st2(W);
+        for (int i = 0; i < W; ++i) { CKE(cudaSetDevice(i)); CKE(cudaStreamCreateWithFlags(&st2[i], cudaStreamNonBlocking)); }
+        const double pb = 2.0 * n_pad * (W - 1) / W;
+        run("P persistent 148x6, one fence/block", pb, [&](int i) { xb::k_push_fenced<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
+        run("P persistent 148x6, fence/unit", pb, [&](int i) { xb::k_push_fenced<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1); });
+        run("P persistent 148x2, fence/unit", pb, [&](int i) { xb::k_push_fenced<<<sms * 2, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1); });
+        run("P 148x2 fence/unit || local update (2 streams)", 26.0 * n, [&](int i) {
+            cudaEvent_t ev; cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            xb::k_push_fenced<<<sms * 2, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1);
+            launch_update(st2[i], L, full[i], n, c, th[i], d[i], m[i], nullptr, nullptr, nullptr);
+            cudaEventRecord(ev, st2[i]); cudaStreamWaitEvent(st[i], ev, 0); cudaEventDestroy(ev); });
+        run("P 148x2 fence/unit || pull update (2 streams)", 26.0 * n, [&](int i) {
+            cudaEvent_t ev; cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+            xb::k_push_fenced<<<sms * 2, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1);
+            xb::k_upd_pull<<<W * ups, 256, 0, st2[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]);
+            cudaEventRecord(ev, st2[i]); cudaStreamWaitEvent(st[i], ev, 0); cudaEventDestroy(ev); });
+    }
     run("AG push R shard to all (persistent 148x8)", 2.0 * shard * (W - 1), [&](int i) { xb::k_ag_push<<<sms * 8, 256, 0, st[i]>>>(R[i], fullp[i], W, i, shard); });
     run("AG push + local update", 26.0 * n, [&](int i) { xb::k_ag_push<<<sms * 8, 256, 0, st[i]>>>(R[i], fullp[i], W, i, shard);
                                                           launch_update(st[i], L, full[i], n, c, th[i], d[i], m[i], nullptr, nullptr, nullptr); });
