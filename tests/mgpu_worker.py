@@ -126,6 +126,43 @@ def main():
         assert np.array_equal(H(mean), om) and np.array_equal(H(var), ov), "BN average not bit-exact"
     L.lmsgd_finalize(ctx)
 
+    # ---- BN without moving averages end to end: momentum = 1 BN
+    #      layers, a different minibatch per rank, then the average before validation
+    from paper_1711_04325_b200 import bn_sync
+    torch.manual_seed(5)   # identical weights on every rank
+    net = torch.nn.Sequential(torch.nn.Conv2d(3, 16, 3), torch.nn.BatchNorm2d(16), torch.nn.ReLU(),
+                              torch.nn.Conv2d(16, 32, 3), torch.nn.BatchNorm2d(32), torch.nn.ReLU(),
+                              torch.nn.Flatten(), torch.nn.LazyLinear(10), torch.nn.BatchNorm1d(10)).to(dev)
+    bn_sync.last_minibatch_bn(net)
+    ctx = L.lmsgd_init(world, rank, local, 1000, S)
+    L.connect_process_group(ctx)
+    net.train()
+    net(torch.randn(32, 3, 12, 12, device=dev))          # materialise the lazy layer
+    sync = bn_sync.BNStatsSync(net, ctx)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(100 + rank)
+    xb = torch.randn(32, 3, 12, 12, device=dev, generator=gen) * (1 + rank)
+    net(xb)                                              # last training minibatch of this rank
+    layers = bn_sync.bn_layers(net)
+    mine_mean = torch.cat([m.running_mean for m in layers]).clone()
+    mine_var = torch.cat([m.running_var for m in layers]).clone()
+    # momentum = 1: running statistics are exactly this minibatch's (first BN layer)
+    h = net[0](xb)
+    assert torch.allclose(layers[0].running_mean, h.mean(dim=(0, 2, 3)), rtol=1e-5, atol=1e-6)
+    all_mean = [torch.empty_like(mine_mean) for _ in range(world)]
+    all_var = [torch.empty_like(mine_var) for _ in range(world)]
+    dist.all_gather(all_mean, mine_mean)
+    dist.all_gather(all_var, mine_var)
+    sync.sync()
+    torch.cuda.synchronize()
+    om, ov = bn.sync_statistics(np.stack([H(t) for t in all_mean]), np.stack([H(t) for t in all_var]))
+    assert np.array_equal(H(sync.mean), om) and np.array_equal(H(sync.var), ov)
+    assert np.array_equal(H(layers[1].running_var), ov[16:48])      # the modules see the averages
+    net.eval()
+    net(torch.randn(4, 3, 12, 12, device=dev))           # validation uses the synced statistics
+    replicas_identical(sync.mean, sync.var)
+    L.lmsgd_finalize(ctx)
+
     # ---- longer run: random schedule steps, replica bit-identity every step,
     #      resync parity every 10th step
     n = 333_331

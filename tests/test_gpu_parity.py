@@ -394,3 +394,26 @@ def test_goyal_schedule_through_ctx():
         check_state(host(th), host(d), host(m), *prev, exchange.exchange(list(g), 1024.0).ghat,
                     schedule.coeffs_at(t, schedule.Hyper(), cl_o))
     L.lmsgd_finalize(ctx)
+
+
+def test_bn_sync_world1_is_last_minibatch():
+    """f2 at world 1: momentum-1 BN keeps the last minibatch's statistics; the sync is
+    the identity (the average of one worker)."""
+    from paper_1711_04325_b200 import bn_sync
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Conv2d(3, 8, 3), torch.nn.BatchNorm2d(8)).to(DEV)
+    bn_sync.last_minibatch_bn(net)
+    ctx = L.lmsgd_init(1, 0, 0, 100, 1.0)
+    sync = bn_sync.BNStatsSync(net, ctx)
+    net.train()
+    for _ in range(3):
+        xb = torch.randn(16, 3, 10, 10, device=DEV)
+        net(xb)
+    h = net[0](xb)
+    before = sync.mean.clone()
+    sync.sync()
+    torch.cuda.synchronize()
+    assert torch.equal(sync.mean, before)
+    assert torch.allclose(net[1].running_mean, h.mean(dim=(0, 2, 3)), rtol=1e-5, atol=1e-6)
+    assert torch.allclose(net[1].running_var, h.var(dim=(0, 2, 3), unbiased=True), rtol=1e-4, atol=1e-6)
+    L.lmsgd_finalize(ctx)
