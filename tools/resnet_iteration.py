@@ -1,0 +1,113 @@
+#!/usr/bin/env python
+"""Whole synchronous-SGD iterations of ResNet-50 on synthetic ImageNet-shaped data
+(the shape of PAPER.md Fig. 1 and the scaling efficiency of
+PAPER.md:113-118), with the lmsgd exchange + blended update as the optimizer.
+
+    python tools/resnet_iteration.py [--iters 30] [--warmup 5]
+    torchrun --nproc-per-node 4 --master-addr 127.0.0.1 tools/resnet_iteration.py
+
+Per rank: minibatch 32 of 3x224x224 synthetic images, torchvision
+ResNet-50 with random init, fp32 compute (cuDNN may use TF32),
+BatchNorm with momentum 1.  The parameters and gradients are views
+of two flat fp32 buffers, so lmsgd_step consumes the gradient in place (row a1).
+Prints one JSON line on rank 0: iteration time, the exchange + update share
+(the "communication time" of Fig. 1), images/s.  Forward/backward are cuDNN
+(library code); the path under test is the lmsgd step.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+import torchvision  # noqa: E402
+
+import paper_1711_04325_b200 as L  # noqa: E402
+from paper_1711_04325_b200 import bn_sync  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--iters", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=32)
+    args = ap.parse_args()
+    rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
+        int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    torch.manual_seed(0)
+    model = torchvision.models.resnet50().to(dev)
+    bn_sync.last_minibatch_bn(model)
+    params = [p for p in model.parameters()]
+    n = sum(p.numel() for p in params)
+    flat_p = torch.empty(n, device=dev)
+    flat_g = torch.zeros(n, device=dev)
+    off = 0
+    for p in params:   # parameters and gradients become views of the flat buffers
+        k = p.numel()
+        flat_p[off:off + k].copy_(p.data.reshape(-1))
+        p.data = flat_p[off:off + k].view_as(p)
+        p.grad = flat_g[off:off + k].view_as(p)
+        off += k
+    delta = torch.zeros(n, device=dev)
+    m = torch.zeros(n, device=dev)
+    ctx = L.lmsgd_init(world, rank, local, n, 1024.0)
+    L.connect_process_group(ctx)
+    sync = bn_sync.BNStatsSync(model, ctx)
+    cl = L.make_cluster(1024, args.batch)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1711 + rank)
+    x = torch.randn(args.batch, 3, 224, 224, device=dev, generator=gen)
+    y = torch.randint(0, 1000, (args.batch,), device=dev, generator=gen)
+    crit = torch.nn.CrossEntropyLoss()
+    stream = torch.cuda.current_stream()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    fb_ms, st_ms, it_ms = [], [], []
+    model.train()
+    for it in range(args.warmup + args.iters):
+        t = it + 1
+        flat_g.zero_()
+        ev[0].record(stream)
+        loss = crit(model(x), y) * 1.0
+        loss.backward()
+        ev[1].record(stream)
+        L.lmsgd_step(ctx, flat_p, flat_g, delta, m, L.lmsgd_schedule_at(None, cl, t))
+        ev[2].record(stream)
+        torch.cuda.synchronize()
+        if it == 0:   # autograd accumulated in place: the gradients are still views of flat_g
+            base = flat_g.data_ptr()
+            assert all(base <= p.grad.data_ptr() < base + 4 * n for p in params), "grad left the flat buffer"
+        if it >= args.warmup:
+            fb_ms.append(ev[0].elapsed_time(ev[1]))
+            st_ms.append(ev[1].elapsed_time(ev[2]))
+            it_ms.append(ev[0].elapsed_time(ev[2]))
+    code, st = L.lmsgd_query_status(ctx)
+    sync.sync()                       # BN statistics average before "validation"
+    torch.cuda.synchronize()
+    med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
+    res = {"fwd_bwd_ms": med(fb_ms), "exchange_update_ms": med(st_ms), "iteration_ms": med(it_ms)}
+    if world > 1:
+        allr = [None] * world
+        dist.all_gather_object(allr, res)
+        res = {k: max(r[k] for r in allr) for k in res}
+    if rank == 0:
+        out = {"what": "ResNet-50 synchronous SGD iteration, synthetic data, lmsgd exchange + update",
+               "n_gpus": world, "batch_per_gpu": args.batch, "params": n, "iters": args.iters, **res,
+               "exchange_share": res["exchange_update_ms"] / res["iteration_ms"],
+               "images_per_s": world * args.batch / (res["iteration_ms"] * 1e-3),
+               "last_status": code, "loss": float(loss)}
+        print(json.dumps(out), flush=True)
+    L.lmsgd_finalize(ctx)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
