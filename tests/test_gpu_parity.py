@@ -323,20 +323,22 @@ def test_fused_step1_matches_pack_update():
 
 # ------------------------------------------------------------------ full size (BASELINE configs)
 
-@pytest.mark.parametrize("t", [1, 392, 1000])
-def test_resnet50_full_size_sampled(t):
-    """C2: the 25,557,032-element ResNet-50 buffer, k = 1, in the launch configuration
-    bench.py times; outputs compared on a sample of indices (the path is elementwise,
-    so the oracle on the sampled indices is exact)."""
-    n = synth.resnet_n_params(50)
+@pytest.mark.parametrize("depth,t,flags", [(50, 1, 0), (50, 392, 0), (50, 1000, 0), (152, 1, 0), (152, 3519, 0),
+                                          (50, 1, L.LMSGD_FLAG_NO_SKIP), (152, 2, L.LMSGD_FLAG_NO_SKIP)])
+def test_resnet_full_size_sampled(depth, t, flags):
+    """C2 / C5 sizes: the 25,557,032-element ResNet-50 and 60,192,808-element
+    ResNet-152 buffers, k = 1, in the launch configuration bench.py times; outputs
+    compared on a sample of indices (the path is elementwise, so the oracle on the
+    sampled indices is exact)."""
+    n = synth.resnet_n_params(depth)
     s = 1024.0
     r = np.random.default_rng(t)
     idx = np.unique(np.concatenate([np.arange(1000), np.arange(n - 1000, n), r.integers(0, n, 200_000)]))
-    th0 = synth.theta0(n, 50)
+    th0 = synth.theta0(n, depth)
     d0 = (r.standard_normal(n) * 1e-3).astype(np.float32)
     m0 = (r.random(n) * 1e-6).astype(np.float32)
     g = synth.grads(1, t, n)
-    ctx = L.lmsgd_init(1, 0, 0, n, s)
+    ctx = L.lmsgd_init(1, 0, 0, n, s, None, flags)
     th, d, m = dev(th0), dev(d0), dev(m0)
     L.lmsgd_step(ctx, th, dev(g[0]), d, m, L.lmsgd_schedule_at(None, K32_C, t))
     code, st = L.lmsgd_query_status(ctx)

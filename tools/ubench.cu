@@ -180,7 +180,7 @@ static float time_it(int iters, const std::function<void()>& f) {
 
 int main(int argc, char** argv) {
     const int64_t n = argc > 1 ? atoll(argv[1]) : 25557032;
-    const int iters = 200;
+    const int iters = getenv("UBENCH_ITERS") ? atoi(getenv("UBENCH_ITERS")) : 200;
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     const int64_t n_pad = (n + 63) / 64 * 64;
     std::vector<float> hg(n), ht(n), hd(n), hm(n);
