@@ -473,6 +473,32 @@ def main():
     e2e = {"value": world * 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 4 * n,
            "d2h_bytes_per_step": ctypes.sizeof(L.StepStatus), "ms_per_step": e2e_ms, "steps": ke}
 
+    # N = 1 guarded default: also time the single-pass fused variant (LMSGD_FLAG_NO_SKIP,
+    # BASELINE.json configs[1] "fused fp16-pack + blended update"; 28 vs 32 B/elem)
+    variants = None
+    if world == 1 and not flags and not args.no_profile:
+        ctxf = L.lmsgd_init(1, 0, local, n, LOSS_SCALE, None, L.LMSGD_FLAG_NO_SKIP)
+        thf, df, mf = theta.clone(), delta.clone(), m.clone()
+        pf = (P(thf.data_ptr()), P(grads.data_ptr()), P(df.data_ptr()), P(mf.data_ptr()))
+        for i in range(args.warmup):
+            lib.lmsgd_step(ctxf.ptr, sp, *pf, ctypes.byref(coeffs[i]))
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(args.steps):
+            lib.lmsgd_step(ctxf.ptr, sp, *pf, ctypes.byref(coeffs[args.warmup + i]))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        fms = e0.elapsed_time(e1) / args.steps
+        codef, _ = L.lmsgd_query_status(ctxf)
+        assert codef == 0
+        variants = {"fused_no_skip": {"ms_per_step": fms, "value": 1e3 / fms, "unit": UNIT,
+                                      "hbm_gbs_algorithmic": FUSED_BYTES_PER_ELEM * n / (fms * 1e-3) / 1e9,
+                                      "frac_of_measured_hbm": FUSED_BYTES_PER_ELEM * n / (fms * 1e-3) / 1e9 / peak,
+                                      "note": "single pass (pack+update, 28 B/elem); non-finite gradients are "
+                                              "reported but not skipped"}}
+        L.lmsgd_finalize(ctxf)
+        del thf, df, mf
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, ns, calls, el = oracle_rate(1, n, 15.0)
@@ -495,6 +521,7 @@ def main():
                        "global_steps_per_s": global_steps_per_s,
                        "grad_elems_per_s": global_steps_per_s * world * n},
             "roofline": roofline, "phases": phases, "nvlink": nvlink, "bn_stats_allreduce": bn,
+            "variants": variants,
             "cpu_baseline": cpu, "e2e": e2e,
             "clocks": ck, "gpu_launches": kernels_per_step * args.steps,
             "profile_pass_ms_per_step": (ms_prof / args.steps) if ms_prof else None,
