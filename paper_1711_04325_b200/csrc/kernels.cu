@@ -410,7 +410,7 @@ __device__ __forceinline__ bool spin_flag(const XArgs& x, const uint32_t* f) {
 // k_xfinalize -- one warp: the step's public status record.
 // Chunk counters in a.ctr are reset by the block that completes them.
 __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");   // let k_xupdate queue up
+    pdl_enter();   // wait for the previous step / caller work; let k_xupdate queue up
     const XArgs& x = a.x;
     __shared__ int s_ok;
     const bool t0 = threadIdx.x == 0;
@@ -686,8 +686,23 @@ int xstep_blocks_per_sm() {
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
     XStep arg = a;
     void* params[] = {&arg};
-    cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_xstep1, dim3((unsigned)L.grid_xstep), dim3(kThreads),
-                                                params, 0, s);
+    cudaError_t e;
+    if (L.pdl_mask & 2) {   // cooperative + programmatic dependent launch (hides the launch latency)
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)L.grid_xstep);
+        cfg.blockDim = dim3(kThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+        attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        e = cudaLaunchKernelEx(&cfg, k_xstep1, arg);
+    } else {
+        e = cudaLaunchCooperativeKernel((const void*)k_xstep1, dim3((unsigned)L.grid_xstep), dim3(kThreads), params, 0, s);
+    }
     if (e != cudaSuccess) return e;
     const int64_t gsh = a.x.lay.shard >> 3;
     (void)gsh;

@@ -50,7 +50,8 @@ struct Launch {
     int sm_count;
     int grid_cap_stream;   // SMs x resident blocks of the streaming kernels (informational)
     int grid_xstep;        // SMs x resident blocks of k_xstep (cooperative, all co-resident)
-    int pdl_mask;          // programmatic dependent launch: bit 1 = the k = 1 kernels
+    int pdl_mask;          // programmatic dependent launch: bit 1 = the k = 1 kernels,
+                           // bit 2 = k_xstep1 (cooperative + PDL)
 };
 
 // ---- single-GPU building blocks (sub-step ABI and world == 1)

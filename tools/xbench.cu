@@ -130,6 +130,45 @@ __global__ void __launch_bounds__(256) k_push_fenced(const float* __restrict__ g
     __threadfence_system();
 }
 
+// P with 16 elements per thread (two 16-B stores per owner per thread)
+__global__ void __launch_bounds__(256) k_push16(const float* __restrict__ g, uint16_t* const* recv, int world,
+                                                int rank, int64_t shard, int64_t n) {
+    const int64_t gsh = shard >> 3;
+    const int64_t g2 = (gsh + 1) / 2;                 // pairs of groups
+    const int64_t ups = (g2 + 255) / 256;
+    for (int64_t us = blockIdx.x; us < ups; us += gridDim.x) {
+        const int64_t pi = us * 256 + threadIdx.x;
+        if (pi * 2 + 1 < gsh) {
+            for (int q = 0; q < world; ++q) {
+                const int owner = (q + rank) % world;
+                const int64_t j0 = ((int64_t)owner * gsh + pi * 2) << 3;
+                float xa[8], xb[8];
+                load8_g(g, j0, n, xa);
+                load8_g(g, j0 + 8, n, xb);
+                int64_t first = kNone; unsigned sat = 0;
+                uint4* dst = reinterpret_cast<uint4*>(recv[owner] + (int64_t)rank * shard + (pi * 2 << 3));
+                dst[0] = pack8(xa, 1024.f, j0, first, sat);
+                dst[1] = pack8(xb, 1024.f, j0 + 8, first, sat);
+            }
+        }
+    }
+    __threadfence_system();
+}
+
+// update pull with the R load on the non-coherent read-only path
+__global__ void __launch_bounds__(256) k_upd_pull_nc(Ptrs P, int world, int rank, int64_t shard, int64_t n, UpdConst c,
+                                                     float* __restrict__ th, float* __restrict__ d, float* __restrict__ m) {
+    const int64_t gsh = shard >> 3;
+    const int64_t u = blockIdx.x;
+    const int owner = (int)((u % world + rank) % world);
+    const int64_t gi = (u / world) * 256 + threadIdx.x;
+    if (gi >= gsh) return;
+    const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+    if (j0 >= n) return;
+    const uint4 r = __ldg(reinterpret_cast<const uint4*>(P.R[owner] + (gi << 3)));
+    update8<true>(r, j0, n, c, th, d, m);
+}
+
 // all-gather push: owner writes its R shard into every rank's full-R buffer (persistent)
 __global__ void __launch_bounds__(256) k_ag_push(const uint16_t* __restrict__ Rmine, uint16_t* const* full, int world,
                                                  int rank, int64_t shard) {
@@ -208,6 +247,10 @@ int main(int argc, char** argv) {
         for (int i = 0; i < W; ++i) { CKE(cudaSetDevice(i)); CKE(cudaStreamCreateWithFlags(&st2[i], cudaStreamNonBlocking)); }
         const double pb = 2.0 * n_pad * (W - 1) / W;
         run("P persistent 148x6, one fence/block", pb, [&](int i) { xb::k_push_fenced<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
+        run("P persistent 148x6, 16 elem/thread", pb, [&](int i) { xb::k_push16<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n); });
+        run("P persistent 148x8, one fence/block", pb, [&](int i) { xb::k_push_fenced<<<sms * 8, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
+        run("P persistent 148x4, one fence/block", pb, [&](int i) { xb::k_push_fenced<<<sms * 4, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
+        run("update pull, R via ld.global.nc", 26.0 * n, [&](int i) { xb::k_upd_pull_nc<<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
         run("P persistent 148x6, fence/unit", pb, [&](int i) { xb::k_push_fenced<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1); });
         run("P persistent 148x2, fence/unit", pb, [&](int i) { xb::k_push_fenced<<<sms * 2, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1); });
         run("P 148x2 fence/unit || local update (2 streams)", 26.0 * n, [&](int i) {
