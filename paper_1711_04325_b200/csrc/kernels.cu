@@ -6,11 +6,12 @@
 // data touched once (g, theta, Delta, m), and keep the fp16 wire buffers on the
 // default policy so a consumer launched right after the producer hits L2.
 //
-// Cross-GPU ordering (world > 1) uses flags in each rank's CUDA-IPC exchange
-// buffer: the last block of a producer kernel (ticket counter) issues a
-// system-scope fence and st.release.sys of the step's epoch into every peer's
-// flag slot; consumer blocks spin with ld.acquire.sys (bounded by a
-// %globaltimer timeout) before touching peer data.
+// Cross-GPU ordering (world > 1) uses epoch-valued flags in each rank's CUDA-IPC
+// exchange buffer: a producer (the last block of a phase, found with a ticket
+// counter, or the block completing a chunk) issues one system-scope fence and then
+// relaxed system-scope stores of the step's epoch into every rank's flag slot;
+// consumers spin with ld.acquire.sys, bounded by a %globaltimer timeout that turns a
+// missing rank into LMSGD_ERR_TIMEOUT instead of a hang.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -24,8 +25,8 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kXUnits = 1;   // k_xupdate: 2048-element units per block
-enum { FLAG_A = 0, FLAG_B = 1, FLAG_C = 2, FLAG_D = 3 };  // pack done, reduce done, BN staged,
-                                                         // local: this step's decision stored
+enum { FLAG_A = 0, FLAG_C = 2, FLAG_D = 3 };  // A: a rank's pack+push is done; C: BN staged;
+                                             // D (local): this step's skip decision is stored
 
 // ------------------------------------------------------------------ helpers
 
