@@ -59,7 +59,7 @@ typedef enum {
     LMSGD_ERR_STATE = -5,         /* call out of order (e.g. step before connect)          */
     LMSGD_ERR_UNSUPPORTED = -6,   /* e.g. world > LMSGD_MAX_WORLD, no peer access          */
     LMSGD_ERR_TIMEOUT = -7,       /* a cross-GPU wait exceeded the timeout; step skipped   */
-    LMSGD_ERR_RANGE = -8          /* schedule asked past its last epoch                    */
+    LMSGD_ERR_RANGE = -8          /* schedule asked past its last epoch / table exhausted  */
 } lmsgd_status;
 
 /* Hyperparameters, PAPER.md:167 (mu1, mu2, eps), PAPER.md:190 (beta_center,
@@ -178,6 +178,28 @@ lmsgd_status lmsgd_step(lmsgd_ctx* ctx, void* stream, float* params, const float
 lmsgd_status lmsgd_step_host(lmsgd_ctx* ctx, void* stream, float* params, const float* grads_host,
                              float* delta, float* m, const lmsgd_coeffs* coeffs,
                              lmsgd_step_status* status_host);
+
+/* ---------------------------------------------------------------- CUDA graphs
+ * lmsgd_step bakes its per-step arguments (coefficients, step number) into the
+ * launches, so a captured lmsgd_step would replay the same step.  The graph entry
+ * point keeps everything that changes between steps in device memory instead: */
+
+/* Upload the coefficients of iterations t_first .. t_first + count - 1
+ * (lmsgd_schedule_at, hyper may be NULL) to a device table and point the device
+ * cursor at its first entry.  Synchronous.  Errors: INVALID_ARG, RANGE (a step past
+ * the schedule), CUDA. */
+lmsgd_status lmsgd_schedule_upload(lmsgd_ctx* ctx, const lmsgd_hyper* hyper, const lmsgd_cluster* cluster,
+                                   int64_t t_first, int64_t count);
+
+/* One iteration like lmsgd_step, with the coefficients taken from the uploaded table at
+ * the device cursor and the step number from a device counter; both advance on the
+ * device at the end of the step.  Safe to capture in a CUDA graph (e.g.
+ * torch.cuda.graph): every replay runs the next iteration.  Past the end of the table
+ * the update is skipped and the status reports LMSGD_ERR_RANGE.  At world == 1 a
+ * context uses either lmsgd_step or lmsgd_step_graph (LMSGD_ERR_STATE otherwise);
+ * at world > 1 the two may be mixed. */
+lmsgd_status lmsgd_step_graph(lmsgd_ctx* ctx, void* stream, float* params, const float* grads,
+                              float* delta, float* m);
 
 /* BN statistics without moving averages (R16): on every rank,
  *   mean[c] <- fp32( (sum_{r=0..k-1} mean_r[c]) / k ),  var likewise,

@@ -29,6 +29,12 @@ struct lmsgd_ctx {
     bool connected = false;
     unsigned int* tickets = nullptr;  // device [4]
     unsigned int* xctr = nullptr;     // device [4 + nchunks] counters of the world > 1 kernels
+    // device-resident step state (so a captured step replays as the next step)
+    struct DevState { uint32_t xepoch, bnepoch, k1epoch, pad; int64_t cursor; };
+    DevState* dstate = nullptr;       // device
+    lmsgd::UpdConst* d_ctab = nullptr;   // lmsgd_schedule_upload table
+    int64_t ctab_count = 0, ctab_cap = 0;
+    int mode1 = 0;                    // world == 1: 0 unused, 1 lmsgd_step, 2 lmsgd_step_graph
     int64_t* last = nullptr;          // device lmsgd_step_status of the last step
     float* d_grads = nullptr;         // device staging for lmsgd_step_host (lazy)
     uint32_t step = 0, bn_calls = 0;
@@ -149,7 +155,7 @@ int64_t* status_slot(lmsgd_ctx* c, int parity) {
     return reinterpret_cast<int64_t*>(c->buf + c->lay.off_status) + parity * lmsgd::ST_WORDS;
 }
 
-lmsgd::XArgs xargs(lmsgd_ctx* c, uint32_t epoch) {
+lmsgd::XArgs xargs(lmsgd_ctx* c, uint32_t epoch, uint32_t* dev_epoch) {
     lmsgd::XArgs x{};
     x.peers = c->peers;
     x.lay = c->lay;
@@ -160,6 +166,7 @@ lmsgd::XArgs xargs(lmsgd_ctx* c, uint32_t epoch) {
     x.n = c->n;
     x.timeout_ns = c->timeout_ns;
     x.ticket = c->tickets;
+    x.dev_epoch = dev_epoch;
     x.trace = nullptr;
     if (c->d_trace) {
         x.trace = c->d_trace + (c->trace_steps % c->trace_cap) * lmsgd::TR_WORDS;
@@ -272,6 +279,8 @@ lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_
     }
     if ((e = cudaMalloc(&c->tickets, 4 * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMemset(c->tickets, 0, 4 * sizeof(unsigned int))) != cudaSuccess ||
+        (e = cudaMalloc(&c->dstate, sizeof(lmsgd_ctx::DevState))) != cudaSuccess ||
+        (e = cudaMemset(c->dstate, 0, sizeof(lmsgd_ctx::DevState))) != cudaSuccess ||
         (e = cudaMalloc(&c->xctr, (4 + c->lay.nchunks) * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMemset(c->xctr, 0, (4 + c->lay.nchunks) * sizeof(unsigned int))) != cudaSuccess ||
         (e = cudaMalloc(&c->last, sizeof(lmsgd_step_status))) != cudaSuccess ||
@@ -326,6 +335,8 @@ lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
         if (c->buf) cudaFree(c->buf);
         if (c->tickets) cudaFree(c->tickets);
         if (c->xctr) cudaFree(c->xctr);
+        if (c->dstate) cudaFree(c->dstate);
+        if (c->d_ctab) cudaFree(c->d_ctab);
         if (c->last) cudaFree(c->last);
         if (c->d_grads) cudaFree(c->d_grads);
         if (c->d_trace) cudaFree(c->d_trace);
@@ -344,6 +355,8 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     if (!coeffs_ok(coeffs))
         return fail(c, LMSGD_ERR_INVALID_ARG, "coeffs: need eta > 0, 0 <= alpha_sgd <= 1, alpha_rmsprop >= 0");
     if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
+    if (c->world == 1 && c->mode1 == 2)
+        return fail(c, LMSGD_ERR_STATE, "world == 1 context already runs lmsgd_step_graph");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const UpdConst u = make_const(c->hyper, *coeffs, c->world, c->scale);
@@ -351,6 +364,7 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     const int parity = static_cast<int>(epoch & 1u);
     c->last_stream = s;
     if (c->world == 1) {
+        c->mode1 = 1;
         uint16_t* h = reinterpret_cast<uint16_t*>(c->buf + c->lay.off_recv);
         if (c->flags & LMSGD_FLAG_NO_SKIP) {
             CK(c, timed(c, s, 0, [&] {
@@ -369,9 +383,73 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
         }
         return LMSGD_OK;
     }
-    const lmsgd::XArgs x = xargs(c, epoch);
-    lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr};
+    const lmsgd::XArgs x = xargs(c, epoch, &c->dstate->xepoch);
+    lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, nullptr, 0, nullptr};
     CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, c->L, a); }));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_schedule_upload(lmsgd_ctx* c, const lmsgd_hyper* hyper, const lmsgd_cluster* cluster,
+                                   int64_t t_first, int64_t count) {
+    if (!c || !cluster || t_first < 1 || count < 1 || count > (int64_t(1) << 24))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "schedule_upload: bad argument");
+    lmsgd_hyper h{};
+    if (hyper) h = *hyper; else lmsgd_hyper_default(&h);
+    std::vector<UpdConst> tab(static_cast<size_t>(count));
+    for (int64_t i = 0; i < count; ++i) {
+        lmsgd_coeffs co{};
+        const lmsgd_status st = lmsgd_schedule_at(&h, cluster, t_first + i, &co);
+        if (st != LMSGD_OK) return fail(c, st, "schedule_upload: step " + std::to_string(t_first + i) + " is out of range");
+        tab[static_cast<size_t>(i)] = make_const(c->hyper, co, c->world, c->scale);
+    }
+    DeviceGuard g(c->device);
+    CK(c, cudaDeviceSynchronize());
+    if (count > c->ctab_cap) {
+        if (c->d_ctab) cudaFree(c->d_ctab);
+        c->d_ctab = nullptr;
+        CK(c, cudaMalloc(&c->d_ctab, count * sizeof(UpdConst)));
+        c->ctab_cap = count;
+    }
+    CK(c, cudaMemcpy(c->d_ctab, tab.data(), count * sizeof(UpdConst), cudaMemcpyHostToDevice));
+    CK(c, cudaMemset(&c->dstate->cursor, 0, sizeof(int64_t)));
+    c->ctab_count = count;
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const float* grads, float* delta,
+                              float* m) {
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (!aligned16(params) || !aligned16(grads) || !aligned16(delta) || !aligned16(m))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "params/grads/delta/m must be non-NULL and 16-byte aligned");
+    if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
+    if (c->ctab_count == 0) return fail(c, LMSGD_ERR_STATE, "lmsgd_schedule_upload has not been called");
+    if (c->world == 1 && c->mode1 == 1)
+        return fail(c, LMSGD_ERR_STATE, "world == 1 context already runs lmsgd_step");
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const UpdConst u{};   // every coefficient comes from the device table
+    c->last_stream = s;
+    ++c->step;            // host-side count only (the kernels use the device counter)
+    if (c->world == 1) {
+        c->mode1 = 2;
+        lmsgd::Dev1 dv{&c->dstate->k1epoch, status_slot(c, 0), c->d_ctab, c->ctab_count, &c->dstate->cursor};
+        uint16_t* h = reinterpret_cast<uint16_t*>(c->buf + c->lay.off_recv);
+        if (c->flags & LMSGD_FLAG_NO_SKIP) {
+            CK(c, lmsgd::launch_fused1(s, c->L, grads, c->n, c->scale, u, params, delta, m, nullptr, nullptr,
+                                       nullptr, dv));
+            CK(c, lmsgd::launch_advance1(s, dv, c->last, true));
+        } else {
+            CK(c, lmsgd::launch_pack(s, c->L, grads, c->n, c->n_pad, c->scale, h, nullptr, dv));
+            CK(c, lmsgd::launch_update(s, c->L, h, c->n, u, params, delta, m, nullptr, nullptr, c->last, dv));
+            CK(c, lmsgd::launch_advance1(s, dv, c->last, false));
+        }
+        return LMSGD_OK;
+    }
+    lmsgd::XArgs x = xargs(c, 0, &c->dstate->xepoch);
+    if (x.trace) { x.trace = nullptr; --c->trace_steps; }   // the trace ring slot would be frozen in a graph
+    lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, c->d_ctab, c->ctab_count,
+                   &c->dstate->cursor};
+    CK(c, lmsgd::launch_xstep(s, c->L, a));
     return LMSGD_OK;
 }
 
@@ -408,7 +486,7 @@ lmsgd_status lmsgd_bn_stats_allreduce(lmsgd_ctx* c, void* stream, float* mean, f
     if (c->world == 1) return LMSGD_OK;  // the average of one worker is itself
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    lmsgd::XArgs x = xargs(c, ++c->bn_calls);
+    lmsgd::XArgs x = xargs(c, ++c->bn_calls, &c->dstate->bnepoch);
     if (x.trace) { x.trace = nullptr; --c->trace_steps; }
     CK(c, lmsgd::launch_bn_allreduce(s, x, mean, var, C));
     return LMSGD_OK;

@@ -208,10 +208,16 @@ __global__ void k_status_reset(int64_t* st, int words) {
     if ((int)threadIdx.x < words) reset_words(st);
 }
 
+// graph mode: this step's status slot pair from the device step counter
+__device__ __forceinline__ int dev_parity(const Dev1& dv) {
+    return (int)((*reinterpret_cast<volatile const uint32_t*>(dv.epoch) + 1u) & 1u);
+}
+
 __global__ void __launch_bounds__(kThreads) k_pack(const float* __restrict__ g, int64_t n,
                                                    int64_t n_pad, float s, uint16_t* __restrict__ h,
-                                                   int64_t* st) {
+                                                   int64_t* st, Dev1 dv) {
     pdl_enter();
+    if (dv.epoch) st = dv.st_base + dev_parity(dv) * ST_WORDS;
     int64_t first = kNone;
     unsigned sat = 0;
     const int64_t nv = n_pad >> 3;
@@ -253,10 +259,21 @@ template <bool RMS>
 __global__ void __launch_bounds__(kThreads) k_update(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
                                                      float* __restrict__ th, float* __restrict__ d,
                                                      float* __restrict__ m, const int64_t* st,
-                                                     int64_t* st_reset, int64_t* last) {
+                                                     int64_t* st_reset, int64_t* last, Dev1 dv) {
     pdl_enter();
     int64_t first = kNone, psat = 0, ssat = 0, err = 0;
-    if (st) { first = st[ST_FIRST]; psat = st[ST_PACK_SAT]; ssat = st[ST_SUM_SAT]; err = st[ST_ERROR]; }
+    if (dv.epoch) {   // graph mode: slots from the device counter, coefficients from the table
+        const int par = dev_parity(dv);
+        st = dv.st_base + par * ST_WORDS;
+        st_reset = dv.st_base + (par ^ 1) * ST_WORDS;
+        const int64_t idx = *reinterpret_cast<volatile const int64_t*>(dv.cursor);
+        if (idx >= dv.count) err = (int64_t)LMSGD_ERR_RANGE;
+        else c = dv.ctab[idx];
+    }
+    if (st) {
+        first = st[ST_FIRST]; psat = st[ST_PACK_SAT]; ssat = st[ST_SUM_SAT];
+        err = err ? err : st[ST_ERROR];
+    }
     const bool skip = first != kNone || err != 0;
     write_last(last, first, psat, ssat, err, skip);
     reset_status(st_reset);
@@ -275,8 +292,16 @@ template <bool RMS>
 __global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g, int64_t n, float s,
                                                      UpdConst c, float* __restrict__ th,
                                                      float* __restrict__ d, float* __restrict__ m,
-                                                     int64_t* st, int64_t* st_reset) {
+                                                     int64_t* st, int64_t* st_reset, Dev1 dv) {
     pdl_enter();
+    if (dv.epoch) {   // graph mode (see k_update)
+        const int par = dev_parity(dv);
+        st = dv.st_base + par * ST_WORDS;
+        st_reset = dv.st_base + (par ^ 1) * ST_WORDS;
+        const int64_t idx = *reinterpret_cast<volatile const int64_t*>(dv.cursor);
+        if (idx >= dv.count) return;   // table exhausted: k_advance1 reports LMSGD_ERR_RANGE
+        c = dv.ctab[idx];
+    }
     reset_status(st_reset);
     int64_t first = kNone;
     unsigned sat = 0;
@@ -298,7 +323,36 @@ __global__ void k_finalize_fused(const int64_t* st, int64_t* last) {
     if (threadIdx.x == 0) store_last(last, st[ST_FIRST], st[ST_PACK_SAT], st[ST_SUM_SAT], st[ST_ERROR], 0);
 }
 
+// Graph mode, k = 1: after the step's kernels, publish the fused step's status and
+// advance the device step counter and coefficient cursor (one warp).
+__global__ void k_advance1(Dev1 dv, int64_t* last, int fused) {
+    pdl_enter();
+    if (threadIdx.x != 0) return;
+    const uint32_t e = *dv.epoch + 1u;
+    const int64_t* st = dv.st_base + (int)(e & 1u) * ST_WORDS;
+    const bool range = *dv.cursor >= dv.count;
+    if (fused)
+        store_last(last, st[ST_FIRST], st[ST_PACK_SAT], st[ST_SUM_SAT],
+                   range ? (int64_t)LMSGD_ERR_RANGE : st[ST_ERROR], range);
+    *dv.cursor += 1;
+    *dv.epoch = e;
+}
+
 // ------------------------------------------------------------------ world > 1
+
+// Every world > 1 kernel works on a block-shared copy of its XArgs whose epoch and
+// parity come from the device counter (*dev_epoch + 1), read once per block.
+__device__ __forceinline__ const XArgs& bind_epoch(const XArgs& in, XArgs& sx) {
+    if (threadIdx.x == 0) {
+        sx = in;
+        if (in.dev_epoch) {
+            sx.epoch = *reinterpret_cast<volatile const uint32_t*>(in.dev_epoch) + 1u;
+            sx.parity = (int)(sx.epoch & 1u);
+        }
+    }
+    __syncthreads();
+    return sx;
+}
 
 __device__ __forceinline__ uint32_t* flag_slot(const XArgs& x, int owner, int which) {
     return reinterpret_cast<uint32_t*>(x.peers.base[owner] + x.lay.off_flags + which * 128);
@@ -412,7 +466,8 @@ __device__ __forceinline__ bool spin_flag(const XArgs& x, const uint32_t* f) {
 // Chunk counters in a.ctr are reset by the block that completes them.
 __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
     pdl_enter();   // wait for the previous step / caller work; let k_xupdate queue up
-    const XArgs& x = a.x;
+    __shared__ XArgs sx;
+    const XArgs& x = bind_epoch(a.x, sx);
     __shared__ int s_ok;
     const bool t0 = threadIdx.x == 0;
     if (blockIdx.x == 0 && t0) stamp(x, TR_PACK_START);
@@ -535,7 +590,19 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
     // no griddepcontrol.wait: ordering with k_xstep1 is by flags D and cflag.
     // kXUnits units per block: 2 was faster in isolation (tools/xbench.cu, 109 vs
     // 120 us) but slower in the step (225 vs 215 us at k = 4), so 1.
-    const XArgs& x = a.x;
+    __shared__ XArgs sx;
+    const XArgs& x = bind_epoch(a.x, sx);
+    __shared__ UpdConst s_c;
+    __shared__ int s_range;
+    if (threadIdx.x == 0) {   // graph mode: this step's coefficients from the device table
+        s_c = a.c;
+        s_range = 0;
+        if (a.ctab) {
+            const int64_t idx = *reinterpret_cast<volatile const int64_t*>(a.cursor);
+            s_range = idx >= a.ctab_count;
+            s_c = a.ctab[s_range ? a.ctab_count - 1 : idx];
+        }
+    }
     __shared__ int s_go;
     const int64_t gsh = x.lay.shard >> 3;
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
@@ -571,7 +638,8 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
         s_go = go;
     }
     __syncthreads();
-    if (!s_go) return;
+    if (!s_go || s_range) return;
+    const UpdConst c = s_c;
 #pragma unroll
     for (int v = 0; v < kXUnits; ++v) {
         if (us[v] >= ups) continue;
@@ -580,7 +648,7 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
         const int64_t j0 = ((int64_t)owner[v] * gsh + gi) << 3;
         if (j0 >= x.n) continue;
         const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner[v]] + x.lay.off_R) + (gi << 3);
-        update8<RMS>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, a.c, a.th, a.d, a.m);
+        update8<RMS>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, c, a.th, a.d, a.m);
     }
 }
 
@@ -588,20 +656,27 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
 // been observed by then, so every rank's sum saturation count is final).
 __global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
     pdl_enter();
-    const XArgs& x = a.x;
+    __shared__ XArgs sx;
+    const XArgs& x = bind_epoch(a.x, sx);
     if (threadIdx.x != 0) return;
     // k_xupdate may complete before k_xstep1 (it never waits for its grid): the step
     // ends only once every k_xstep1 block has retired its last memory operation
     while (ld_acquire_sys(a.ctr + 1) < xstep1_blocks) __nanosleep(64);
     a.ctr[1] = 0;
     const volatile int64_t* mine = status_of(x, x.rank);
-    const int64_t gfirst = mine[ST_G_FIRST], err = mine[ST_G_ERROR];
+    const int64_t gfirst = mine[ST_G_FIRST];
+    int64_t err = mine[ST_G_ERROR];
+    if (!err && a.ctab && *a.cursor >= a.ctab_count) err = (int64_t)LMSGD_ERR_RANGE;   // table exhausted
     const bool skip = gfirst != kNone || err != 0;
     int64_t ssat = 0;
     if (!skip)
         for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, p))[ST_SUM_SAT];
     store_last(a.last, gfirst, mine[ST_G_PACK_SAT], ssat, err, skip);
     stamp(x, TR_UPD_END);
+    // the step is complete on this GPU: advance the device step counter (and cursor)
+    if (a.cursor) *a.cursor += 1;
+    __threadfence();
+    *a.x.dev_epoch = x.epoch;
 }
 
 // BN statistics without moving averages, one cooperative kernel
@@ -609,8 +684,10 @@ __global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
 // system fence per block, the last block releases flag C, every block acquires C of
 // all ranks, then averages its slice over the ranks' staging buffers in rank order,
 // in fp64, one rounding to fp32 (R16).  Double-buffered by call parity.
-__global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs x, float* __restrict__ mean,
+__global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs xin, float* __restrict__ mean,
                                                            float* __restrict__ var, int64_t C) {
+    __shared__ XArgs sx;
+    const XArgs& x = bind_epoch(xin, sx);
     __shared__ int s_ok;
     const int64_t Cp = (C + 3) & ~int64_t(3);   // var staged at a 16-B aligned offset
     const int64_t off = (int64_t)x.parity * 2 * LMSGD_MAX_BN_CHANNELS;
@@ -619,7 +696,10 @@ __global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs x, float* __res
         stage[i] = mean[i];
         stage[Cp + i] = var[i];
     }
-    if (grid_last(x, FLAG_C)) publish(x, FLAG_C);
+    if (grid_last(x, FLAG_C)) {
+        publish(x, FLAG_C);
+        *xin.dev_epoch = x.epoch;   // every block has read the call counter by now
+    }
     if (threadIdx.x == 0) s_ok = thread_wait_all(x, FLAG_C) ? 1 : 0;
     __syncthreads();
     if (!s_ok) return;
@@ -708,7 +788,7 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
     const int64_t gsh = a.x.lay.shard >> 3;
     (void)gsh;
     const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits);
-    if (a.c.a_rms != 0.0f)
+    if (a.c.a_rms != 0.0f || a.ctab)
         e = launch_pdl_if(true, k_xupdate<true>, grid, kThreads, s, a);
     else
         e = launch_pdl_if(true, k_xupdate<false>, grid, kThreads, s, a);
@@ -732,8 +812,8 @@ cudaError_t launch_status_reset(cudaStream_t s, int64_t* st) {
 }
 
 cudaError_t launch_pack(cudaStream_t s, const Launch& L, const float* g, int64_t n, int64_t n_pad,
-                        float scale, uint16_t* h, int64_t* st) {
-    return launch_pdl(k_pack, grid_for(L, n_pad >> 3), kThreads, s, g, n, n_pad, scale, h, st);
+                        float scale, uint16_t* h, int64_t* st, const Dev1& dv) {
+    return launch_pdl(k_pack, grid_for(L, n_pad >> 3), kThreads, s, g, n, n_pad, scale, h, st, dv);
 }
 
 cudaError_t launch_reduce_local(cudaStream_t s, const Launch& L, const uint16_t* h, int k,
@@ -743,27 +823,31 @@ cudaError_t launch_reduce_local(cudaStream_t s, const Launch& L, const uint16_t*
 
 cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, int64_t n,
                           const UpdConst& c, float* th, float* d, float* m, const int64_t* st,
-                          int64_t* st_reset, int64_t* last) {
+                          int64_t* st_reset, int64_t* last, const Dev1& dv) {
     const int grid = grid_for(L, (n + 7) >> 3);
-    if (c.a_rms != 0.0f)
-        return launch_pdl(k_update<true>, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last);
+    if (c.a_rms != 0.0f || dv.epoch)   // graph mode: alpha_RMSprop is only known on the device
+        return launch_pdl(k_update<true>, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last, dv);
     else
-        return launch_pdl(k_update<false>, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last);
+        return launch_pdl(k_update<false>, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last, dv);
 }
 
 cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                           const UpdConst& c, float* th, float* d, float* m, int64_t* st,
-                          int64_t* st_reset, int64_t* /*last: see launch_finalize_fused*/) {
+                          int64_t* st_reset, int64_t* /*last: see launch_finalize_fused*/, const Dev1& dv) {
     const int grid = grid_for(L, (n + 7) >> 3);
-    if (c.a_rms != 0.0f)
-        return launch_pdl(k_fused1<true>, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset);
+    if (c.a_rms != 0.0f || dv.epoch)
+        return launch_pdl(k_fused1<true>, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset, dv);
     else
-        return launch_pdl(k_fused1<false>, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset);
+        return launch_pdl(k_fused1<false>, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset, dv);
 }
 
 int64_t host_units(const XArgs& x) {
     const int64_t gsh = x.lay.shard >> 3;
     return (int64_t)x.world * ((gsh + kThreads - 1) / kThreads);
+}
+
+cudaError_t launch_advance1(cudaStream_t s, const Dev1& dv, int64_t* last, bool fused) {
+    return launch_pdl_if(true, k_advance1, 1, 32, s, dv, last, fused ? 1 : 0);
 }
 
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last) {

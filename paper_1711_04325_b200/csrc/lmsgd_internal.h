@@ -54,18 +54,31 @@ struct Launch {
                            // bit 2 = k_xstep1 (cooperative + PDL)
 };
 
+// Graph mode of the world == 1 step (lmsgd_step_graph): everything that changes
+// between steps is read from device memory at fixed addresses, so a captured CUDA
+// graph replays as the next step.  epoch == NULL selects host mode (arguments).
+struct Dev1 {
+    uint32_t* epoch;         // completed steps; this step is *epoch + 1 (parity = its low bit)
+    int64_t* st_base;        // the two status slots [2][ST_WORDS]
+    const UpdConst* ctab;    // coefficient table (lmsgd_schedule_upload)
+    int64_t count;
+    int64_t* cursor;         // index of this step's coefficients
+};
+
 // ---- single-GPU building blocks (sub-step ABI and world == 1)
 cudaError_t launch_status_reset(cudaStream_t s, int64_t* st);
 cudaError_t launch_pack(cudaStream_t s, const Launch& L, const float* g, int64_t n, int64_t n_pad,
-                        float scale, uint16_t* h, int64_t* st);
+                        float scale, uint16_t* h, int64_t* st, const Dev1& dv = Dev1{});
 cudaError_t launch_reduce_local(cudaStream_t s, const Launch& L, const uint16_t* h, int k,
                                 int64_t n_pad, uint16_t* R, int64_t* st);
 cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, int64_t n,
                           const UpdConst& c, float* th, float* d, float* m, const int64_t* st,
-                          int64_t* st_reset, int64_t* last);
+                          int64_t* st_reset, int64_t* last, const Dev1& dv = Dev1{});
 cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                           const UpdConst& c, float* th, float* d, float* m, int64_t* st,
-                          int64_t* st_reset, int64_t* last);
+                          int64_t* st_reset, int64_t* last, const Dev1& dv = Dev1{});
+// graph mode, k = 1: publish the fused step's status (fused) and advance the counters
+cudaError_t launch_advance1(cudaStream_t s, const Dev1& dv, int64_t* last, bool fused);
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last);
 int stream_blocks_per_sm();
 
@@ -80,6 +93,9 @@ struct XArgs {
     int64_t timeout_ns;
     unsigned int* ticket;
     int64_t* trace;      // NULL, or this step's TR_WORDS %globaltimer stamps (lmsgd_trace_enable)
+    uint32_t* dev_epoch; // device counter of completed steps (world > 1) or BN calls: the kernels
+                         // use epoch = *dev_epoch + 1 and the phase's last kernel advances it,
+                         // so a step captured in a CUDA graph replays as the next step
 };
 
 // Trace stamps of one world > 1 step (ns, this GPU's %globaltimer): pack start,
@@ -98,6 +114,9 @@ struct XStep {
     int64_t* last;
     unsigned int* ctr;   // local counters, reset by their completer: [0] pack blocks done,
                          // [1] k_xstep1 blocks retired, [2..3] unused, [4 + c] reduce units of chunk c
+    const UpdConst* ctab;    // graph mode: device coefficient table (lmsgd_schedule_upload), else NULL
+    int64_t ctab_count;
+    int64_t* cursor;         // graph mode: device index of the next step's coefficients
 };
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a);
 int xstep_blocks_per_sm();

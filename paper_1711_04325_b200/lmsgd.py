@@ -78,6 +78,8 @@ def _load() -> ctypes.CDLL:
         "lmsgd_step": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs)]),
         "lmsgd_step_host": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs), P]),
         "lmsgd_bn_stats_allreduce": (I32, [P, P, P, P, I64]),
+        "lmsgd_schedule_upload": (I32, [P, ctypes.POINTER(Hyper), ctypes.POINTER(Cluster), I64, I64]),
+        "lmsgd_step_graph": (I32, [P, P, P, P, P, P]),
         "lmsgd_query_status": (I32, [P, ctypes.POINTER(StepStatus)]),
         "lmsgd_profile_enable": (I32, [P, I64]),
         "lmsgd_profile_read": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]),
@@ -238,6 +240,22 @@ def lmsgd_step(ctx: Context, params, grads, delta, m, coeffs: Coeffs, stream=Non
     _check(_lib.lmsgd_step(ctx.ptr, _stream(stream), _ptr(params, torch.float32, "params"),
                            _ptr(grads, torch.float32, "grads"), _ptr(delta, torch.float32, "delta"),
                            _ptr(m, torch.float32, "m"), ctypes.byref(coeffs)), ctx)
+
+
+def lmsgd_schedule_upload(ctx: Context, hyper: Hyper | None, cluster: Cluster, t_first: int, count: int):
+    _check(_lib.lmsgd_schedule_upload(ctx.ptr, ctypes.byref(hyper) if hyper is not None else None,
+                                      ctypes.byref(cluster), int(t_first), int(count)), ctx)
+
+
+def lmsgd_step_graph(ctx: Context, params, grads, delta, m, stream=None):
+    """Graph-capturable step (coefficients and step number on the device)."""
+    import torch
+    for t, nm in ((params, "params"), (grads, "grads"), (delta, "delta"), (m, "m")):
+        if t.numel() != ctx.n:
+            raise ValueError(f"{nm} must have n_params = {ctx.n} elements")
+    _check(_lib.lmsgd_step_graph(ctx.ptr, _stream(stream), _ptr(params, torch.float32, "params"),
+                                 _ptr(grads, torch.float32, "grads"), _ptr(delta, torch.float32, "delta"),
+                                 _ptr(m, torch.float32, "m")), ctx)
 
 
 def lmsgd_step_host(ctx: Context, params, grads_host, delta, m, coeffs: Coeffs, status_host,

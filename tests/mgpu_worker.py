@@ -163,6 +163,42 @@ def main():
     replicas_identical(sync.mean, sync.var)
     L.lmsgd_finalize(ctx)
 
+    # ---- CUDA-graph entry point: device coefficient table + device step counter,
+    #      mixed with host steps, then captured once and replayed
+    n = 77_777
+    ctx = L.lmsgd_init(world, rank, local, n, S)
+    L.connect_process_group(ctx)
+    a = synth.grad_scale(n)
+    th0 = synth.theta0(n, None)
+    th, d, m = D(th0), D(np.zeros(n, np.float32)), D(np.zeros(n, np.float32))
+    L.lmsgd_schedule_upload(ctx, None, C1_C, 3, 10)          # steps 3 .. 12
+    gbuf = D(np.zeros(n, np.float32))
+    side = torch.cuda.Stream()
+    graph = None
+    for t in range(1, 8):
+        g = synth.grads(world, t, n, a)
+        prev = H(th), H(d), H(m)
+        gbuf.copy_(D(g[rank]))
+        if t <= 2:
+            L.lmsgd_step(ctx, th, gbuf, d, m, L.lmsgd_schedule_at(None, C1_C, t))
+        elif t == 3:
+            L.lmsgd_step_graph(ctx, th, gbuf, d, m)
+        else:
+            if graph is None:
+                graph = torch.cuda.CUDAGraph()
+                torch.cuda.synchronize()
+                with torch.cuda.stream(side):
+                    with torch.cuda.graph(graph, stream=side):
+                        L.lmsgd_step_graph(ctx, th, gbuf, d, m, stream=side)
+            graph.replay()
+        torch.cuda.synchronize()
+        code, st = L.lmsgd_query_status(ctx)
+        assert code == 0 and st.skipped == 0, (t, code)
+        check_state(H(th), H(d), H(m), *prev, exchange.exchange(list(g), S).ghat,
+                    schedule.coeffs_at(t, schedule.Hyper(), C1))
+        replicas_identical(th, d, m)
+    L.lmsgd_finalize(ctx)
+
     # ---- longer run: random schedule steps, replica bit-identity every step,
     #      resync parity every 10th step
     n = 333_331

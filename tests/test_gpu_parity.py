@@ -419,3 +419,54 @@ def test_bn_sync_world1_is_last_minibatch():
     assert torch.allclose(net[1].running_mean, h.mean(dim=(0, 2, 3)), rtol=1e-5, atol=1e-6)
     assert torch.allclose(net[1].running_var, h.var(dim=(0, 2, 3), unbiased=True), rtol=1e-4, atol=1e-6)
     L.lmsgd_finalize(ctx)
+
+
+# ------------------------------------------------------------------ CUDA graphs
+
+@pytest.mark.parametrize("flags", [0, L.LMSGD_FLAG_NO_SKIP])
+def test_graph_step_matches_host_step_and_replays(flags):
+    """lmsgd_step_graph (device coefficient table + device step counter) equals
+    lmsgd_step bit for bit, also when captured once in a CUDA graph and replayed."""
+    n, s = 300_007, 1024.0
+    th0, d0, m0 = init_state(n)
+    a = synth.grad_scale(n)
+    grads = [dev(synth.grads(1, t, n, a)[0]) for t in range(1, 7)]
+    ref = L.lmsgd_init(1, 0, 0, n, s, None, flags)
+    rt, rd, rm = dev(th0), dev(d0), dev(m0)
+    refs = []
+    for t in range(1, 7):
+        L.lmsgd_step(ref, rt, grads[t - 1], rd, rm, L.lmsgd_schedule_at(None, C1_C, t))
+        torch.cuda.synchronize()
+        refs.append((rt.clone(), rd.clone(), rm.clone()))
+    L.lmsgd_finalize(ref)
+
+    ctx = L.lmsgd_init(1, 0, 0, n, s, None, flags)
+    L.lmsgd_schedule_upload(ctx, None, C1_C, 1, 6)
+    th, d, m = dev(th0), dev(d0), dev(m0)
+    gbuf = grads[0].clone()
+    L.lmsgd_step_graph(ctx, th, gbuf, d, m)                  # step 1 eagerly
+    torch.cuda.synchronize()
+    assert all(torch.equal(x, y) for x, y in zip((th, d, m), refs[0]))
+    side = torch.cuda.Stream()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        with torch.cuda.graph(graph, stream=side):
+            L.lmsgd_step_graph(ctx, th, gbuf, d, m, stream=side)
+    for t in range(2, 7):                                     # each replay = the next step
+        gbuf.copy_(grads[t - 1])
+        graph.replay()
+        torch.cuda.synchronize()
+        assert all(torch.equal(x, y) for x, y in zip((th, d, m), refs[t - 1])), t
+        code, st = L.lmsgd_query_status(ctx)
+        assert code == 0 and st.skipped == 0
+    gbuf.copy_(grads[0])
+    before = (th.clone(), d.clone(), m.clone())
+    graph.replay()                                            # past the uploaded table
+    torch.cuda.synchronize()
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == L.LMSGD_ERR_RANGE and st.skipped == 1
+    assert all(torch.equal(x, y) for x, y in zip((th, d, m), before))
+    with pytest.raises(L.LmsgdError) as e:                    # no mixing at world 1
+        L.lmsgd_step(ctx, th, gbuf, d, m, L.make_coeffs(0.1, 1.0, 0.0))
+    assert e.value.status == L.LMSGD_ERR_STATE
+    L.lmsgd_finalize(ctx)
