@@ -34,7 +34,7 @@ struct lmsgd_ctx {
     DevState* dstate = nullptr;       // device
     lmsgd::UpdConst* d_ctab = nullptr;   // lmsgd_schedule_upload table
     int64_t ctab_count = 0, ctab_cap = 0;
-    int mode1 = 0;                    // world == 1: 0 unused, 1 lmsgd_step, 2 lmsgd_step_graph
+    int mode = 0;                     // 0 unused, 1 lmsgd_step, 2 lmsgd_step_graph (not mixed)
     int64_t* last = nullptr;          // device lmsgd_step_status of the last step
     float* d_grads = nullptr;         // device staging for lmsgd_step_host (lazy)
     uint32_t step = 0, bn_calls = 0;
@@ -355,16 +355,15 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     if (!coeffs_ok(coeffs))
         return fail(c, LMSGD_ERR_INVALID_ARG, "coeffs: need eta > 0, 0 <= alpha_sgd <= 1, alpha_rmsprop >= 0");
     if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
-    if (c->world == 1 && c->mode1 == 2)
-        return fail(c, LMSGD_ERR_STATE, "world == 1 context already runs lmsgd_step_graph");
+    if (c->mode == 2) return fail(c, LMSGD_ERR_STATE, "this context already runs lmsgd_step_graph");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const UpdConst u = make_const(c->hyper, *coeffs, c->world, c->scale);
     const uint32_t epoch = ++c->step;
     const int parity = static_cast<int>(epoch & 1u);
     c->last_stream = s;
+    c->mode = 1;
     if (c->world == 1) {
-        c->mode1 = 1;
         uint16_t* h = reinterpret_cast<uint16_t*>(c->buf + c->lay.off_recv);
         if (c->flags & LMSGD_FLAG_NO_SKIP) {
             CK(c, timed(c, s, 0, [&] {
@@ -423,15 +422,14 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
         return fail(c, LMSGD_ERR_INVALID_ARG, "params/grads/delta/m must be non-NULL and 16-byte aligned");
     if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
     if (c->ctab_count == 0) return fail(c, LMSGD_ERR_STATE, "lmsgd_schedule_upload has not been called");
-    if (c->world == 1 && c->mode1 == 1)
-        return fail(c, LMSGD_ERR_STATE, "world == 1 context already runs lmsgd_step");
+    if (c->mode == 1) return fail(c, LMSGD_ERR_STATE, "this context already runs lmsgd_step");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     const UpdConst u{};   // every coefficient comes from the device table
     c->last_stream = s;
     ++c->step;            // host-side count only (the kernels use the device counter)
+    c->mode = 2;
     if (c->world == 1) {
-        c->mode1 = 2;
         lmsgd::Dev1 dv{&c->dstate->k1epoch, status_slot(c, 0), c->d_ctab, c->ctab_count, &c->dstate->cursor};
         uint16_t* h = reinterpret_cast<uint16_t*>(c->buf + c->lay.off_recv);
         if (c->flags & LMSGD_FLAG_NO_SKIP) {
@@ -486,7 +484,8 @@ lmsgd_status lmsgd_bn_stats_allreduce(lmsgd_ctx* c, void* stream, float* mean, f
     if (c->world == 1) return LMSGD_OK;  // the average of one worker is itself
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    lmsgd::XArgs x = xargs(c, ++c->bn_calls, &c->dstate->bnepoch);
+    ++c->bn_calls;
+    lmsgd::XArgs x = xargs(c, 0, &c->dstate->bnepoch);   // epoch from the device call counter
     if (x.trace) { x.trace = nullptr; --c->trace_steps; }
     CK(c, lmsgd::launch_bn_allreduce(s, x, mean, var, C));
     return LMSGD_OK;

@@ -340,15 +340,16 @@ __global__ void k_advance1(Dev1 dv, int64_t* last, int fused) {
 
 // ------------------------------------------------------------------ world > 1
 
-// Every world > 1 kernel works on a block-shared copy of its XArgs whose epoch and
-// parity come from the device counter (*dev_epoch + 1), read once per block.
+// Host mode passes the step's epoch as an argument (x.epoch > 0).  Graph mode passes
+// epoch 0: the kernel then works on a block-shared copy of its XArgs whose epoch and
+// parity come from the device counter (*dev_epoch + 1), read once per block.  The
+// branch is uniform; host mode pays nothing.
 __device__ __forceinline__ const XArgs& bind_epoch(const XArgs& in, XArgs& sx) {
+    if (in.epoch != 0u) return in;
     if (threadIdx.x == 0) {
         sx = in;
-        if (in.dev_epoch) {
-            sx.epoch = *reinterpret_cast<volatile const uint32_t*>(in.dev_epoch) + 1u;
-            sx.parity = (int)(sx.epoch & 1u);
-        }
+        sx.epoch = *reinterpret_cast<volatile const uint32_t*>(in.dev_epoch) + 1u;
+        sx.parity = (int)(sx.epoch & 1u);
     }
     __syncthreads();
     return sx;
@@ -675,7 +676,6 @@ __global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
     stamp(x, TR_UPD_END);
     // the step is complete on this GPU: advance the device step counter (and cursor)
     if (a.cursor) *a.cursor += 1;
-    __threadfence();
     *a.x.dev_epoch = x.epoch;
 }
 
@@ -698,7 +698,7 @@ __global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs xin, float* __r
     }
     if (grid_last(x, FLAG_C)) {
         publish(x, FLAG_C);
-        *xin.dev_epoch = x.epoch;   // every block has read the call counter by now
+        *xin.dev_epoch = x.epoch;   // every block has read the call counter by now (graph mode)
     }
     if (threadIdx.x == 0) s_ok = thread_wait_all(x, FLAG_C) ? 1 : 0;
     __syncthreads();

@@ -289,11 +289,11 @@ def lmsgd_bn_stats_allreduce(ctx: Context, mean, var, stream=None):
 
 
 def lmsgd_query_status(ctx: Context) -> tuple[int, StepStatus]:
-    """(status code, StepStatus) of the last step; LMSGD_ERR_NONFINITE / TIMEOUT are
-    returned, not raised."""
+    """(status code, StepStatus) of the last step; LMSGD_ERR_NONFINITE / TIMEOUT /
+    RANGE (graph mode, table exhausted) are returned, not raised."""
     s = StepStatus()
     st = _lib.lmsgd_query_status(ctx.ptr, ctypes.byref(s))
-    if st not in (LMSGD_OK, LMSGD_ERR_NONFINITE, LMSGD_ERR_TIMEOUT):
+    if st not in (LMSGD_OK, LMSGD_ERR_NONFINITE, LMSGD_ERR_TIMEOUT, LMSGD_ERR_RANGE) or (st != LMSGD_OK and s.error == 0):
         _check(st, ctx)
     return st, s
 

@@ -164,14 +164,14 @@ def main():
     L.lmsgd_finalize(ctx)
 
     # ---- CUDA-graph entry point: device coefficient table + device step counter,
-    #      mixed with host steps, then captured once and replayed
+    #      eagerly, then captured once and replayed
     n = 77_777
     ctx = L.lmsgd_init(world, rank, local, n, S)
     L.connect_process_group(ctx)
     a = synth.grad_scale(n)
     th0 = synth.theta0(n, None)
     th, d, m = D(th0), D(np.zeros(n, np.float32)), D(np.zeros(n, np.float32))
-    L.lmsgd_schedule_upload(ctx, None, C1_C, 3, 10)          # steps 3 .. 12
+    L.lmsgd_schedule_upload(ctx, None, C1_C, 1, 10)          # steps 1 .. 10
     gbuf = D(np.zeros(n, np.float32))
     side = torch.cuda.Stream()
     graph = None
@@ -179,9 +179,7 @@ def main():
         g = synth.grads(world, t, n, a)
         prev = H(th), H(d), H(m)
         gbuf.copy_(D(g[rank]))
-        if t <= 2:
-            L.lmsgd_step(ctx, th, gbuf, d, m, L.lmsgd_schedule_at(None, C1_C, t))
-        elif t == 3:
+        if t <= 3:
             L.lmsgd_step_graph(ctx, th, gbuf, d, m)
         else:
             if graph is None:
