@@ -340,26 +340,27 @@ __global__ void k_advance1(Dev1 dv, int64_t* last, int fused) {
 
 // ------------------------------------------------------------------ world > 1
 
-// Host mode passes the step's epoch as an argument (x.epoch > 0).  Graph mode passes
-// epoch 0: the kernel then works on a block-shared copy of its XArgs whose epoch and
-// parity come from the device counter (*dev_epoch + 1), read once per block.  The
-// branch is uniform; host mode pays nothing.
-__device__ __forceinline__ const XArgs& bind_epoch(const XArgs& in, XArgs& sx) {
-    if (in.epoch != 0u) return in;
-    if (threadIdx.x == 0) {
-        sx = in;
-        sx.epoch = *reinterpret_cast<volatile const uint32_t*>(in.dev_epoch) + 1u;
-        sx.parity = (int)(sx.epoch & 1u);
-    }
+// The step's (or BN call's) epoch and status parity.  Host mode passes them as
+// arguments (x.epoch > 0); graph mode passes epoch 0 and the kernel reads the device
+// counter (*dev_epoch + 1) once per block.  The branch is uniform; the XArgs
+// themselves always stay in the kernel parameter space.
+struct Ep {
+    uint32_t e;
+    int par;
+};
+__device__ __forceinline__ Ep get_ep(const XArgs& x) {
+    if (x.epoch != 0u) return Ep{x.epoch, x.parity};
+    __shared__ uint32_t s_e;
+    if (threadIdx.x == 0) s_e = *reinterpret_cast<volatile const uint32_t*>(x.dev_epoch) + 1u;
     __syncthreads();
-    return sx;
+    return Ep{s_e, (int)(s_e & 1u)};
 }
 
 __device__ __forceinline__ uint32_t* flag_slot(const XArgs& x, int owner, int which) {
     return reinterpret_cast<uint32_t*>(x.peers.base[owner] + x.lay.off_flags + which * 128);
 }
-__device__ __forceinline__ int64_t* status_of(const XArgs& x, int owner) {
-    return reinterpret_cast<int64_t*>(x.peers.base[owner] + x.lay.off_status) + x.parity * ST_WORDS;
+__device__ __forceinline__ int64_t* status_of(const XArgs& x, const Ep& ep, int owner) {
+    return reinterpret_cast<int64_t*>(x.peers.base[owner] + x.lay.off_status) + ep.par * ST_WORDS;
 }
 
 __device__ __forceinline__ void stamp(const XArgs& x, int which) {
@@ -390,26 +391,26 @@ __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
 // Release `value` into slot p of every rank: one system-scope fence, then relaxed
 // stores (= a release pattern).  k st.release.sys cost ~1.5 us each on NVLink 5
 // (tools/flagbench.cu); the single fence + relaxed stores ~1 us total.
-__device__ void publish(const XArgs& x, int which) {
+__device__ void publish(const XArgs& x, const Ep& ep, int which) {
     __threadfence_system();
-    for (int p = 0; p < x.world; ++p) st_relaxed_sys(flag_slot(x, p, which) + x.rank, x.epoch);
+    for (int p = 0; p < x.world; ++p) st_relaxed_sys(flag_slot(x, p, which) + x.rank, ep.e);
 }
 
 
 // One thread: wait until every rank has published `which` for this epoch (bounded
 // spin; on timeout record LMSGD_ERR_TIMEOUT in this rank's words and return false).
-__device__ bool thread_wait_all(const XArgs& x, int which, bool trace_seen = false) {
+__device__ bool thread_wait_all(const XArgs& x, const Ep& ep, int which, bool trace_seen = false) {
     const uint64_t t0 = globaltimer();
     for (int p = 0; p < x.world; ++p) {
         const uint32_t* f = flag_slot(x, x.rank, which) + p;
         if (trace_seen && x.trace) {   // per-peer arrival, diagnostics only
-            while ((int32_t)(ld_acquire_sys(f) - x.epoch) < 0) {}
+            while ((int32_t)(ld_acquire_sys(f) - ep.e) < 0) {}
             x.trace[TR_A_SEEN + p] = (int64_t)globaltimer();
         }
-        while ((int32_t)(ld_acquire_sys(f) - x.epoch) < 0) {
+        while ((int32_t)(ld_acquire_sys(f) - ep.e) < 0) {
             __nanosleep(64);
             if ((int64_t)(globaltimer() - t0) > x.timeout_ns) {
-                int64_t* mine = status_of(x, x.rank);
+                int64_t* mine = status_of(x, ep, x.rank);
                 mine[ST_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
                 mine[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
                 __threadfence_system();
@@ -438,9 +439,9 @@ __device__ __forceinline__ uint32_t* cflag(const XArgs& x, int r, int c, int own
     return reinterpret_cast<uint32_t*>(x.peers.base[r] + x.lay.off_cflags) + (int64_t)c * LMSGD_MAX_WORLD + owner;
 }
 
-__device__ __forceinline__ bool spin_flag(const XArgs& x, const uint32_t* f) {
+__device__ __forceinline__ bool spin_flag(const XArgs& x, const Ep& ep, const uint32_t* f) {
     const uint64_t t0 = globaltimer();
-    while ((int32_t)(ld_acquire_sys(f) - x.epoch) < 0) {
+    while ((int32_t)(ld_acquire_sys(f) - ep.e) < 0) {
         __nanosleep(32);
         if ((int64_t)(globaltimer() - t0) > x.timeout_ns) return false;
     }
@@ -467,14 +468,14 @@ __device__ __forceinline__ bool spin_flag(const XArgs& x, const uint32_t* f) {
 // Chunk counters in a.ctr are reset by the block that completes them.
 __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
     pdl_enter();   // wait for the previous step / caller work; let k_xupdate queue up
-    __shared__ XArgs sx;
-    const XArgs& x = bind_epoch(a.x, sx);
+    const XArgs& x = a.x;
+    const Ep ep = get_ep(x);
     __shared__ int s_ok;
     const bool t0 = threadIdx.x == 0;
     if (blockIdx.x == 0 && t0) stamp(x, TR_PACK_START);
     const int64_t gsh = x.lay.shard >> 3;
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
-    int64_t* mine = status_of(x, x.rank);
+    int64_t* mine = status_of(x, ep, x.rank);
 
     // ---- 1. pack + push
     {
@@ -499,18 +500,18 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
     if (t0 && atomicAdd(a.ctr + 0, 1u) + 1u == gridDim.x) {
         a.ctr[0] = 0;
         stamp(x, TR_PACK_END);
-        publish(x, FLAG_A);
+        publish(x, ep, FLAG_A);
         stamp(x, TR_PUB_END);
     }
 
     // ---- 2. all ranks packed; block 0 makes the global skip decision (identical on
     //         every rank) and releases the local flag D.  The reduce does not need it.
-    if (t0) s_ok = thread_wait_all(x, FLAG_A, blockIdx.x == 0) ? 1 : 0;
+    if (t0) s_ok = thread_wait_all(x, ep, FLAG_A, blockIdx.x == 0) ? 1 : 0;
     __syncthreads();
     if (blockIdx.x == 0) {
         __shared__ int64_t s_st[3 * LMSGD_MAX_WORLD];
         if (threadIdx.x < x.world) {   // every rank's final pack words, read in parallel
-            const volatile int64_t* sp = status_of(x, threadIdx.x);
+            const volatile int64_t* sp = status_of(x, ep, threadIdx.x);
             s_st[3 * threadIdx.x] = sp[ST_FIRST];
             s_st[3 * threadIdx.x + 1] = sp[ST_PACK_SAT];
             s_st[3 * threadIdx.x + 2] = sp[ST_ERROR];
@@ -527,10 +528,10 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
             mine[ST_G_PACK_SAT] = psat;
             mine[ST_G_ERROR] = err;
             int64_t* nxt = reinterpret_cast<int64_t*>(x.peers.base[x.rank] + x.lay.off_status) +
-                           (x.parity ^ 1) * ST_WORDS;   // next step's slot: every rank has read it
+                           (ep.par ^ 1) * ST_WORDS;   // next step's slot: every rank has read it
             for (int w = 0; w < ST_WORDS; ++w) nxt[w] = (w == ST_FIRST || w == ST_G_FIRST) ? kNone : 0;
             __threadfence();
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag_slot(x, x.rank, FLAG_D)), "r"(x.epoch)
+            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag_slot(x, x.rank, FLAG_D)), "r"(ep.e)
                          : "memory");
             stamp(x, TR_RED_START);
         }
@@ -578,7 +579,7 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
             const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
             if (atomicAdd(a.ctr + 4 + c, 1u) + 1u == cnt) {
                 a.ctr[4 + c] = 0;
-                for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, c, x.rank), x.epoch);
+                for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, c, x.rank), ep.e);
             }
         }
     }
@@ -591,8 +592,8 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
     // no griddepcontrol.wait: ordering with k_xstep1 is by flags D and cflag.
     // kXUnits units per block: 2 was faster in isolation (tools/xbench.cu, 109 vs
     // 120 us) but slower in the step (225 vs 215 us at k = 4), so 1.
-    __shared__ XArgs sx;
-    const XArgs& x = bind_epoch(a.x, sx);
+    const XArgs& x = a.x;
+    const Ep ep = get_ep(x);
     __shared__ UpdConst s_c;
     __shared__ int s_range;
     if (threadIdx.x == 0) {   // graph mode: this step's coefficients from the device table
@@ -622,17 +623,17 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
     }
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) stamp(x, TR_UPD_START);
-        int go = spin_flag(x, flag_slot(x, x.rank, FLAG_D)) ? 1 : 0;
+        int go = spin_flag(x, ep, flag_slot(x, x.rank, FLAG_D)) ? 1 : 0;
         if (go) {
             // wait for the owners' chunks even when the step is skipped: the step may
             // end only after every owner's reduce has finished reading its receive slots
             for (int v = 0; v < kXUnits; ++v)
-                if (us[v] < ups && !spin_flag(x, cflag(x, x.rank, cch[v], owner[v]))) {
+                if (us[v] < ups && !spin_flag(x, ep, cflag(x, x.rank, cch[v], owner[v]))) {
                     go = 0;
-                    status_of(x, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+                    status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
                     break;
                 }
-            const volatile int64_t* vm = status_of(x, x.rank);
+            const volatile int64_t* vm = status_of(x, ep, x.rank);
             if (vm[ST_G_FIRST] != kNone || vm[ST_G_ERROR] != 0) go = 0;   // skipped step
         }
         if (blockIdx.x == 0) stamp(x, TR_UPD_GO);
@@ -657,26 +658,26 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
 // been observed by then, so every rank's sum saturation count is final).
 __global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
     pdl_enter();
-    __shared__ XArgs sx;
-    const XArgs& x = bind_epoch(a.x, sx);
+    const XArgs& x = a.x;
+    const Ep ep = get_ep(x);
     if (threadIdx.x != 0) return;
     // k_xupdate may complete before k_xstep1 (it never waits for its grid): the step
     // ends only once every k_xstep1 block has retired its last memory operation
     while (ld_acquire_sys(a.ctr + 1) < xstep1_blocks) __nanosleep(64);
     a.ctr[1] = 0;
-    const volatile int64_t* mine = status_of(x, x.rank);
+    const volatile int64_t* mine = status_of(x, ep, x.rank);
     const int64_t gfirst = mine[ST_G_FIRST];
     int64_t err = mine[ST_G_ERROR];
     if (!err && a.ctab && *a.cursor >= a.ctab_count) err = (int64_t)LMSGD_ERR_RANGE;   // table exhausted
     const bool skip = gfirst != kNone || err != 0;
     int64_t ssat = 0;
     if (!skip)
-        for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, p))[ST_SUM_SAT];
+        for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, ep, p))[ST_SUM_SAT];
     store_last(a.last, gfirst, mine[ST_G_PACK_SAT], ssat, err, skip);
     stamp(x, TR_UPD_END);
     // the step is complete on this GPU: advance the device step counter (and cursor)
     if (a.cursor) *a.cursor += 1;
-    *a.x.dev_epoch = x.epoch;
+    *a.x.dev_epoch = ep.e;
 }
 
 // BN statistics without moving averages, one cooperative kernel
@@ -684,23 +685,22 @@ __global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
 // system fence per block, the last block releases flag C, every block acquires C of
 // all ranks, then averages its slice over the ranks' staging buffers in rank order,
 // in fp64, one rounding to fp32 (R16).  Double-buffered by call parity.
-__global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs xin, float* __restrict__ mean,
+__global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs x, float* __restrict__ mean,
                                                            float* __restrict__ var, int64_t C) {
-    __shared__ XArgs sx;
-    const XArgs& x = bind_epoch(xin, sx);
+    const Ep ep = get_ep(x);
     __shared__ int s_ok;
     const int64_t Cp = (C + 3) & ~int64_t(3);   // var staged at a 16-B aligned offset
-    const int64_t off = (int64_t)x.parity * 2 * LMSGD_MAX_BN_CHANNELS;
+    const int64_t off = (int64_t)ep.par * 2 * LMSGD_MAX_BN_CHANNELS;
     float* stage = reinterpret_cast<float*>(x.peers.base[x.rank] + x.lay.off_bn) + off;
     for (int64_t i = gtid(); i < C; i += gstride()) {
         stage[i] = mean[i];
         stage[Cp + i] = var[i];
     }
     if (grid_last(x, FLAG_C)) {
-        publish(x, FLAG_C);
-        *xin.dev_epoch = x.epoch;   // every block has read the call counter by now (graph mode)
+        publish(x, ep, FLAG_C);
+        *x.dev_epoch = ep.e;   // every block has read the call counter by now
     }
-    if (threadIdx.x == 0) s_ok = thread_wait_all(x, FLAG_C) ? 1 : 0;
+    if (threadIdx.x == 0) s_ok = thread_wait_all(x, ep, FLAG_C) ? 1 : 0;
     __syncthreads();
     if (!s_ok) return;
     // one float4 of every rank per thread, all peer loads issued before the sums
