@@ -153,7 +153,10 @@ lmsgd_status lmsgd_ipc_handle(lmsgd_ctx* ctx, uint8_t* out);
  * must be called by all ranks before the first step. */
 lmsgd_status lmsgd_connect(lmsgd_ctx* ctx, const uint8_t* handles);
 
-/* Synchronizes the device, unmaps peers, frees library buffers.  NULL is a no-op. */
+/* Synchronizes the device, unmaps peers, frees library buffers.  NULL is a no-op.
+ * world > 1: collective -- every rank must have finished its last step (e.g. a
+ * barrier after lmsgd_query_status) before any rank finalizes, since peers write
+ * into this rank's buffer during a step. */
 lmsgd_status lmsgd_finalize(lmsgd_ctx* ctx);
 
 /* Message of the last failing call on ctx ("" if none); valid until the next call. */

@@ -5,6 +5,12 @@
 //        -I paper_1711_04325_b200/csrc tools/xbench.cu -o tools/xbench
 #include "../paper_1711_04325_b200/csrc/kernels.cu"
 
+namespace lmsgd {
+namespace {
+#include "../paper_1711_04325_b200/csrc/stream_tma.cuh"
+}  // namespace
+}  // namespace lmsgd
+
 #include <cstdio>
 #include <cstdlib>
 #include <functional>
@@ -169,6 +175,51 @@ __global__ void __launch_bounds__(256) k_upd_pull_nc(Ptrs P, int world, int rank
     update8<true>(r, j0, n, c, th, d, m);
 }
 
+// update pull with the unit's R fetched by one bulk copy (TMA engine) into shared memory
+__global__ void __launch_bounds__(256) k_upd_pull_bulk(Ptrs P, int world, int rank, int64_t shard, int64_t n, UpdConst c,
+                                                       float* __restrict__ th, float* __restrict__ d, float* __restrict__ m) {
+    __shared__ __align__(128) uint4 sR[256];
+    __shared__ __align__(8) uint64_t bar;
+    const int64_t gsh = shard >> 3;
+    const int64_t u = blockIdx.x;
+    const int owner = (int)((u % world + rank) % world);
+    const int64_t g0 = (u / world) * 256;
+    const int64_t cnt = (gsh - g0) < 256 ? (gsh - g0) : 256;
+    if (cnt <= 0) return;
+    if (threadIdx.x == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        mbar_expect_tx(&bar, (unsigned)(cnt * 16));
+        bulk_g2s(sR, P.R[owner] + (g0 << 3), (unsigned)(cnt * 16), &bar, policy_evict_first());
+    }
+    const int64_t gi = g0 + threadIdx.x;
+    const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+    const bool act = threadIdx.x < cnt && j0 < n;
+    float4 t0, t1, d0, d1, m0, m1;
+    if (act && j0 + 8 <= n) {   // state loads in flight while the bulk copy runs
+        t0 = __ldcs(reinterpret_cast<const float4*>(th + j0)); t1 = __ldcs(reinterpret_cast<const float4*>(th + j0) + 1);
+        d0 = __ldcs(reinterpret_cast<const float4*>(d + j0)); d1 = __ldcs(reinterpret_cast<const float4*>(d + j0) + 1);
+        m0 = __ldcs(reinterpret_cast<const float4*>(m + j0)); m1 = __ldcs(reinterpret_cast<const float4*>(m + j0) + 1);
+    }
+    mbar_wait(&bar, 0);
+    if (!act) return;
+    if (j0 + 8 > n) { update8<true>(sR[threadIdx.x], j0, n, c, th, d, m); return; }
+    const uint4 r = sR[threadIdx.x];
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+    float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+    float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    float mv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) upd1<true>(h2f(w[i >> 1], i & 1) * c.inv_ks, tv[i], dv[i], mv[i], c);
+    float4* t4 = reinterpret_cast<float4*>(th + j0); float4* d4 = reinterpret_cast<float4*>(d + j0); float4* m4 = reinterpret_cast<float4*>(m + j0);
+    __stcs(t4, make_float4(tv[0], tv[1], tv[2], tv[3])); __stcs(t4 + 1, make_float4(tv[4], tv[5], tv[6], tv[7]));
+    __stcs(d4, make_float4(dv[0], dv[1], dv[2], dv[3])); __stcs(d4 + 1, make_float4(dv[4], dv[5], dv[6], dv[7]));
+    __stcs(m4, make_float4(mv[0], mv[1], mv[2], mv[3])); __stcs(m4 + 1, make_float4(mv[4], mv[5], mv[6], mv[7]));
+}
+
 // all-gather push: owner writes its R shard into every rank's full-R buffer (persistent)
 __global__ void __launch_bounds__(256) k_ag_push(const uint16_t* __restrict__ Rmine, uint16_t* const* full, int world,
                                                  int rank, int64_t shard) {
@@ -250,7 +301,8 @@ int main(int argc, char** argv) {
         run("P persistent 148x6, 16 elem/thread", pb, [&](int i) { xb::k_push16<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n); });
         run("P persistent 148x8, one fence/block", pb, [&](int i) { xb::k_push_fenced<<<sms * 8, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
         run("P persistent 148x4, one fence/block", pb, [&](int i) { xb::k_push_fenced<<<sms * 4, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
-        run("update pull, R via ld.global.nc", 26.0 * n, [&](int i) { xb::k_upd_pull_nc<<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
+        run("update pull, R by one bulk copy per block", 26.0 * n, [&](int i) { xb::k_upd_pull_bulk<<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
+    run("update pull, R via ld.global.nc", 26.0 * n, [&](int i) { xb::k_upd_pull_nc<<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
         run("P persistent 148x6, fence/unit", pb, [&](int i) { xb::k_push_fenced<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1); });
         run("P persistent 148x2, fence/unit", pb, [&](int i) { xb::k_push_fenced<<<sms * 2, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1); });
         run("P 148x2 fence/unit || local update (2 streams)", 26.0 * n, [&](int i) {
