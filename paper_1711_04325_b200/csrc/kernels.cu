@@ -788,10 +788,11 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
     const int64_t gsh = a.x.lay.shard >> 3;
     (void)gsh;
     const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits);
+    const bool pdl = (L.pdl_mask & 4) == 0;   // bit 4 (diagnostics): launch k_xupdate after k_xstep1 completes
     if (a.c.a_rms != 0.0f || a.ctab)
-        e = launch_pdl_if(true, k_xupdate<true>, grid, kThreads, s, a);
+        e = launch_pdl_if(pdl, k_xupdate<true>, grid, kThreads, s, a);
     else
-        e = launch_pdl_if(true, k_xupdate<false>, grid, kThreads, s, a);
+        e = launch_pdl_if(pdl, k_xupdate<false>, grid, kThreads, s, a);
     if (e != cudaSuccess) return e;
     return launch_pdl_if(true, k_xfinalize, 1, 32, s, a, (unsigned int)L.grid_xstep);
 }
