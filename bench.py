@@ -289,8 +289,9 @@ def main():
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    code, st = L.lmsgd_query_status(ctx)
-    assert code == 0, f"warm-up step status {code}"
+    if args.warmup > 0:
+        code, st = L.lmsgd_query_status(ctx)
+        assert code == 0, f"warm-up step status {code}"
 
     # kernels launched per step: fused = k_fused1 + status finalize; guarded k=1 = k_pack
     # + k_update; world > 1 = k_xstep1 + k_xupdate + k_xfinalize
