@@ -104,7 +104,9 @@ typedef struct lmsgd_ctx lmsgd_ctx;   /* opaque, library-owned */
 
 /* init flags */
 #define LMSGD_FLAG_NO_SKIP 0x1u   /* k = 1: single-pass fused pack+update (28 B/elem); non-finite
-                                     gradients are detected and reported but NOT skipped */
+                                     gradients are detected and reported but NOT skipped.
+                                     Ignored for world > 1, where the skip decision is free
+                                     (the reduce needs every rank's payload anyway). */
 
 /* ---------------------------------------------------------------- host-only */
 

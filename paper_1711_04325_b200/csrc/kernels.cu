@@ -199,6 +199,24 @@ __device__ __forceinline__ void write_last(int64_t* last, int64_t first, int64_t
     if (last && blockIdx.x == 0 && threadIdx.x == 0) store_last(last, first, psat, ssat, err, skipped);
 }
 
+// R[j0 .. j0+8) = sat16_RNE(sum_{p<k} slot_p[j0 .. j0+8)), slots `stride` elements apart:
+// widened to fp64 and summed in slot order (exact, so order-free), one rounding.
+__device__ __forceinline__ void reduce8(const uint16_t* __restrict__ slots, int64_t stride, int k, int64_t j0,
+                                        uint16_t* __restrict__ R, unsigned& sat) {
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int p = 0; p < k; ++p) {
+        const uint4 q = *reinterpret_cast<const uint4*>(slots + (int64_t)p * stride + j0);
+        const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
+    }
+    unsigned short o[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
+    *reinterpret_cast<uint4*>(R + j0) = make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
+                                                  o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
+}
+
 __device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 
@@ -236,22 +254,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_local(const uint16_t* __res
     pdl_enter();
     unsigned sat = 0;
     const int64_t nv = n_pad >> 3;
-    for (int64_t v = gtid(); v < nv; v += gstride()) {
-        const int64_t j0 = v << 3;
-        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-        for (int i = 0; i < k; ++i) {  // worker order; exact, so order-free anyway
-            const uint4 q = *reinterpret_cast<const uint4*>(h + (int64_t)i * n_pad + j0);
-            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-            for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
-        }
-        unsigned short o[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
-        *reinterpret_cast<uint4*>(R + j0) =
-            make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
-                       o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
-    }
+    for (int64_t v = gtid(); v < nv; v += gstride()) reduce8(h, n_pad, k, v << 3, R, sat);
     if (st) flush_status(kNone, sat, st, ST_SUM_SAT);
 }
 
@@ -550,22 +553,7 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
     unsigned sat = 0;
     for (int64_t u = blockIdx.x; u < ups; u += gridDim.x) {
         const int64_t gi = u * kThreads + threadIdx.x;
-        if (gi < gsh) {
-            const int64_t j0 = gi << 3;
-            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-            for (int p = 0; p < x.world; ++p) {
-                const uint4 q = *reinterpret_cast<const uint4*>(recv + (int64_t)p * x.lay.shard + j0);
-                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-#pragma unroll
-                for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
-            }
-            unsigned short o[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
-            *reinterpret_cast<uint4*>(R + j0) =
-                make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16,
-                           o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
-        }
+        if (gi < gsh) reduce8(recv, x.lay.shard, x.world, gi << 3, R, sat);
     }
     flush_status(kNone, sat, mine, ST_SUM_SAT);
     // one system fence per block (a fence per unit stalls behind the concurrent
