@@ -164,6 +164,14 @@ lmsgd_status lmsgd_finalize(lmsgd_ctx* ctx);
 /* Message of the last failing call on ctx ("" if none); valid until the next call. */
 const char* lmsgd_last_error(const lmsgd_ctx* ctx);
 
+/* Weight decay inherited from Goyal et al. ("the same settings are
+ * used unless otherwise specified"; reading R12): from the next step on,
+ * ghat_j <- ghat_j + lambda theta_j for j < n_decay (-1 = all n_params) before the
+ * m update -- the torch.optim convention, so the caller puts the decayed tensors
+ * (e.g. conv/fc weights) first and BN / bias parameters after them.  lambda = 0
+ * (default) disables it.  Graph mode: set before lmsgd_schedule_upload. */
+lmsgd_status lmsgd_set_weight_decay(lmsgd_ctx* ctx, double lambda, int64_t n_decay);
+
 /* ---------------------------------------------------------------- hot path */
 
 /* One synchronous data-parallel iteration on this rank (all ranks must call it

@@ -52,10 +52,10 @@ def run(theta0, grads_fn, k: int, T: int, s: float = 1.0,
 
 
 def resync_step(theta_prev, delta_prev, m_prev, ghat, c: schedule.Coeffs,
-                hyper: schedule.Hyper = schedule.Hyper()):
+                hyper: schedule.Hyper = schedule.Hyper(), weight_decay=0.0, n_decay=None):
     """Float64 update from a given state and ghat (the GPU's fp32 values)."""
     return update.step(theta_prev, ghat, m_prev, delta_prev, c.eta, c.alpha_sgd,
-                       c.alpha_rmsprop, hyper.mu1, hyper.mu2, hyper.eps)
+                       c.alpha_rmsprop, hyper.mu1, hyper.mu2, hyper.eps, weight_decay, n_decay)
 
 
 def scaled_error(x_gpu, x_ora, scale) -> float:

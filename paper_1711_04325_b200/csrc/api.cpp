@@ -22,6 +22,8 @@ struct lmsgd_ctx {
     int64_t n = 0, n_pad = 0;
     float scale = 1.0f;
     lmsgd_hyper hyper{};
+    double wd = 0.0;                  // lmsgd_set_weight_decay (R12)
+    int64_t n_wd = 0;
     uint32_t flags = 0;
     Layout lay{};
     char* buf = nullptr;           // own exchange buffer (IPC-shared when world > 1)
@@ -110,8 +112,11 @@ bool hyper_ok(const lmsgd_hyper* h) {
 }
 
 // fp32 constants rounded once from double (R15: fp32(1 - mu2), not 1 - fp32(mu2)).
-UpdConst make_const(const lmsgd_hyper& h, const lmsgd_coeffs& c, int k, float s) {
+UpdConst make_const(const lmsgd_hyper& h, const lmsgd_coeffs& c, int k, float s, double wd = 0.0,
+                    int64_t n_wd = 0) {
     UpdConst u{};
+    u.wd = static_cast<float>(wd);
+    u.n_wd = wd > 0.0 ? n_wd : 0;   // wd = 0: the decay branch is never taken (keeps -0.0 exact)
     u.mu1 = static_cast<float>(h.mu1);
     u.mu2 = static_cast<float>(h.mu2);
     u.omm2 = static_cast<float>(1.0 - h.mu2);
@@ -358,7 +363,7 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     if (c->mode == 2) return fail(c, LMSGD_ERR_STATE, "this context already runs lmsgd_step_graph");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const UpdConst u = make_const(c->hyper, *coeffs, c->world, c->scale);
+    const UpdConst u = make_const(c->hyper, *coeffs, c->world, c->scale, c->wd, c->n_wd);
     const uint32_t epoch = ++c->step;
     const int parity = static_cast<int>(epoch & 1u);
     c->last_stream = s;
@@ -388,6 +393,15 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     return LMSGD_OK;
 }
 
+lmsgd_status lmsgd_set_weight_decay(lmsgd_ctx* c, double lambda, int64_t n_decay) {
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (!(lambda >= 0.0) || !std::isfinite(lambda) || n_decay < -1 || n_decay > c->n)
+        return fail(c, LMSGD_ERR_INVALID_ARG, "weight decay: need lambda >= 0 and -1 <= n_decay <= n_params");
+    c->wd = lambda;
+    c->n_wd = n_decay < 0 ? c->n : n_decay;
+    return LMSGD_OK;
+}
+
 lmsgd_status lmsgd_schedule_upload(lmsgd_ctx* c, const lmsgd_hyper* hyper, const lmsgd_cluster* cluster,
                                    int64_t t_first, int64_t count) {
     if (!c || !cluster || t_first < 1 || count < 1 || count > (int64_t(1) << 24))
@@ -399,7 +413,7 @@ lmsgd_status lmsgd_schedule_upload(lmsgd_ctx* c, const lmsgd_hyper* hyper, const
         lmsgd_coeffs co{};
         const lmsgd_status st = lmsgd_schedule_at(&h, cluster, t_first + i, &co);
         if (st != LMSGD_OK) return fail(c, st, "schedule_upload: step " + std::to_string(t_first + i) + " is out of range");
-        tab[static_cast<size_t>(i)] = make_const(c->hyper, co, c->world, c->scale);
+        tab[static_cast<size_t>(i)] = make_const(c->hyper, co, c->world, c->scale, c->wd, c->n_wd);
     }
     DeviceGuard g(c->device);
     CK(c, cudaDeviceSynchronize());

@@ -157,7 +157,8 @@ __device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const Up
         float mv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            const float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
+            float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
+            if (j0 + i < c.n_wd) gh = fmaf(c.wd, tv[i], gh);   // R12 weight decay (wd = 0: exact no-op)
             upd1<RMS>(gh, tv[i], dv[i], mv[i], c);
         }
         __stcs(th4, make_float4(tv[0], tv[1], tv[2], tv[3]));
@@ -168,8 +169,9 @@ __device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const Up
         __stcs(m4 + 1, make_float4(mv[4], mv[5], mv[6], mv[7]));
     } else {
         for (int i = 0; i < 8 && j0 + i < n; ++i) {
-            const float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
+            float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
             float t = th[j0 + i], dd = d[j0 + i], mm = m[j0 + i];
+            if (j0 + i < c.n_wd) gh = fmaf(c.wd, t, gh);
             upd1<RMS>(gh, t, dd, mm, c);
             th[j0 + i] = t; d[j0 + i] = dd; m[j0 + i] = mm;
         }

@@ -22,6 +22,8 @@ struct UpdConst {
     float mu1, mu2, omm2, eps;   // omm2 = fp32(1 - mu2), computed in double
     float eta, a_sgd, a_rms;
     float inv_ks;                // fp32(1 / (k s)), exact for power-of-two k s
+    float wd;                    // weight decay lambda (R12), 0 = off
+    int64_t n_wd;                // elements [0, n_wd) are decayed
 };
 
 // Layout of one rank's exchange buffer (CUDA IPC-shared when world > 1).

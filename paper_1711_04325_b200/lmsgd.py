@@ -78,6 +78,7 @@ def _load() -> ctypes.CDLL:
         "lmsgd_step": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs)]),
         "lmsgd_step_host": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs), P]),
         "lmsgd_bn_stats_allreduce": (I32, [P, P, P, P, I64]),
+        "lmsgd_set_weight_decay": (I32, [P, ctypes.c_double, I64]),
         "lmsgd_schedule_upload": (I32, [P, ctypes.POINTER(Hyper), ctypes.POINTER(Cluster), I64, I64]),
         "lmsgd_step_graph": (I32, [P, P, P, P, P, P]),
         "lmsgd_query_status": (I32, [P, ctypes.POINTER(StepStatus)]),
@@ -240,6 +241,10 @@ def lmsgd_step(ctx: Context, params, grads, delta, m, coeffs: Coeffs, stream=Non
     _check(_lib.lmsgd_step(ctx.ptr, _stream(stream), _ptr(params, torch.float32, "params"),
                            _ptr(grads, torch.float32, "grads"), _ptr(delta, torch.float32, "delta"),
                            _ptr(m, torch.float32, "m"), ctypes.byref(coeffs)), ctx)
+
+
+def lmsgd_set_weight_decay(ctx: Context, lam: float, n_decay: int = -1):
+    _check(_lib.lmsgd_set_weight_decay(ctx.ptr, float(lam), int(n_decay)), ctx)
 
 
 def lmsgd_schedule_upload(ctx: Context, hyper: Hyper | None, cluster: Cluster, t_first: int, count: int):

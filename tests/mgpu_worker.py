@@ -31,10 +31,14 @@ C1 = schedule.Cluster(n_workers=2, b_local=32, n_train=64)
 C1_C = L.make_cluster(2, 32, 64)
 
 
-def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, tol=1e-6):
+def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, tol=1e-6, wd=0.0, n_wd=None):
     hyper = schedule.Hyper()
-    th_o, d_o, m_o = run.resync_step(th0, d0, m0, ghat, c, hyper)
+    th_o, d_o, m_o = run.resync_step(th0, d0, m0, ghat, c, hyper, wd, n_wd)
     gh = np.asarray(ghat, dtype=np.float64)
+    if wd:
+        gh = gh.copy()
+        k = gh.size if n_wd is None else n_wd
+        gh[:k] += wd * np.asarray(th0, np.float64)[:k]
     coef = c.alpha_sgd + c.alpha_rmsprop / (np.sqrt(m_o) + hyper.eps)
     scale_d = hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + np.abs(coef * gh)
     e = (run.scaled_error(m_g, m_o, m_o), run.scaled_error(d_g, d_o, scale_d),
@@ -78,6 +82,23 @@ def main():
             check_state(H(th), H(d), H(m), *prev, ex.ghat, schedule.coeffs_at(t, schedule.Hyper(), C1))
             replicas_identical(th, d, m)
         L.lmsgd_finalize(ctx)
+
+    # ---- weight decay on a prefix (R12), exchange + update across the ranks
+    n = 50_021
+    ctx = L.lmsgd_init(world, rank, local, n, S)
+    L.connect_process_group(ctx)
+    L.lmsgd_set_weight_decay(ctx, 1e-4, 30_000)
+    th0 = synth.theta0(n, None)
+    th, d, m = D(th0), D(np.zeros(n, np.float32)), D(np.zeros(n, np.float32))
+    g = synth.grads(world, 2, n)
+    L.lmsgd_step(ctx, th, D(g[rank]), d, m, L.lmsgd_schedule_at(None, C1_C, 2))
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == 0
+    z = np.zeros(n, np.float32)
+    check_state(H(th), H(d), H(m), th0, z, z, exchange.exchange(list(g), S).ghat,
+                schedule.coeffs_at(2, schedule.Hyper(), C1), wd=1e-4, n_wd=30_000)
+    replicas_identical(th, d, m)
+    L.lmsgd_finalize(ctx)
 
     # ---- ghat bit-exact (mu1 = 0, (a_SGD, a_RMS) = (1, 0) => Delta = -ghat), with saturation
     n = 200_003

@@ -36,9 +36,13 @@ def host(x):
     return x.cpu().numpy()
 
 
-def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, hyper=schedule.Hyper(), tol=TOL):
-    th_o, d_o, m_o = run.resync_step(th0, d0, m0, ghat, c, hyper)
+def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, hyper=schedule.Hyper(), tol=TOL, wd=0.0, n_wd=None):
+    th_o, d_o, m_o = run.resync_step(th0, d0, m0, ghat, c, hyper, wd, n_wd)
     gh = np.asarray(ghat, dtype=np.float64)
+    if wd:
+        gh = gh.copy()
+        k = gh.size if n_wd is None else n_wd
+        gh[:k] += wd * np.asarray(th0, np.float64)[:k]
     coef = c.alpha_sgd + c.alpha_rmsprop / (np.sqrt(m_o) + hyper.eps)
     scale_d = hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + np.abs(coef * gh)
     e = {
@@ -469,4 +473,23 @@ def test_graph_step_matches_host_step_and_replays(flags):
     with pytest.raises(L.LmsgdError) as e:                    # no mixing at world 1
         L.lmsgd_step(ctx, th, gbuf, d, m, L.make_coeffs(0.1, 1.0, 0.0))
     assert e.value.status == L.LMSGD_ERR_STATE
+    L.lmsgd_finalize(ctx)
+
+
+@pytest.mark.parametrize("flags", [0, L.LMSGD_FLAG_NO_SKIP])
+def test_weight_decay_prefix(flags):
+    """R12: weight decay on the first n_decay elements (PAPER.md:52-53 via Goyal)."""
+    n, s, lam, nd = 100_003, 1024.0, 1e-4, 60_001
+    th0, d0, m0 = init_state(n)
+    ctx = L.lmsgd_init(1, 0, 0, n, s, None, flags)
+    L.lmsgd_set_weight_decay(ctx, lam, nd)
+    th, d, m = dev(th0), dev(d0), dev(m0)
+    for t in (1, 15):
+        g = synth.grads(1, t, n)
+        prev = host(th), host(d), host(m)
+        L.lmsgd_step(ctx, th, dev(g[0]), d, m, L.lmsgd_schedule_at(None, C1_C, t))
+        check_state(host(th), host(d), host(m), *prev, exchange.exchange(list(g), s).ghat,
+                    schedule.coeffs_at(t, schedule.Hyper(), C1), wd=lam, n_wd=nd)
+    with pytest.raises(L.LmsgdError):
+        L.lmsgd_set_weight_decay(ctx, -1.0)
     L.lmsgd_finalize(ctx)

@@ -124,3 +124,25 @@ def test_inputs_not_modified():
     th = np.ones(4); g = np.ones(4); m = np.ones(4); d = np.ones(4)
     upd.step(th, g, m, d, 0.1, 0.5, 0.5)
     assert th.tolist() == g.tolist() == m.tolist() == d.tolist() == [1.0] * 4
+
+
+def test_weight_decay_is_torch_weight_decay():
+    """R12 (Goyal's settings): g + lambda theta before the m update --
+    torch.optim.SGD / RMSprop(weight_decay=lambda) at the two endpoints."""
+    theta = np.random.default_rng(11).standard_normal(500)
+    grads, etas = _grads(500, 40, 12), _etas(40)
+    lam = 1e-4
+    for (a_sgd, a_rms), fac in (((1.0, 0.0), lambda ps: torch.optim.SGD(ps, lr=0.1, momentum=0.9, weight_decay=lam)),
+                                ((0.0, 1.0), lambda ps: torch.optim.RMSprop(ps, lr=0.1, alpha=0.99, eps=1e-8,
+                                                                           momentum=0.9, weight_decay=lam))):
+        th, d, m = theta.copy(), np.zeros(500), np.zeros(500)
+        for g, eta in zip(grads, etas):
+            th, d, m = upd.step(th, g, m, d, eta, a_sgd, a_rms, weight_decay=lam)
+        ref, _ = _torch_run(fac, theta, grads, etas)
+        assert np.max(np.abs(th - ref)) <= 1e-12
+
+
+def test_weight_decay_prefix_only():
+    th = np.ones(10)
+    a = upd.step(th, np.zeros(10), np.zeros(10), np.zeros(10), 1.0, 1.0, 0.0, weight_decay=0.5, n_decay=4)
+    assert np.array_equal(a[1][:4], np.full(4, -0.5)) and not a[1][4:].any()
