@@ -24,6 +24,7 @@ struct lmsgd_ctx {
     lmsgd_hyper hyper{};
     double wd = 0.0;                  // lmsgd_set_weight_decay (R12)
     int64_t n_wd = 0;
+    int64_t ctab_n_wd = 0;   // n_wd the uploaded table was built with (selects the kernel variant)
     uint32_t flags = 0;
     Layout lay{};
     char* buf = nullptr;           // own exchange buffer (IPC-shared when world > 1)
@@ -426,6 +427,7 @@ lmsgd_status lmsgd_schedule_upload(lmsgd_ctx* c, const lmsgd_hyper* hyper, const
     CK(c, cudaMemcpy(c->d_ctab, tab.data(), count * sizeof(UpdConst), cudaMemcpyHostToDevice));
     CK(c, cudaMemset(&c->dstate->cursor, 0, sizeof(int64_t)));
     c->ctab_count = count;
+    c->ctab_n_wd = tab[0].n_wd;
     return LMSGD_OK;
 }
 
@@ -439,7 +441,8 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
     if (c->mode == 1) return fail(c, LMSGD_ERR_STATE, "this context already runs lmsgd_step");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const UpdConst u{};   // every coefficient comes from the device table
+    UpdConst u{};         // every coefficient comes from the device table; n_wd selects the kernel variant
+    u.n_wd = c->ctab_n_wd;
     c->last_stream = s;
     ++c->step;            // host-side count only (the kernels use the device counter)
     c->mode = 2;

@@ -139,8 +139,10 @@ __device__ __forceinline__ void upd1(float gh, float& th, float& d, float& m, co
     m = m1;
 }
 
-// Update 8 consecutive elements from j0 given their 8 fp16 wire values.
-template <bool RMS>
+// Update 8 consecutive elements from j0 given their 8 fp16 wire values.  WD: the
+// weight-decay variant (R12, g += lambda theta on [0, n_wd)); a separate
+// instantiation so the default path carries no per-element test.
+template <bool RMS, bool WD>
 __device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const UpdConst& c,
                                         float* __restrict__ th, float* __restrict__ d,
                                         float* __restrict__ m) {
@@ -158,7 +160,7 @@ __device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const Up
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
-            if (j0 + i < c.n_wd) gh = fmaf(c.wd, tv[i], gh);   // R12 weight decay (wd = 0: exact no-op)
+            if (WD && j0 + i < c.n_wd) gh = fmaf(c.wd, tv[i], gh);
             upd1<RMS>(gh, tv[i], dv[i], mv[i], c);
         }
         __stcs(th4, make_float4(tv[0], tv[1], tv[2], tv[3]));
@@ -171,7 +173,7 @@ __device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const Up
         for (int i = 0; i < 8 && j0 + i < n; ++i) {
             float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
             float t = th[j0 + i], dd = d[j0 + i], mm = m[j0 + i];
-            if (j0 + i < c.n_wd) gh = fmaf(c.wd, t, gh);
+            if (WD && j0 + i < c.n_wd) gh = fmaf(c.wd, t, gh);
             upd1<RMS>(gh, t, dd, mm, c);
             th[j0 + i] = t; d[j0 + i] = dd; m[j0 + i] = mm;
         }
@@ -260,7 +262,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_local(const uint16_t* __res
     if (st) flush_status(kNone, sat, st, ST_SUM_SAT);
 }
 
-template <bool RMS>
+template <bool RMS, bool WD>
 __global__ void __launch_bounds__(kThreads) k_update(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
                                                      float* __restrict__ th, float* __restrict__ d,
                                                      float* __restrict__ m, const int64_t* st,
@@ -287,13 +289,13 @@ __global__ void __launch_bounds__(kThreads) k_update(const uint16_t* __restrict_
     for (int64_t v = gtid(); v < nv; v += gstride()) {
         const int64_t j0 = v << 3;
         const uint4 r = *reinterpret_cast<const uint4*>(R + j0);
-        update8<RMS>(r, j0, n, c, th, d, m);
+        update8<RMS, WD>(r, j0, n, c, th, d, m);
     }
 }
 
 // k = 1 single pass (LMSGD_FLAG_NO_SKIP): h = sat16(s g) kept in registers,
 // ghat = fp32(h) / s, update.  28 B/elem of HBM traffic.
-template <bool RMS>
+template <bool RMS, bool WD>
 __global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g, int64_t n, float s,
                                                      UpdConst c, float* __restrict__ th,
                                                      float* __restrict__ d, float* __restrict__ m,
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g
         float x[8];
         load8_g(g, j0, n, x);
         const uint4 r = pack8(x, s, j0, first, sat);
-        update8<RMS>(r, j0, n, c, th, d, m);
+        update8<RMS, WD>(r, j0, n, c, th, d, m);
     }
     flush_status(first, sat, st, ST_PACK_SAT);
 }
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
     if (t0) atomicAdd(a.ctr + 1, 1u);   // k_xfinalize waits for every block of this grid
 }
 
-template <bool RMS>
+template <bool RMS, bool WD>
 __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
     // no griddepcontrol.wait: ordering with k_xstep1 is by flags D and cflag.
     // kXUnits units per block: 2 was faster in isolation (tools/xbench.cu, 109 vs
@@ -640,7 +642,7 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
         const int64_t j0 = ((int64_t)owner[v] * gsh + gi) << 3;
         if (j0 >= x.n) continue;
         const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner[v]] + x.lay.off_R) + (gi << 3);
-        update8<RMS>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, c, a.th, a.d, a.m);
+        update8<RMS, WD>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, c, a.th, a.d, a.m);
     }
 }
 
@@ -779,10 +781,10 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
     (void)gsh;
     const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits);
     const bool pdl = (L.pdl_mask & 4) == 0;   // bit 4 (diagnostics): launch k_xupdate after k_xstep1 completes
-    if (a.c.a_rms != 0.0f || a.ctab)
-        e = launch_pdl_if(pdl, k_xupdate<true>, grid, kThreads, s, a);
-    else
-        e = launch_pdl_if(pdl, k_xupdate<false>, grid, kThreads, s, a);
+    const bool rms = a.c.a_rms != 0.0f || a.ctab, wd = a.c.n_wd > 0;
+    auto* kern = rms ? (wd ? k_xupdate<true, true> : k_xupdate<true, false>)
+                     : (wd ? k_xupdate<false, true> : k_xupdate<false, false>);
+    e = launch_pdl_if(pdl, kern, grid, kThreads, s, a);
     if (e != cudaSuccess) return e;
     return launch_pdl_if(true, k_xfinalize, 1, 32, s, a, (unsigned int)L.grid_xstep);
 }
@@ -790,9 +792,9 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
 
 int stream_blocks_per_sm() {
     int worst = 1 << 30, b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update<true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update<true, false>, kThreads, 0);
     worst = b < worst ? b : worst;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true>, kThreads, 0);  // NOLINT
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true, false>, kThreads, 0);  // NOLINT
     worst = b < worst ? b : worst;
     return worst > 0 ? worst : 1;
 }
@@ -816,20 +818,21 @@ cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, in
                           const UpdConst& c, float* th, float* d, float* m, const int64_t* st,
                           int64_t* st_reset, int64_t* last, const Dev1& dv) {
     const int grid = grid_for(L, (n + 7) >> 3);
-    if (c.a_rms != 0.0f || dv.epoch)   // graph mode: alpha_RMSprop is only known on the device
-        return launch_pdl(k_update<true>, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last, dv);
-    else
-        return launch_pdl(k_update<false>, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last, dv);
+    // graph mode: alpha_RMSprop is only known on the device; c.n_wd > 0 selects the decay variant
+    const bool rms = c.a_rms != 0.0f || dv.epoch, wd = c.n_wd > 0;
+    auto* kern = rms ? (wd ? k_update<true, true> : k_update<true, false>)
+                     : (wd ? k_update<false, true> : k_update<false, false>);
+    return launch_pdl(kern, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last, dv);
 }
 
 cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                           const UpdConst& c, float* th, float* d, float* m, int64_t* st,
                           int64_t* st_reset, int64_t* /*last: see launch_finalize_fused*/, const Dev1& dv) {
     const int grid = grid_for(L, (n + 7) >> 3);
-    if (c.a_rms != 0.0f || dv.epoch)
-        return launch_pdl(k_fused1<true>, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset, dv);
-    else
-        return launch_pdl(k_fused1<false>, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset, dv);
+    const bool rms = c.a_rms != 0.0f || dv.epoch, wd = c.n_wd > 0;
+    auto* kern = rms ? (wd ? k_fused1<true, true> : k_fused1<true, false>)
+                     : (wd ? k_fused1<false, true> : k_fused1<false, false>);
+    return launch_pdl(kern, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset, dv);
 }
 
 int64_t host_units(const XArgs& x) {

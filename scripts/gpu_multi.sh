@@ -3,6 +3,7 @@
 # fused) and at N = all GPUs (traced), plus the ResNet-152 buffer (config C5 sizes).
 cd $GRAFT_REPO_ROOT
 mkdir -p gpurun_out
+python paper_1711_04325_b200/build.py > gpurun_out/build.log 2>&1   # no-op unless a source is newer than the .so
 N=$(nvidia-smi -L | wc -l)
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log

@@ -34,14 +34,16 @@ C1_C = L.make_cluster(2, 32, 64)
 def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, tol=1e-6, wd=0.0, n_wd=None):
     hyper = schedule.Hyper()
     th_o, d_o, m_o = run.resync_step(th0, d0, m0, ghat, c, hyper, wd, n_wd)
-    gh = np.asarray(ghat, dtype=np.float64)
+    # |g| + |lambda theta|: the fp32 g + lambda theta is exact to that scale, not to
+    # the (possibly cancelled) sum (R12)
+    gh = np.abs(np.asarray(ghat, dtype=np.float64))
     if wd:
-        gh = gh.copy()
         k = gh.size if n_wd is None else n_wd
-        gh[:k] += wd * np.asarray(th0, np.float64)[:k]
+        gh[:k] += wd * np.abs(np.asarray(th0, np.float64)[:k])
     coef = c.alpha_sgd + c.alpha_rmsprop / (np.sqrt(m_o) + hyper.eps)
-    scale_d = hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + np.abs(coef * gh)
-    e = (run.scaled_error(m_g, m_o, m_o), run.scaled_error(d_g, d_o, scale_d),
+    scale_d = hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + coef * gh
+    scale_m = m_o + (1.0 - hyper.mu2) * gh * gh
+    e = (run.scaled_error(m_g, m_o, scale_m), run.scaled_error(d_g, d_o, scale_d),
          run.scaled_error(th_g, th_o, np.abs(np.asarray(th0, np.float64)) + c.eta * scale_d))
     assert max(e) <= tol, e
 

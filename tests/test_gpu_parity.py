@@ -4,7 +4,7 @@ Bar (BASELINE.json north_star):
   * fp16 wire payloads R and the averaged gradient ghat: bit-exact (the sum is exact);
   * schedule: bit-exact (tests/test_lib_host.py);
   * fp32 state after one step, oracle resynced to the GPU's previous state:
-    |x_gpu - x_oracle| <= 1e-6 * scale_x with scale_m = m_t,
+    |x_gpu - x_oracle| <= 1e-6 * scale_x with scale_m = m_t + (1-mu2) |ghat|^2,
     scale_Delta = mu1 |Delta_{t-1}| + |c ghat|, scale_theta = |theta_{t-1}| + eta scale_Delta;
   * status words (first non-finite index, saturation counts): exact.
 """
@@ -38,15 +38,17 @@ def host(x):
 
 def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, hyper=schedule.Hyper(), tol=TOL, wd=0.0, n_wd=None):
     th_o, d_o, m_o = run.resync_step(th0, d0, m0, ghat, c, hyper, wd, n_wd)
-    gh = np.asarray(ghat, dtype=np.float64)
+    # |g| + |lambda theta|: the fp32 g + lambda theta is exact to that scale, not to
+    # the (possibly cancelled) sum (R12)
+    gh = np.abs(np.asarray(ghat, dtype=np.float64))
     if wd:
-        gh = gh.copy()
         k = gh.size if n_wd is None else n_wd
-        gh[:k] += wd * np.asarray(th0, np.float64)[:k]
+        gh[:k] += wd * np.abs(np.asarray(th0, np.float64)[:k])
     coef = c.alpha_sgd + c.alpha_rmsprop / (np.sqrt(m_o) + hyper.eps)
-    scale_d = hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + np.abs(coef * gh)
+    scale_d = hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + coef * gh
+    scale_m = m_o + (1.0 - hyper.mu2) * gh * gh
     e = {
-        "m": run.scaled_error(m_g, m_o, m_o),
+        "m": run.scaled_error(m_g, m_o, scale_m),
         "delta": run.scaled_error(d_g, d_o, scale_d),
         # Delta's own rounding (relative to scale_d) propagates through eta: DESIGN.md "Tolerances"
         "theta": run.scaled_error(th_g, th_o, np.abs(np.asarray(th0, np.float64)) + c.eta * scale_d),
@@ -493,3 +495,24 @@ def test_weight_decay_prefix(flags):
     with pytest.raises(L.LmsgdError):
         L.lmsgd_set_weight_decay(ctx, -1.0)
     L.lmsgd_finalize(ctx)
+    # graph mode: the uploaded table carries lambda (and selects the decay kernel)
+    gctx = L.lmsgd_init(1, 0, 0, n, s, None, flags)
+    L.lmsgd_set_weight_decay(gctx, lam, nd)
+    L.lmsgd_schedule_upload(gctx, None, C1_C, 1, 1)
+    gt, gd, gm = dev(th0), dev(d0), dev(m0)
+    hctx = L.lmsgd_init(1, 0, 0, n, s, None, flags)
+    L.lmsgd_set_weight_decay(hctx, lam, nd)
+    ht, hd, hm = dev(th0), dev(d0), dev(m0)
+    g1 = dev(synth.grads(1, 1, n)[0])
+    L.lmsgd_step_graph(gctx, gt, g1, gd, gm)
+    L.lmsgd_step(hctx, ht, g1, hd, hm, L.lmsgd_schedule_at(None, C1_C, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(gt, ht) and torch.equal(gd, hd) and torch.equal(gm, hm)
+    octx = L.lmsgd_init(1, 0, 0, n, s, None, flags)      # no decay: same suffix, other prefix
+    ot, od, om = dev(th0), dev(d0), dev(m0)
+    L.lmsgd_step(octx, ot, g1, od, om, L.lmsgd_schedule_at(None, C1_C, 1))
+    torch.cuda.synchronize()
+    assert torch.equal(gm[nd:], om[nd:]) and not torch.equal(gm[:nd], om[:nd])
+    L.lmsgd_finalize(octx)
+    L.lmsgd_finalize(gctx)
+    L.lmsgd_finalize(hctx)

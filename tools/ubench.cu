@@ -242,7 +242,7 @@ int main(int argc, char** argv) {
     struct V { const char* name; std::function<void()> f; };
     const int gridc = L.grid_cap_stream;
     std::vector<V> vs = {
-        {"V0 update (prod)", [&] { k_update<true><<<gridc, kThreads>>>(h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); }},
+        {"V0 update (prod)", [&] { k_update<true, false><<<gridc, kThreads>>>(h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); }},
         {"V1 update unroll2", [&] { k_update_u2<true><<<gridc, kThreads>>>(h, n, c, th, d, m); }},
         {"V2 update flat", [&] { k_update_flat<true><<<(int)(((n >> 3) + kThreads - 1) / kThreads), kThreads>>>(h, n, c, th, d, m); }},
         {"V7 update flat bs512", [&] { k_update_flat_bs<512><<<(int)(((n >> 3) + 511) / 512), 512>>>(h, n, c, th, d, m); }},
