@@ -73,11 +73,20 @@ typedef struct lmsgd_hyper {
  * (PAPER.md:217-221).  Independent of the physical world size k: the paper's
  * 32k run is n_workers = 1024, b_local = 32.  n_train = images per epoch (the
  * paper does not print it; ImageNet-1k = 1,281,167, R5).
- * schedule: 0 = slow-start, 1 = Goyal et al.. */
+ * schedule: 0 = slow-start, 1 = Goyal et al..
+ * transition: the alpha_SGD warm-up function:
+ *   LMSGD_TRANSITION_ELU (0, the paper's, reading R1), and the alternatives the paper
+ *   examined without printing them (reading R20, each 1/2 at beta_center with slope
+ *   1/beta_period there): LINEAR clamp(1/2 + (e - bc)/bp, 0, 1), SIGMOID
+ *   1/(1 + exp(-4 (e - bc)/bp)), SUDDEN 0 below bc, 1 from bc on. */
+#define LMSGD_TRANSITION_ELU 0
+#define LMSGD_TRANSITION_LINEAR 1
+#define LMSGD_TRANSITION_SIGMOID 2
+#define LMSGD_TRANSITION_SUDDEN 3
 typedef struct lmsgd_cluster {
     int64_t n_workers, b_local, n_train;
     int32_t schedule;
-    int32_t reserved;
+    int32_t transition;
 } lmsgd_cluster;
 
 /* Per-step coefficients.  lmsgd_schedule_at is the canonical source; a caller may

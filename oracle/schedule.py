@@ -10,7 +10,9 @@ multipliers 0.5 / 0.075 / 0.01 / 0.001 for 40 / 30 / 15 / 5 epochs; Goyal et al.
 Readings: R1 linear-branch slope 1/beta_period (the displayed "2" at
 PAPER.md:180 contradicts PAPER.md:186-188); R2 fractional epoch per iteration;
 R3 step t uses epoch (t-1) b_total / N_train; R4 right-open phase boundaries tested
-with integers; R5 N_train = 1,281,167.
+with integers; R5 N_train = 1,281,167.  R20: the other transition
+functions the paper examined -- linear, sigmoid and a sudden switch
+-- are not written out in the paper; R20 fixes them (below, alpha_sgd_at).
 
 All arithmetic is IEEE double in the operation order written below (the C++ host
 schedule is checked bit-exact against these doubles).
@@ -48,6 +50,7 @@ class Cluster:
     b_local: int = 32
     n_train: int = N_TRAIN_IMAGENET
     schedule: str = "slow_start"
+    transition: str = "elu"      # R20: "elu" (the paper's), "linear", "sigmoid", "sudden"
 
     @property
     def b_total(self) -> int:
@@ -73,21 +76,35 @@ def eta_base(n_workers: int, b_local: int) -> float:
     return 0.1 * b_total / 256
 
 
-def alpha_sgd_at(epoch: float, beta_center: float = 10.0, beta_period: float = 5.0) -> float:
+def alpha_sgd_at(epoch: float, beta_center: float = 10.0, beta_period: float = 5.0,
+                 transition: str = "elu") -> float:
     """PAPER.md:178-182 with reading R1 (slope 1/beta_period on the linear branch):
         1/2 exp(2 (epoch - beta_c) / beta_p)      epoch < beta_c
         1/2 + (epoch - beta_c) / beta_p             epoch < beta_c + beta_p / 2
         1                                           otherwise
+    Reading R20, the alternatives PAPER.md:205-210 names without formulas, each
+    through 1/2 at beta_c with the ELU's slope 1/beta_p there:
+        linear   min(max(1/2 + (epoch - beta_c) / beta_p, 0), 1)
+        sigmoid  1 / (1 + exp(-4 (epoch - beta_c) / beta_p))
+        sudden   0 if epoch < beta_c else 1       (Wu et al.'s switch)
     """
     if beta_period <= 0:
         raise ValueError("beta_period must be > 0")
     if epoch < 0:
         raise ValueError("epoch must be >= 0")
-    if epoch < beta_center:
-        return 0.5 * math.exp(2.0 * (epoch - beta_center) / beta_period)
-    if epoch < beta_center + 0.5 * beta_period:
-        return 0.5 + (epoch - beta_center) / beta_period
-    return 1.0
+    if transition == "elu":
+        if epoch < beta_center:
+            return 0.5 * math.exp(2.0 * (epoch - beta_center) / beta_period)
+        if epoch < beta_center + 0.5 * beta_period:
+            return 0.5 + (epoch - beta_center) / beta_period
+        return 1.0
+    if transition == "linear":
+        return min(max(0.5 + (epoch - beta_center) / beta_period, 0.0), 1.0)
+    if transition == "sigmoid":
+        return 1.0 / (1.0 + math.exp(-4.0 * (epoch - beta_center) / beta_period))
+    if transition == "sudden":
+        return 0.0 if epoch < beta_center else 1.0
+    raise ValueError(f"unknown transition {transition!r}")
 
 
 def phase_at(t: int, cl: Cluster) -> int:
@@ -121,7 +138,7 @@ def coeffs_at(t: int, hyper: Hyper = Hyper(), cl: Cluster = Cluster()) -> Coeffs
     eta = SCHEDULES[cl.schedule][p][1] * eta_base(cl.n_workers, cl.b_local)
     if not eta > 0:
         raise ValueError("eta must be > 0")
-    a_sgd = alpha_sgd_at(epoch, hyper.beta_center, hyper.beta_period)
+    a_sgd = alpha_sgd_at(epoch, hyper.beta_center, hyper.beta_period, cl.transition)
     a_rms = ((1.0 - a_sgd) * hyper.eta_rmsprop) / eta
     return Coeffs(epoch, eta, a_sgd, a_rms, p)
 

@@ -33,14 +33,24 @@ bool cluster_ok(const lmsgd_cluster* c) {
     // keep (t-1) * b_total and 90 * n_train well inside int64 and exact in double
     return c && c->n_workers > 0 && c->b_local > 0 && c->n_train > 0 &&
            c->n_workers <= (int64_t(1) << 24) && c->b_local <= (int64_t(1) << 24) &&
-           c->n_train <= (int64_t(1) << 40) && phases_of(c->schedule) != nullptr;
+           c->n_train <= (int64_t(1) << 40) && phases_of(c->schedule) != nullptr &&
+           c->transition >= LMSGD_TRANSITION_ELU && c->transition <= LMSGD_TRANSITION_SUDDEN;
 }
 
-// PAPER.md:178-182 with R1.
-double alpha_sgd(double epoch, double bc, double bp) {
-    if (epoch < bc) return 0.5 * std::exp(2.0 * (epoch - bc) / bp);
-    if (epoch < bc + 0.5 * bp) return 0.5 + (epoch - bc) / bp;
-    return 1.0;
+// PAPER.md:178-182 with R1; the alternatives of PAPER.md:205-210 with R20.
+double alpha_sgd(double epoch, double bc, double bp, int32_t transition) {
+    switch (transition) {
+    case LMSGD_TRANSITION_LINEAR:
+        return std::fmin(std::fmax(0.5 + (epoch - bc) / bp, 0.0), 1.0);
+    case LMSGD_TRANSITION_SIGMOID:
+        return 1.0 / (1.0 + std::exp(-4.0 * (epoch - bc) / bp));
+    case LMSGD_TRANSITION_SUDDEN:
+        return epoch < bc ? 0.0 : 1.0;
+    default:
+        if (epoch < bc) return 0.5 * std::exp(2.0 * (epoch - bc) / bp);
+        if (epoch < bc + 0.5 * bp) return 0.5 + (epoch - bc) / bp;
+        return 1.0;
+    }
 }
 
 }  // namespace
@@ -80,7 +90,7 @@ extern "C" lmsgd_status lmsgd_schedule_at(const lmsgd_hyper* h, const lmsgd_clus
     const double eta_base = 0.1 * static_cast<double>(b_total) / 256.0;
     const double eta = ph[p].mult * eta_base;
     if (!(eta > 0.0)) return LMSGD_ERR_INVALID_ARG;
-    const double a = alpha_sgd(epoch, h->beta_center, h->beta_period);
+    const double a = alpha_sgd(epoch, h->beta_center, h->beta_period, c->transition);
     out->epoch = epoch;
     out->eta = eta;
     out->alpha_sgd = a;

@@ -28,6 +28,7 @@ LMSGD_MAX_BN_CHANNELS = 1 << 20
 LMSGD_FLAG_NO_SKIP = 0x1
 SCHEDULE_SLOW_START = 0
 SCHEDULE_GOYAL = 1
+TRANSITION_ELU, TRANSITION_LINEAR, TRANSITION_SIGMOID, TRANSITION_SUDDEN = 0, 1, 2, 3   # R20
 
 
 class Hyper(ctypes.Structure):
@@ -38,7 +39,7 @@ class Hyper(ctypes.Structure):
 
 class Cluster(ctypes.Structure):
     _fields_ = [("n_workers", ctypes.c_int64), ("b_local", ctypes.c_int64), ("n_train", ctypes.c_int64),
-                ("schedule", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("schedule", ctypes.c_int32), ("transition", ctypes.c_int32)]
 
 
 class Coeffs(ctypes.Structure):
@@ -124,8 +125,9 @@ def lmsgd_hyper_default() -> Hyper:
     return h
 
 
-def make_cluster(n_workers=1024, b_local=32, n_train=1_281_167, schedule=SCHEDULE_SLOW_START) -> Cluster:
-    return Cluster(n_workers, b_local, n_train, schedule, 0)
+def make_cluster(n_workers=1024, b_local=32, n_train=1_281_167, schedule=SCHEDULE_SLOW_START,
+                 transition=TRANSITION_ELU) -> Cluster:
+    return Cluster(n_workers, b_local, n_train, schedule, transition)
 
 
 def lmsgd_schedule_at(hyper: Hyper | None, cluster: Cluster, t: int) -> Coeffs:

@@ -58,11 +58,17 @@ def _f32(x):
     dict(n_workers=2, b_local=32, n_train=64, schedule="slow_start"),
     dict(n_workers=8, b_local=32, n_train=1_281_167, schedule="slow_start"),
     dict(n_workers=1000, b_local=7, n_train=999_983, schedule="slow_start"),
+    dict(n_workers=1024, b_local=32, n_train=1_281_167, schedule="slow_start", transition="linear"),
+    dict(n_workers=1024, b_local=32, n_train=1_281_167, schedule="slow_start", transition="sigmoid"),
+    dict(n_workers=1024, b_local=32, n_train=1_281_167, schedule="goyal", transition="sudden"),
+    dict(n_workers=2, b_local=32, n_train=64, schedule="slow_start", transition="sigmoid"),
+    dict(n_workers=2, b_local=32, n_train=64, schedule="slow_start", transition="linear"),
 ])
 def test_schedule_bit_exact_vs_oracle(cfg):
     ocl = sch.Cluster(**cfg)
+    tr = {"elu": 0, "linear": 1, "sigmoid": 2, "sudden": 3}[cfg.get("transition", "elu")]
     ccl = L.make_cluster(cfg["n_workers"], cfg["b_local"], cfg["n_train"],
-                         0 if cfg["schedule"] == "slow_start" else 1)
+                         0 if cfg["schedule"] == "slow_start" else 1, tr)
     T = sch.n_steps(ocl)
     assert L.lmsgd_schedule_steps(ccl) == T
     step = max(1, T // 4000)
@@ -106,7 +112,8 @@ def test_schedule_arg_errors():
         with pytest.raises(L.LmsgdError) as e:
             L.lmsgd_schedule_at(None, cl, bad_t)
         assert e.value.status == L.LMSGD_ERR_INVALID_ARG
-    for bad in (L.make_cluster(0, 32), L.make_cluster(8, 0), L.make_cluster(8, 32, 0), L.make_cluster(schedule=7)):
+    for bad in (L.make_cluster(0, 32), L.make_cluster(8, 0), L.make_cluster(8, 32, 0), L.make_cluster(schedule=7),
+                L.make_cluster(transition=4), L.make_cluster(transition=-1)):
         with pytest.raises(L.LmsgdError):
             L.lmsgd_schedule_at(None, bad, 1)
     h = L.lmsgd_hyper_default()

@@ -139,3 +139,44 @@ def test_operation_order_of_alpha_rmsprop():
     for t in range(1, 21):
         c = sch.coeffs_at(t, sch.Hyper(), cl)
         assert c.alpha_rmsprop == ((1.0 - c.alpha_sgd) * 0.0003) / c.eta
+
+
+# ---- R20: the transition functions PAPER.md:205-210 names (f3) -------------------
+
+@pytest.mark.parametrize("tr", ["elu", "linear", "sigmoid"])
+def test_transition_half_at_center_with_elu_slope(tr):
+    """Each smooth variant passes 1/2 at beta_center with the ELU's
+    slope there, 1/beta_p (the exp branch's derivative, reading R1)."""
+    for bc, bp in ((10.0, 5.0), (3.0, 2.0)):
+        assert sch.alpha_sgd_at(bc, bc, bp, tr) == 0.5
+        h = 1e-6
+        slope = (sch.alpha_sgd_at(bc + h, bc, bp, tr) - sch.alpha_sgd_at(bc - h, bc, bp, tr)) / (2 * h)
+        assert slope == pytest.approx(1.0 / bp, rel=1e-6)
+
+
+def test_transition_closed_forms():
+    # sigmoid: 1 / (1 + e^{-4 (e - 10) / 5}); at e = 15: 1/(1+e^-4), at e = 0: 1/(1+e^8)
+    assert sch.alpha_sgd_at(15.0, transition="sigmoid") == pytest.approx(0.9820137900379085, rel=1e-15)
+    assert sch.alpha_sgd_at(0.0, transition="sigmoid") == pytest.approx(3.353501304664781e-4, rel=1e-14)
+    # linear: 0 up to beta_c - beta_p/2 = 7.5, 3/4 at 11.25, 1 from 12.5 on
+    assert [sch.alpha_sgd_at(e, transition="linear") for e in (0.0, 7.5, 8.75, 11.25, 12.5, 80.0)] == \
+           [0.0, 0.0, 0.25, 0.75, 1.0, 1.0]
+    # sudden switch (Wu et al., PAPER.md:203-204) at beta_center
+    assert [sch.alpha_sgd_at(e, transition="sudden") for e in (0.0, 9.999999, 10.0, 50.0)] == [0.0, 0.0, 1.0, 1.0]
+    with pytest.raises(ValueError):
+        sch.alpha_sgd_at(1.0, transition="cosine")
+
+
+@pytest.mark.parametrize("tr", ["elu", "linear", "sigmoid", "sudden"])
+def test_transition_monotone_bounded_and_rms_closed_form(tr):
+    cl = sch.Cluster(transition=tr)
+    prev = -1.0
+    for t in range(1, sch.n_steps(cl) + 1, 5):
+        c = sch.coeffs_at(t, sch.Hyper(), cl)
+        assert 0.0 <= c.alpha_sgd <= 1.0 and c.alpha_sgd >= prev
+        prev = c.alpha_sgd
+        assert c.alpha_rmsprop == ((1.0 - c.alpha_sgd) * 3e-4) / c.eta
+    # sudden at 32k: pure RMSprop (alpha_RMS = eta_R / eta) until t = 392, then SGD
+    if tr == "sudden":
+        assert sch.coeffs_at(391, sch.Hyper(), cl).alpha_rmsprop == 3e-4 / 6.4
+        assert sch.coeffs_at(392, sch.Hyper(), cl).alpha_rmsprop == 0.0
