@@ -500,6 +500,40 @@ def main():
         L.lmsgd_finalize(ctxf)
         del thf, df, mf
 
+    # SGD phase (alpha_RMSprop = 0, t >= 490 at 32k: 86% of the 3,519 steps), with and
+    # without LMSGD_FLAG_FREEZE_M (m not touched: 18 instead of 26 B/elem in the update)
+    if not args.no_profile and not args.full_schedule:
+        variants = variants or {}
+        t_sgd = 1000
+        csgd = [L.lmsgd_schedule_at(None, cl, t_sgd + i) for i in range(args.warmup + args.steps)]
+        for name, vflags in (("sgd_phase", flags), ("sgd_phase_freeze_m", flags | L.LMSGD_FLAG_FREEZE_M)):
+            ctxv = L.lmsgd_init(world, rank, local, n, LOSS_SCALE, None, vflags)
+            L.connect_process_group(ctxv)
+            thv, dv_, mv = theta.clone(), delta.clone(), m.clone()
+            pv = (P(thv.data_ptr()), P(grads.data_ptr()), P(dv_.data_ptr()), P(mv.data_ptr()))
+            for i in range(args.warmup):
+                lib.lmsgd_step(ctxv.ptr, sp, *pv, ctypes.byref(csgd[i]))
+            torch.cuda.synchronize()
+            barrier()
+            torch.cuda.synchronize()
+            e0.record(stream)
+            for i in range(args.steps):
+                lib.lmsgd_step(ctxv.ptr, sp, *pv, ctypes.byref(csgd[args.warmup + i]))
+            e1.record(stream)
+            torch.cuda.synchronize()
+            barrier()
+            vms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+            codev, _ = L.lmsgd_query_status(ctxv)
+            assert codev == 0
+            variants[name] = {"ms_per_step": vms, "value": world * 1e3 / vms, "unit": UNIT, "t_from": t_sgd,
+                              "note": ("alpha_RMSprop = 0: the SGD instantiation of the same step"
+                                       if name == "sgd_phase" else
+                                       "LMSGD_FLAG_FREEZE_M: theta and Delta bit-identical to the full rule, "
+                                       "m left at its last RMSprop-phase value (not the paper's m_t)")}
+            barrier()
+            L.lmsgd_finalize(ctxv)
+            del thv, dv_, mv
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         rate, ns, calls, el = oracle_rate(1, n, 15.0)

@@ -116,6 +116,12 @@ typedef struct lmsgd_ctx lmsgd_ctx;   /* opaque, library-owned */
                                      gradients are detected and reported but NOT skipped.
                                      Ignored for world > 1, where the skip decision is free
                                      (the reduce needs every rank's payload anyway). */
+#define LMSGD_FLAG_FREEZE_M 0x2u  /* lmsgd_step only: on steps with alpha_rmsprop == 0 (SGD after the
+                                     warm-up) m is neither read nor written -- it
+                                     does not enter Delta or theta then, so theta and Delta are
+                                     bit-identical to the full rule while the update moves 18 instead
+                                     of 26 B/elem.  m then holds its value from the last RMSprop step
+                                     (NOT the paper's m_t); off by default.  lmsgd_step_graph ignores it. */
 
 /* ---------------------------------------------------------------- host-only */
 

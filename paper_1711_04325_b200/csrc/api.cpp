@@ -258,7 +258,7 @@ lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_
     lmsgd_hyper h{};
     if (hyper) h = *hyper; else lmsgd_hyper_default(&h);
     if (!hyper_ok(&h)) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "hyperparameters out of range");
-    if (flags & ~LMSGD_FLAG_NO_SKIP) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "unknown flags");
+    if (flags & ~(LMSGD_FLAG_NO_SKIP | LMSGD_FLAG_FREEZE_M)) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "unknown flags");
 
     int ndev = 0;
     cudaError_t e = cudaGetDeviceCount(&ndev);
@@ -364,7 +364,8 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     if (c->mode == 2) return fail(c, LMSGD_ERR_STATE, "this context already runs lmsgd_step_graph");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    const UpdConst u = make_const(c->hyper, *coeffs, c->world, c->scale, c->wd, c->n_wd);
+    UpdConst u = make_const(c->hyper, *coeffs, c->world, c->scale, c->wd, c->n_wd);
+    u.freeze_m = (c->flags & LMSGD_FLAG_FREEZE_M) && u.a_rms == 0.0f;
     const uint32_t epoch = ++c->step;
     const int parity = static_cast<int>(epoch & 1u);
     c->last_stream = s;

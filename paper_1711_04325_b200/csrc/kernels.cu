@@ -142,7 +142,9 @@ __device__ __forceinline__ void upd1(float gh, float& th, float& d, float& m, co
 // Update 8 consecutive elements from j0 given their 8 fp16 wire values.  WD: the
 // weight-decay variant (R12, g += lambda theta on [0, n_wd)); a separate
 // instantiation so the default path carries no per-element test.
-template <bool RMS, bool WD>
+// KM == false (LMSGD_FLAG_FREEZE_M, only with alpha_RMSprop == 0, RMS == false): m
+// is neither read nor written -- it does not enter Delta or theta then.
+template <bool RMS, bool WD, bool KM = true>
 __device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const UpdConst& c,
                                         float* __restrict__ th, float* __restrict__ d,
                                         float* __restrict__ m) {
@@ -153,7 +155,9 @@ __device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const Up
         float4* m4 = reinterpret_cast<float4*>(m + j0);
         float4 t0 = __ldcs(th4), t1 = __ldcs(th4 + 1);
         float4 d0 = __ldcs(d4), d1 = __ldcs(d4 + 1);
-        float4 m0 = __ldcs(m4), m1 = __ldcs(m4 + 1);
+        static_assert(KM || !RMS, "m is only frozen when alpha_RMSprop == 0");
+        float4 m0 = make_float4(0.f, 0.f, 0.f, 0.f), m1 = m0;
+        if (KM) { m0 = __ldcs(m4); m1 = __ldcs(m4 + 1); }
         float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
         float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
         float mv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
@@ -167,15 +171,18 @@ __device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const Up
         __stcs(th4 + 1, make_float4(tv[4], tv[5], tv[6], tv[7]));
         __stcs(d4, make_float4(dv[0], dv[1], dv[2], dv[3]));
         __stcs(d4 + 1, make_float4(dv[4], dv[5], dv[6], dv[7]));
-        __stcs(m4, make_float4(mv[0], mv[1], mv[2], mv[3]));
-        __stcs(m4 + 1, make_float4(mv[4], mv[5], mv[6], mv[7]));
+        if (KM) {
+            __stcs(m4, make_float4(mv[0], mv[1], mv[2], mv[3]));
+            __stcs(m4 + 1, make_float4(mv[4], mv[5], mv[6], mv[7]));
+        }
     } else {
         for (int i = 0; i < 8 && j0 + i < n; ++i) {
             float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
-            float t = th[j0 + i], dd = d[j0 + i], mm = m[j0 + i];
+            float t = th[j0 + i], dd = d[j0 + i], mm = KM ? m[j0 + i] : 0.f;
             if (WD && j0 + i < c.n_wd) gh = fmaf(c.wd, t, gh);
             upd1<RMS>(gh, t, dd, mm, c);
-            th[j0 + i] = t; d[j0 + i] = dd; m[j0 + i] = mm;
+            th[j0 + i] = t; d[j0 + i] = dd;
+            if (KM) m[j0 + i] = mm;
         }
     }
 }
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_local(const uint16_t* __res
     if (st) flush_status(kNone, sat, st, ST_SUM_SAT);
 }
 
-template <bool RMS, bool WD>
+template <bool RMS, bool WD, bool KM>
 __global__ void __launch_bounds__(kThreads) k_update(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
                                                      float* __restrict__ th, float* __restrict__ d,
                                                      float* __restrict__ m, const int64_t* st,
@@ -289,13 +296,13 @@ __global__ void __launch_bounds__(kThreads) k_update(const uint16_t* __restrict_
     for (int64_t v = gtid(); v < nv; v += gstride()) {
         const int64_t j0 = v << 3;
         const uint4 r = *reinterpret_cast<const uint4*>(R + j0);
-        update8<RMS, WD>(r, j0, n, c, th, d, m);
+        update8<RMS, WD, KM>(r, j0, n, c, th, d, m);
     }
 }
 
 // k = 1 single pass (LMSGD_FLAG_NO_SKIP): h = sat16(s g) kept in registers,
 // ghat = fp32(h) / s, update.  28 B/elem of HBM traffic.
-template <bool RMS, bool WD>
+template <bool RMS, bool WD, bool KM>
 __global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g, int64_t n, float s,
                                                      UpdConst c, float* __restrict__ th,
                                                      float* __restrict__ d, float* __restrict__ m,
@@ -318,7 +325,7 @@ __global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g
         float x[8];
         load8_g(g, j0, n, x);
         const uint4 r = pack8(x, s, j0, first, sat);
-        update8<RMS, WD>(r, j0, n, c, th, d, m);
+        update8<RMS, WD, KM>(r, j0, n, c, th, d, m);
     }
     flush_status(first, sat, st, ST_PACK_SAT);
 }
@@ -579,7 +586,7 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
     if (t0) atomicAdd(a.ctr + 1, 1u);   // k_xfinalize waits for every block of this grid
 }
 
-template <bool RMS, bool WD>
+template <bool RMS, bool WD, bool KM>
 __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
     // no griddepcontrol.wait: ordering with k_xstep1 is by flags D and cflag.
     // kXUnits units per block: 2 was faster in isolation (tools/xbench.cu, 109 vs
@@ -642,7 +649,7 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
         const int64_t j0 = ((int64_t)owner[v] * gsh + gi) << 3;
         if (j0 >= x.n) continue;
         const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner[v]] + x.lay.off_R) + (gi << 3);
-        update8<RMS, WD>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, c, a.th, a.d, a.m);
+        update8<RMS, WD, KM>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, c, a.th, a.d, a.m);
     }
 }
 
@@ -730,6 +737,19 @@ int grid_for(const Launch&, int64_t work_items) {
 
 // ------------------------------------------------------------------ launchers
 
+// The update's kernel instantiation for a step: RMS (alpha_RMSprop != 0, or unknown
+// on the host in graph mode), WD (weight decay on), KM (m kept: not FREEZE_M).
+struct UpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_update<R, W, K>; } };
+struct Fused1K { template <bool R, bool W, bool K> static constexpr auto get() { return k_fused1<R, W, K>; } };
+struct XUpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_xupdate<R, W, K>; } };
+template <typename K>
+auto pick_variant(const UpdConst& c, bool graph) {
+    const bool rms = c.a_rms != 0.0f || graph, wd = c.n_wd > 0, km = rms || !c.freeze_m;
+    if (rms) return wd ? K::template get<true, true, true>() : K::template get<true, false, true>();
+    if (km) return wd ? K::template get<false, true, true>() : K::template get<false, false, true>();
+    return wd ? K::template get<false, true, false>() : K::template get<false, false, false>();
+}
+
 // Launch with the programmatic-stream-serialization attribute (see pdl_enter).
 template <typename... KArgs, typename... Args>
 cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), int grid, int block, cudaStream_t s,
@@ -781,10 +801,7 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
     (void)gsh;
     const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits);
     const bool pdl = (L.pdl_mask & 4) == 0;   // bit 4 (diagnostics): launch k_xupdate after k_xstep1 completes
-    const bool rms = a.c.a_rms != 0.0f || a.ctab, wd = a.c.n_wd > 0;
-    auto* kern = rms ? (wd ? k_xupdate<true, true> : k_xupdate<true, false>)
-                     : (wd ? k_xupdate<false, true> : k_xupdate<false, false>);
-    e = launch_pdl_if(pdl, kern, grid, kThreads, s, a);
+    e = launch_pdl_if(pdl, pick_variant<XUpdateK>(a.c, a.ctab != nullptr), grid, kThreads, s, a);
     if (e != cudaSuccess) return e;
     return launch_pdl_if(true, k_xfinalize, 1, 32, s, a, (unsigned int)L.grid_xstep);
 }
@@ -792,9 +809,9 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
 
 int stream_blocks_per_sm() {
     int worst = 1 << 30, b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update<true, false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update<true, false, true>, kThreads, 0);
     worst = b < worst ? b : worst;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true, false>, kThreads, 0);  // NOLINT
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true, false, true>, kThreads, 0);  // NOLINT
     worst = b < worst ? b : worst;
     return worst > 0 ? worst : 1;
 }
@@ -818,21 +835,17 @@ cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, in
                           const UpdConst& c, float* th, float* d, float* m, const int64_t* st,
                           int64_t* st_reset, int64_t* last, const Dev1& dv) {
     const int grid = grid_for(L, (n + 7) >> 3);
-    // graph mode: alpha_RMSprop is only known on the device; c.n_wd > 0 selects the decay variant
-    const bool rms = c.a_rms != 0.0f || dv.epoch, wd = c.n_wd > 0;
-    auto* kern = rms ? (wd ? k_update<true, true> : k_update<true, false>)
-                     : (wd ? k_update<false, true> : k_update<false, false>);
-    return launch_pdl(kern, grid, kThreads, s, R, n, c, th, d, m, st, st_reset, last, dv);
+    // graph mode: alpha_RMSprop is only known on the device
+    return launch_pdl(pick_variant<UpdateK>(c, dv.epoch != nullptr), grid, kThreads, s, R, n, c, th, d, m, st,
+                      st_reset, last, dv);
 }
 
 cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                           const UpdConst& c, float* th, float* d, float* m, int64_t* st,
                           int64_t* st_reset, int64_t* /*last: see launch_finalize_fused*/, const Dev1& dv) {
     const int grid = grid_for(L, (n + 7) >> 3);
-    const bool rms = c.a_rms != 0.0f || dv.epoch, wd = c.n_wd > 0;
-    auto* kern = rms ? (wd ? k_fused1<true, true> : k_fused1<true, false>)
-                     : (wd ? k_fused1<false, true> : k_fused1<false, false>);
-    return launch_pdl(kern, grid, kThreads, s, g, n, scale, c, th, d, m, st, st_reset, dv);
+    return launch_pdl(pick_variant<Fused1K>(c, dv.epoch != nullptr), grid, kThreads, s, g, n, scale, c, th, d, m,
+                      st, st_reset, dv);
 }
 
 int64_t host_units(const XArgs& x) {

@@ -23,6 +23,7 @@ struct UpdConst {
     float eta, a_sgd, a_rms;
     float inv_ks;                // fp32(1 / (k s)), exact for power-of-two k s
     float wd;                    // weight decay lambda (R12), 0 = off
+    int32_t freeze_m;            // host-side only: LMSGD_FLAG_FREEZE_M and a_rms == 0 (kernel choice)
     int64_t n_wd;                // elements [0, n_wd) are decayed
 };
 

@@ -220,10 +220,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const float* g = static_cast<const float*>(wire);
             for (int i = 0; i < 8; ++i) x8[i] = (n8 + i < n) ? g[n8 + i] : 0.0f;
             const uint4 h = pack8(x8, s, n8, first, sat);
-            update8<RMS>(h, n8, n, c, th, d, m);
+            update8<RMS, false>(h, n8, n, c, th, d, m);
         } else {
             const uint4 r = *reinterpret_cast<const uint4*>(static_cast<const uint16_t*>(wire) + n8);
-            update8<RMS>(r, n8, n, c, th, d, m);
+            update8<RMS, false>(r, n8, n, c, th, d, m);
         }
     }
     if (FUSED && st_out) {

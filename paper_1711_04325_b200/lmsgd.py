@@ -26,6 +26,7 @@ LMSGD_MAX_WORLD = 8
 LMSGD_IPC_HANDLE_BYTES = 64
 LMSGD_MAX_BN_CHANNELS = 1 << 20
 LMSGD_FLAG_NO_SKIP = 0x1
+LMSGD_FLAG_FREEZE_M = 0x2
 SCHEDULE_SLOW_START = 0
 SCHEDULE_GOYAL = 1
 TRANSITION_ELU, TRANSITION_LINEAR, TRANSITION_SIGMOID, TRANSITION_SUDDEN = 0, 1, 2, 3   # R20

@@ -102,6 +102,29 @@ def main():
     replicas_identical(th, d, m)
     L.lmsgd_finalize(ctx)
 
+    # ---- LMSGD_FLAG_FREEZE_M: theta, Delta bit-identical to the full rule; m untouched on SGD steps
+    ref = L.lmsgd_init(world, rank, local, n, S)
+    L.connect_process_group(ref)
+    frz = L.lmsgd_init(world, rank, local, n, S, None, L.LMSGD_FLAG_FREEZE_M)
+    L.connect_process_group(frz)
+    a = [D(th0), D(np.zeros(n, np.float32)), D(np.zeros(n, np.float32))]
+    b = [x.clone() for x in a]
+    for t in (3, 12, 13):
+        co = L.lmsgd_schedule_at(None, C1_C, t)
+        gt = D(synth.grads(world, t, n)[rank])
+        m_before = b[2].clone()
+        L.lmsgd_step(ref, a[0], gt, a[1], a[2], co)
+        L.lmsgd_step(frz, b[0], gt, b[1], b[2], co)
+        torch.cuda.synchronize()
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]), t
+        assert torch.equal(b[2], m_before) if co.alpha_rmsprop == 0.0 else torch.equal(a[2], b[2]), t
+    replicas_identical(*b)
+    L.lmsgd_query_status(ref)
+    L.lmsgd_query_status(frz)
+    dist.barrier()
+    L.lmsgd_finalize(ref)
+    L.lmsgd_finalize(frz)
+
     # ---- ghat bit-exact (mu1 = 0, (a_SGD, a_RMS) = (1, 0) => Delta = -ghat), with saturation
     n = 200_003
     hyp = L.lmsgd_hyper_default()

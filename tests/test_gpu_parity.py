@@ -516,3 +516,28 @@ def test_weight_decay_prefix(flags):
     L.lmsgd_finalize(octx)
     L.lmsgd_finalize(gctx)
     L.lmsgd_finalize(hctx)
+
+
+@pytest.mark.parametrize("flags", [0, L.LMSGD_FLAG_NO_SKIP])
+def test_freeze_m_sgd_phase(flags):
+    """LMSGD_FLAG_FREEZE_M: RMSprop steps are the full rule; on alpha_RMSprop = 0 steps
+    theta and Delta are bit-identical to the full rule and m is not touched."""
+    n, s = 100_003, 1024.0
+    th0, d0, m0 = init_state(n)
+    ref = L.lmsgd_init(1, 0, 0, n, s, None, flags)
+    frz = L.lmsgd_init(1, 0, 0, n, s, None, flags | L.LMSGD_FLAG_FREEZE_M)
+    a, b = [dev(th0), dev(d0), dev(m0)], [dev(th0), dev(d0), dev(m0)]
+    for t in (1, 9, 12, 15, 16):   # exp branch, alpha = 1/2 (a_RMS > 0), then SGD
+        co = L.lmsgd_schedule_at(None, C1_C, t)
+        g = dev(synth.grads(1, t, n)[0])
+        m_before = b[2].clone()
+        L.lmsgd_step(ref, *a[:1], g, *a[1:], co)
+        L.lmsgd_step(frz, *b[:1], g, *b[1:], co)
+        torch.cuda.synchronize()
+        assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1]), t
+        if co.alpha_rmsprop == 0.0:
+            assert torch.equal(b[2], m_before) and not torch.equal(a[2], b[2]), t
+        else:
+            assert torch.equal(a[2], b[2]), t
+    L.lmsgd_finalize(ref)
+    L.lmsgd_finalize(frz)

@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) k_update_flat(const uint16_t* __rest
                                                           float* __restrict__ th, float* __restrict__ d,
                                                           float* __restrict__ m) {
     const int64_t v = gtid();
-    if (v < (n >> 3)) update8<RMS>(*reinterpret_cast<const uint4*>(R + (v << 3)), v << 3, n, c, th, d, m);
+    if (v < (n >> 3)) update8<RMS, false>(*reinterpret_cast<const uint4*>(R + (v << 3)), v << 3, n, c, th, d, m);
 }
 
 // V8: flat, two groups per thread (loads of both hoisted)
@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(kThreads) k_update_flat2(const uint16_t* __res
     uint4 r0 = make_uint4(0, 0, 0, 0), r1 = r0;
     if (v0 < nv) r0 = *reinterpret_cast<const uint4*>(R + (v0 << 3));
     if (v1 < nv) r1 = *reinterpret_cast<const uint4*>(R + (v1 << 3));
-    if (v0 < nv) update8<RMS>(r0, v0 << 3, n, c, th, d, m);
-    if (v1 < nv) update8<RMS>(r1, v1 << 3, n, c, th, d, m);
+    if (v0 < nv) update8<RMS, false>(r0, v0 << 3, n, c, th, d, m);
+    if (v1 < nv) update8<RMS, false>(r1, v1 << 3, n, c, th, d, m);
 }
 
 template <int BS>
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(BS) k_update_flat_bs(const uint16_t* __restric
                                                        float* __restrict__ th, float* __restrict__ d,
                                                        float* __restrict__ m) {
     const int64_t v = (int64_t)blockIdx.x * BS + threadIdx.x;
-    if (v < (n >> 3)) update8<true>(*reinterpret_cast<const uint4*>(R + (v << 3)), v << 3, n, c, th, d, m);
+    if (v < (n >> 3)) update8<true, false>(*reinterpret_cast<const uint4*>(R + (v << 3)), v << 3, n, c, th, d, m);
 }
 
 __global__ void __launch_bounds__(kThreads) k_pack_flat(const float* __restrict__ g, int64_t n, int64_t n_pad, float s,
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) k_fused_flat(const float* __restrict
         const int64_t j0 = v << 3;
         float x[8];
         load8_g(g, j0, n, x);
-        update8<RMS>(pack8(x, s, j0, first, sat), j0, n, c, th, d, m);
+        update8<RMS, false>(pack8(x, s, j0, first, sat), j0, n, c, th, d, m);
     }
     flush_status(first, sat, st, ST_PACK_SAT);
 }
@@ -155,10 +155,70 @@ __global__ void __launch_bounds__(kThreads) k_update_discard(const uint16_t* __r
         // each lane holds 16 B; lanes 0,8,16,24 own whole 128-B lines when the warp is aligned
         if ((j0 & 63) == 0 && j0 + 64 <= ((n + 7) & ~int64_t(7)))
             asm volatile("discard.global.L2 [%0], 128;" ::"l"(R + j0) : "memory");
-        update8<RMS>(r, j0, n, c, th, d, m);
+        update8<RMS, false>(r, j0, n, c, th, d, m);
     }
 }
 
+
+// S*: a guarded k = 1 step without the fp16 staging buffer: a read-only scan of g
+// (status words only), then a single fused pass that re-reads g -- hopefully from
+// L2 (g is clean, so nothing is written back) -- and is skipped by the status.
+__device__ __forceinline__ float4 ld_el(const float* p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+template <int MODE>   // 0: __ldcs, 1: evict_last, 2: plain
+__global__ void __launch_bounds__(kThreads) k_scan(const float* __restrict__ g, int64_t n, float s, int64_t* st) {
+    int64_t first = kNone;
+    unsigned sat = 0;
+    const int64_t v = gtid();
+    if (v < ((n + 7) >> 3)) {
+        const int64_t j0 = v << 3;
+        float x[8];
+        if (MODE != 0 && j0 + 8 <= n) {
+            float4 a, b;
+            if (MODE == 1) { const uint64_t pol = policy_evict_last(); a = ld_el(g + j0, pol); b = ld_el(g + j0 + 4, pol); }
+            else { a = *reinterpret_cast<const float4*>(g + j0); b = *reinterpret_cast<const float4*>(g + j0 + 4); }
+            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+        } else {
+            load8_g(g, j0, n, x);
+        }
+        const uint4 o = pack8(x, s, j0, first, sat);
+        (void)o;
+    }
+    flush_status(first, sat, st, ST_PACK_SAT);
+}
+template <bool REV, bool LDCS>
+__global__ void __launch_bounds__(kThreads) k_fused_guard(const float* __restrict__ g, int64_t n, float s, UpdConst c,
+                                                          float* __restrict__ th, float* __restrict__ d,
+                                                          float* __restrict__ m, const int64_t* st) {
+    if (st[ST_FIRST] != kNone || st[ST_ERROR] != 0) return;
+    const int64_t b = REV ? (int64_t)gridDim.x - 1 - blockIdx.x : blockIdx.x;
+    const int64_t v = b * blockDim.x + threadIdx.x;
+    if (v < ((n + 7) >> 3)) {
+        const int64_t j0 = v << 3;
+        float x[8];
+        if (!LDCS && j0 + 8 <= n) {
+            const float4 a = *reinterpret_cast<const float4*>(g + j0), bb = *reinterpret_cast<const float4*>(g + j0 + 4);
+            x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w; x[4] = bb.x; x[5] = bb.y; x[6] = bb.z; x[7] = bb.w;
+        } else {
+            load8_g(g, j0, n, x);
+        }
+        int64_t first = kNone;
+        unsigned sat = 0;
+        update8<true, false>(pack8(x, s, j0, first, sat), j0, n, c, th, d, m);
+    }
+}
+// reversed flat update (reads the freshest part of h first)
+__global__ void __launch_bounds__(kThreads) k_update_rev(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
+                                                         float* __restrict__ th, float* __restrict__ d,
+                                                         float* __restrict__ m, const int64_t* st) {
+    if (st[ST_FIRST] != kNone || st[ST_ERROR] != 0) return;
+    const int64_t v = ((int64_t)gridDim.x - 1 - blockIdx.x) * blockDim.x + threadIdx.x;
+    if (v < ((n + 7) >> 3)) update8<true, false>(*reinterpret_cast<const uint4*>(R + (v << 3)), v << 3, n, c, th, d, m);
+}
 }  // namespace
 }  // namespace lmsgd
 
@@ -223,13 +283,13 @@ int main(int argc, char** argv) {
     const double upd_bytes = 26.0 * n, fused_bytes = 28.0 * n, pack_bytes = 6.0 * n;
     // reference result: one pack + update (production kernels)
     reset();
-    launch_pack(0, L, g, n, n_pad, 1024.f, h, st);
-    launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr);
+    launch_pack(0, L, g, n, n_pad, 1024.f, h, st, Dev1{});
+    launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr, Dev1{});
     snapshot(rt, rd, rm);
 
     printf("n=%lld sms=%d blocks/sm(stream)=%d\n", (long long)n, sms, stream_blocks_per_sm());
     float t;
-    t = time_it(iters, [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st); });
+    t = time_it(iters, [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st, Dev1{}); });
     printf("P0 pack            %8.2f us  %7.1f GB/s\n", t, pack_bytes / t / 1e3);
     t = time_it(iters, [&] { k_pack_l2<<<L.grid_cap_stream, kThreads>>>(g, n, n_pad, 1024.f, h, st); });
     printf("P1 pack evict_last %8.2f us  %7.1f GB/s\n", t, pack_bytes / t / 1e3);
@@ -237,12 +297,12 @@ int main(int argc, char** argv) {
     t = time_it(iters, [&] { k_pack_flat<<<fgrid, kThreads>>>(g, n, n_pad, 1024.f, h, st); });
     printf("P2 pack flat       %8.2f us  %7.1f GB/s\n", t, pack_bytes / t / 1e3);
 
-    reset(); launch_pack(0, L, g, n, n_pad, 1024.f, h, st); CKE(cudaDeviceSynchronize());
+    reset(); launch_pack(0, L, g, n, n_pad, 1024.f, h, st, Dev1{}); CKE(cudaDeviceSynchronize());
     // update variants (single step each for bitwise check, then timed repeatedly)
     struct V { const char* name; std::function<void()> f; };
     const int gridc = L.grid_cap_stream;
     std::vector<V> vs = {
-        {"V0 update (prod)", [&] { k_update<true, false><<<gridc, kThreads>>>(h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); }},
+        {"V0 update (prod)", [&] { k_update<true, false, true><<<gridc, kThreads>>>(h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); }},
         {"V1 update unroll2", [&] { k_update_u2<true><<<gridc, kThreads>>>(h, n, c, th, d, m); }},
         {"V2 update flat", [&] { k_update_flat<true><<<(int)(((n >> 3) + kThreads - 1) / kThreads), kThreads>>>(h, n, c, th, d, m); }},
         {"V7 update flat bs512", [&] { k_update_flat_bs<512><<<(int)(((n >> 3) + 511) / 512), 512>>>(h, n, c, th, d, m); }},
@@ -272,9 +332,9 @@ int main(int argc, char** argv) {
         printf("%-30s %8.2f us  %7.1f GB/s  bitexact=%d\n", v.name, t, upd_bytes / t / 1e3, ok);
     }
     // fused variants vs production fused
-    reset(); launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr); snapshot(rt, rd, rm);
+    reset(); launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr, Dev1{}); snapshot(rt, rd, rm);
     std::vector<V> fs = {
-        {"F0 fused (prod)", [&] { launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr); }},
+        {"F0 fused (prod)", [&] { launch_fused1(0, L, g, n, 1024.f, c, th, d, m, st, nullptr, nullptr, Dev1{}); }},
         {"F2 fused flat", [&] { k_fused_flat<true><<<(int)((((n + 7) >> 3) + kThreads - 1) / kThreads), kThreads>>>(g, n, 1024.f, c, th, d, m, st); }},
         {"F3 fused tma TE2048 S6", [&] {
              k_stream_tma<true, true, 2048, 6><<<sms, kTmaThreads, 6 * tma_stage_bytes<true, 2048>()>>>(g, n, 1024.f, c, th, d, m, nullptr, st); }},
@@ -289,9 +349,10 @@ int main(int argc, char** argv) {
         printf("%-30s %8.2f us  %7.1f GB/s  bitexact=%d\n", v.name, t, fused_bytes / t / 1e3, ok);
     }
     // guarded pair: pack + update, and the L2-resident variant
-    reset(); launch_pack(0, L, g, n, n_pad, 1024.f, h, st); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr); snapshot(rt, rd, rm);
+    reset(); launch_pack(0, L, g, n, n_pad, 1024.f, h, st, Dev1{}); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); snapshot(rt, rd, rm);
+    const int fgrid8 = (int)((((n + 7) >> 3) + kThreads - 1) / kThreads);
     std::vector<V> ps = {
-        {"G0 pack+update (prod)", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr); }},
+        {"G0 pack+update (prod)", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st, Dev1{}); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); }},
         {"G1 pack_l2+update_discard", [&] { k_pack_l2<<<gridc, kThreads>>>(g, n, n_pad, 1024.f, h, st);
                                              k_update_discard<true><<<gridc, kThreads>>>(h, n, c, th, d, m, st); }},
         {"G2 pack_l2+update tma", [&] { k_pack_l2<<<gridc, kThreads>>>(g, n, n_pad, 1024.f, h, st);
@@ -300,8 +361,20 @@ int main(int argc, char** argv) {
              k_update_flat<true><<<(int)(((n >> 3) + kThreads - 1) / kThreads), kThreads>>>(h, n, c, th, d, m); }},
         {"G5 pack evict_last+update flat", [&] { k_pack_l2<<<fgrid, kThreads>>>(g, n, n_pad, 1024.f, h, st);
              k_update_flat<true><<<(int)(((n >> 3) + kThreads - 1) / kThreads), kThreads>>>(h, n, c, th, d, m); }},
-        {"G6 prod pack+update (PDL)", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr); }},
-        {"G3 pack+update tma", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st);
+        {"G6 prod pack+update (PDL)", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st, Dev1{}); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); }},
+        {"S1 scan ldcs + fused", [&] { k_scan<0><<<fgrid8, kThreads>>>(g, n, 1024.f, st);
+             k_fused_guard<false, true><<<fgrid8, kThreads>>>(g, n, 1024.f, c, th, d, m, st); }},
+        {"S2 scan evict_last + fused", [&] { k_scan<1><<<fgrid8, kThreads>>>(g, n, 1024.f, st);
+             k_fused_guard<false, false><<<fgrid8, kThreads>>>(g, n, 1024.f, c, th, d, m, st); }},
+        {"S3 scan evict_last + fused rev", [&] { k_scan<1><<<fgrid8, kThreads>>>(g, n, 1024.f, st);
+             k_fused_guard<true, false><<<fgrid8, kThreads>>>(g, n, 1024.f, c, th, d, m, st); }},
+        {"S4 scan plain + fused rev", [&] { k_scan<2><<<fgrid8, kThreads>>>(g, n, 1024.f, st);
+             k_fused_guard<true, false><<<fgrid8, kThreads>>>(g, n, 1024.f, c, th, d, m, st); }},
+        {"S5 scan plain + fused rev ldcs", [&] { k_scan<2><<<fgrid8, kThreads>>>(g, n, 1024.f, st);
+             k_fused_guard<true, true><<<fgrid8, kThreads>>>(g, n, 1024.f, c, th, d, m, st); }},
+        {"G7 pack + update rev", [&] { k_pack_flat<<<fgrid, kThreads>>>(g, n, n_pad, 1024.f, h, st);
+             k_update_rev<<<fgrid8, kThreads>>>(h, n, c, th, d, m, st); }},
+        {"G3 pack+update tma", [&] { launch_pack(0, L, g, n, n_pad, 1024.f, h, st, Dev1{});
              k_stream_tma<true, false, 2048, 6><<<sms, kTmaThreads, 6 * tma_stage_bytes<false, 2048>()>>>(h, n, 1024.f, c, th, d, m, st, nullptr); }},
     };
     for (auto& v : ps) {
