@@ -125,6 +125,28 @@ def main():
     L.lmsgd_finalize(ref)
     L.lmsgd_finalize(frz)
 
+    # ---- the torch-style front end (LMSGD) on a small net, one minibatch per rank
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Conv2d(3, 8, 3), torch.nn.BatchNorm2d(8), torch.nn.ReLU(),
+                              torch.nn.Flatten(), torch.nn.Linear(8 * 6 * 6, 10)).to(dev)
+    opt = L.LMSGD(net.parameters(), cluster=C1_C, loss_scale=S, weight_decay=1e-4)
+    for t in (1, 2, 3):
+        gen = torch.Generator(device="cpu").manual_seed(1000 * t + rank)
+        x, y = torch.randn(32, 3, 8, 8, generator=gen).to(dev), torch.randint(0, 10, (32,), generator=gen).to(dev)
+        opt.zero_grad()
+        torch.nn.functional.cross_entropy(net(x), y).backward()
+        allg = [torch.empty_like(opt.flat_g) for _ in range(world)]
+        dist.all_gather(allg, opt.flat_g)
+        prev = H(opt.flat_p), H(opt.delta), H(opt.m)
+        opt.step()
+        assert opt.status()[0] == 0
+        check_state(H(opt.flat_p), H(opt.delta), H(opt.m), *prev,
+                    exchange.exchange([H(a) for a in allg], S).ghat, schedule.coeffs_at(t, schedule.Hyper(), C1),
+                    wd=1e-4, n_wd=opt.n_decay)
+        replicas_identical(opt.flat_p, opt.delta, opt.m)
+    dist.barrier()
+    opt.close()
+
     # ---- ghat bit-exact (mu1 = 0, (a_SGD, a_RMS) = (1, 0) => Delta = -ghat), with saturation
     n = 200_003
     hyp = L.lmsgd_hyper_default()

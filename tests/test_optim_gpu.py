@@ -1,0 +1,94 @@
+"""The torch-style front end (paper_1711_04325_b200.optim.LMSGD) on a small conv net:
+zero-copy flat buffers (row a1), schedule (a0), weight-decay ordering (R12),
+one-step parity against the oracle on every step, checkpoint/resume bit-exact."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA GPU", allow_module_level=True)
+
+import paper_1711_04325_b200 as L  # noqa: E402
+from oracle import exchange, schedule  # noqa: E402
+from test_gpu_parity import check_state  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+DEV = torch.device("cuda:0")
+C1 = schedule.Cluster(n_workers=2, b_local=32, n_train=64)
+
+
+def _net(seed=0):
+    torch.manual_seed(seed)
+    return torch.nn.Sequential(torch.nn.Conv2d(3, 8, 3), torch.nn.BatchNorm2d(8), torch.nn.ReLU(),
+                               torch.nn.Flatten(), torch.nn.Linear(8 * 6 * 6, 10)).to(DEV)
+
+
+def _batch(t):
+    g = torch.Generator(device="cpu").manual_seed(100 + t)
+    return (torch.randn(32, 3, 8, 8, generator=g).to(DEV), torch.randint(0, 10, (32,), generator=g).to(DEV))
+
+
+def _train_step(net, opt, t):
+    x, y = _batch(t)
+    opt.zero_grad()
+    torch.nn.functional.cross_entropy(net(x), y).backward()
+
+
+def test_lmsgd_optimizer_matches_oracle_and_resumes(monkeypatch):
+    # bit-exact resume needs a deterministic backward (cuDNN's default conv wgrad may use atomics)
+    monkeypatch.setattr(torch.backends.cudnn, "deterministic", True)
+    monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
+    lam, s = 1e-4, 1024.0
+    net = _net()
+    opt = L.LMSGD(net.parameters(), cluster=L.make_cluster(2, 32, 64), loss_scale=s, weight_decay=lam)
+    # R12 ordering: conv and fc weights first (decayed), BN and biases after
+    assert opt.n_decay == 8 * 3 * 3 * 3 + 10 * 8 * 6 * 6
+    assert opt.n == sum(p.numel() for p in net.parameters())
+    for t in range(1, 6):   # exp branch: alpha_RMS > 0
+        _train_step(net, opt, t)
+        g = opt.flat_g.cpu().numpy()[None]
+        prev = opt.flat_p.cpu().numpy(), opt.delta.cpu().numpy(), opt.m.cpu().numpy()
+        c = opt.step()
+        code, st = opt.status()
+        assert code == 0 and st.skipped == 0 and c.epoch == schedule.coeffs_at(t, schedule.Hyper(), C1).epoch
+        check_state(opt.flat_p.cpu().numpy(), opt.delta.cpu().numpy(), opt.m.cpu().numpy(), *prev,
+                    exchange.exchange(list(g), s).ghat, schedule.coeffs_at(t, schedule.Hyper(), C1),
+                    wd=lam, n_wd=opt.n_decay)
+    # the module's parameters ARE the flat buffer (zero copy)
+    assert net[0].weight.data_ptr() == opt.flat_p.data_ptr()
+    # checkpoint, continue 3 steps; restore into a fresh model + optimizer, same 3 steps
+    ck_model = {k: v.clone() for k, v in net.state_dict().items()}
+    ck_opt = opt.state_dict()
+    for t in range(6, 9):
+        _train_step(net, opt, t)
+        opt.step()
+    torch.cuda.synchronize()
+    net2 = _net(seed=1)
+    opt2 = L.LMSGD(net2.parameters(), cluster=L.make_cluster(2, 32, 64), loss_scale=s, weight_decay=lam)
+    net2.load_state_dict(ck_model)
+    opt2.load_state_dict(ck_opt)
+    assert opt2.t == 6
+    for t in range(6, 9):
+        _train_step(net2, opt2, t)
+        opt2.step()
+    torch.cuda.synchronize()
+    assert torch.equal(opt.flat_p, opt2.flat_p) and torch.equal(opt.delta, opt2.delta) and torch.equal(opt.m, opt2.m)
+    opt.close()
+    opt2.close()
+
+
+def test_lmsgd_detached_grad_fails_loudly():
+    net = _net()
+    opt = L.LMSGD(net.parameters(), cluster=L.make_cluster(2, 32, 64))
+    _train_step(net, opt, 1)
+    net.zero_grad(set_to_none=True)
+    x, y = _batch(2)
+    torch.nn.functional.cross_entropy(net(x), y).backward()
+    with pytest.raises(RuntimeError, match="flat gradient"):
+        opt.step()
+    opt.close()
+
+
+def test_lmsgd_rejects_cpu_params():
+    with pytest.raises(ValueError):
+        L.LMSGD(torch.nn.Linear(4, 4).parameters())

@@ -9,7 +9,7 @@ PAPER.md:113-118), with the lmsgd exchange + blended update as the optimizer.
 Per rank: minibatch 32 of 3x224x224 synthetic images, torchvision
 ResNet-50 with random init, fp32 compute (cuDNN may use TF32),
 BatchNorm with momentum 1.  The parameters and gradients are views
-of two flat fp32 buffers, so lmsgd_step consumes the gradient in place (row a1).
+of two flat fp32 buffers (``LMSGD``, row a1), so lmsgd_step consumes the gradient in place.
 Prints one JSON line on rank 0: iteration time, the exchange + update share
 (the "communication time" of Fig. 1), images/s.  Forward/backward are cuDNN
 (library code); the path under test is the lmsgd step.
@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--iters", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--weight-decay", type=float, default=0.0, help="R12 (Goyal et al. used 1e-4)")
     args = ap.parse_args()
     rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
         int(os.environ.get("LOCAL_RANK", 0))
@@ -45,23 +46,11 @@ def main():
     torch.manual_seed(0)
     model = torchvision.models.resnet50().to(dev)
     bn_sync.last_minibatch_bn(model)
-    params = [p for p in model.parameters()]
-    n = sum(p.numel() for p in params)
-    flat_p = torch.empty(n, device=dev)
-    flat_g = torch.zeros(n, device=dev)
-    off = 0
-    for p in params:   # parameters and gradients become views of the flat buffers
-        k = p.numel()
-        flat_p[off:off + k].copy_(p.data.reshape(-1))
-        p.data = flat_p[off:off + k].view_as(p)
-        p.grad = flat_g[off:off + k].view_as(p)
-        off += k
-    delta = torch.zeros(n, device=dev)
-    m = torch.zeros(n, device=dev)
-    ctx = L.lmsgd_init(world, rank, local, n, 1024.0)
-    L.connect_process_group(ctx)
+    # the torch-style front end: parameters and gradients become views of flat buffers
+    opt = L.LMSGD(model.parameters(), cluster=L.make_cluster(1024, args.batch), loss_scale=1024.0,
+                  weight_decay=args.weight_decay)
+    n, ctx = opt.n, opt.ctx
     sync = bn_sync.BNStatsSync(model, ctx)
-    cl = L.make_cluster(1024, args.batch)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1711 + rank)
     x = torch.randn(args.batch, 3, 224, 224, device=dev, generator=gen)
@@ -72,23 +61,19 @@ def main():
     fb_ms, st_ms, it_ms = [], [], []
     model.train()
     for it in range(args.warmup + args.iters):
-        t = it + 1
-        flat_g.zero_()
+        opt.zero_grad()
         ev[0].record(stream)
         loss = crit(model(x), y) * 1.0
         loss.backward()
         ev[1].record(stream)
-        L.lmsgd_step(ctx, flat_p, flat_g, delta, m, L.lmsgd_schedule_at(None, cl, t))
+        opt.step()
         ev[2].record(stream)
         torch.cuda.synchronize()
-        if it == 0:   # autograd accumulated in place: the gradients are still views of flat_g
-            base = flat_g.data_ptr()
-            assert all(base <= p.grad.data_ptr() < base + 4 * n for p in params), "grad left the flat buffer"
         if it >= args.warmup:
             fb_ms.append(ev[0].elapsed_time(ev[1]))
             st_ms.append(ev[1].elapsed_time(ev[2]))
             it_ms.append(ev[0].elapsed_time(ev[2]))
-    code, st = L.lmsgd_query_status(ctx)
+    code, st = opt.status()
     sync.sync()                       # BN statistics average before "validation"
     torch.cuda.synchronize()
     med = lambda v: sorted(v)[len(v) // 2]  # noqa: E731
@@ -104,7 +89,7 @@ def main():
                "images_per_s": world * args.batch / (res["iteration_ms"] * 1e-3),
                "last_status": code, "loss": float(loss)}
         print(json.dumps(out), flush=True)
-    L.lmsgd_finalize(ctx)
+    opt.close()
     if world > 1:
         dist.destroy_process_group()
 
