@@ -415,6 +415,25 @@ def main():
         nvlink["nccl_fp16_allreduce_us"] = nccl_ms * 1e3
         nvlink["nccl_fp16_allreduce_bus_gbs"] = bus_bytes / (nccl_ms * 1e-3) / 1e9
         del buf
+        # our fp16 all-reduce alone (lmsgd_exchange: pack + push + exact reduce + pulled
+        # all-gather into a local buffer), same payload, same convention
+        rout = torch.empty(n_pad, dtype=torch.int16, device=devc)
+        for _ in range(5):
+            L.lmsgd_exchange(ctx, grads, rout)
+        torch.cuda.synchronize()
+        barrier()
+        y0.record(stream)
+        for _ in range(50):
+            L.lmsgd_exchange(ctx, grads, rout)
+        y1.record(stream)
+        torch.cuda.synchronize()
+        code, _ = L.lmsgd_query_status(ctx)
+        assert code == 0, f"exchange status {code}"
+        x_ms = max_over_ranks(y0.elapsed_time(y1) / 50)
+        nvlink["lmsgd_exchange_us"] = x_ms * 1e3
+        nvlink["lmsgd_exchange_bus_gbs"] = bus_bytes / (x_ms * 1e-3) / 1e9
+        nvlink["lmsgd_exchange_bus_frac_of_900"] = nvlink["lmsgd_exchange_bus_gbs"] / 900.0
+        del rout
 
     # config C4: BN last-minibatch statistics average over the ranks (53 layers, 26,560
     # channels for ResNet-50), latency-bound; device time per call, max over ranks

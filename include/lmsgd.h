@@ -207,6 +207,23 @@ lmsgd_status lmsgd_step_host(lmsgd_ctx* ctx, void* stream, float* params, const 
                              float* delta, float* m, const lmsgd_coeffs* coeffs,
                              lmsgd_step_status* status_host);
 
+/* The fp16 all-reduce of the step on its own -- rows a2-a4 (pack, reduce-scatter,
+ * all-gather) without the update; PAPER.md:82-87 ("half-precision floats for
+ * communication" in the all-reduce), readings R7-R10 and R19:
+ *   R_out[j] = sat16_RNE( sum_{r<k} sat16_RNE(s * g_r[j]) )  for j < n_params,
+ *   R_out[j] = 0                                               for n_params <= j < n_pad,
+ * binary16 bits, the exact sum rounded once (the payload lmsgd_step averages as
+ * fp32(R) / (k s)).  grads: device fp32 [n_params], this rank's gradient;
+ * R_out: device uint16 [n_pad] (lmsgd_layout(world, n_params)), caller-owned,
+ * identical on every rank afterwards.  Collective: every rank calls it, in the same
+ * order relative to lmsgd_step (both advance the context's step counter).
+ * Enqueued on `stream`.  lmsgd_query_status reports the saturation counts and the
+ * first non-finite index; a non-finite gradient sets skipped = 1 and error =
+ * LMSGD_ERR_NONFINITE and leaves R_out's values unspecified.  world == 1: R_out is
+ * the packed gradient (one kernel).  Errors: INVALID_ARG (NULL / misaligned),
+ * STATE (before lmsgd_connect, or on a context that runs lmsgd_step_graph). */
+lmsgd_status lmsgd_exchange(lmsgd_ctx* ctx, void* stream, const float* grads, uint16_t* R_out);
+
 /* ---------------------------------------------------------------- CUDA graphs
  * lmsgd_step bakes its per-step arguments (coefficients, step number) into the
  * launches, so a captured lmsgd_step would replay the same step.  The graph entry

@@ -395,6 +395,31 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     return LMSGD_OK;
 }
 
+lmsgd_status lmsgd_exchange(lmsgd_ctx* c, void* stream, const float* grads, uint16_t* R_out) {
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (!aligned16(grads) || !aligned16(R_out))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "grads/R_out must be non-NULL and 16-byte aligned");
+    if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
+    if (c->mode == 2) return fail(c, LMSGD_ERR_STATE, "this context runs lmsgd_step_graph");
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint32_t epoch = ++c->step;   // one collective epoch, shared with lmsgd_step
+    const int parity = static_cast<int>(epoch & 1u);
+    c->last_stream = s;
+    if (c->world == 1) {
+        CK(c, timed(c, s, 0, [&] {
+               return lmsgd::launch_pack(s, c->L, grads, c->n, c->n_pad, c->scale, R_out, status_slot(c, parity));
+           }));
+        CK(c, lmsgd::launch_xfinal1(s, status_slot(c, parity), status_slot(c, parity ^ 1), c->last));
+        return LMSGD_OK;
+    }
+    const lmsgd::XArgs x = xargs(c, epoch, &c->dstate->xepoch);
+    lmsgd::XStep a{x, grads, c->scale, lmsgd::UpdConst{}, nullptr, nullptr, nullptr, c->last, c->xctr,
+                   nullptr, 0, nullptr, R_out};
+    CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, c->L, a); }));
+    return LMSGD_OK;
+}
+
 lmsgd_status lmsgd_set_weight_decay(lmsgd_ctx* c, double lambda, int64_t n_decay) {
     if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
     if (!(lambda >= 0.0) || !std::isfinite(lambda) || n_decay < -1 || n_decay > c->n)

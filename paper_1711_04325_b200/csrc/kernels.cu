@@ -583,6 +583,7 @@ __global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
         }
     }
     if (blockIdx.x == 0 && t0) stamp(x, TR_RED_END);
+
     if (t0) atomicAdd(a.ctr + 1, 1u);   // k_xfinalize waits for every block of this grid
 }
 
@@ -651,6 +652,51 @@ __global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
         const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner[v]] + x.lay.off_R) + (gi << 3);
         update8<RMS, WD, KM>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, c, a.th, a.d, a.m);
     }
+}
+
+// lmsgd_exchange, world > 1: the all-gather half of the fp16 all-reduce (row a4) on
+// its own, as a flat pull into the caller's buffer.  Same unit order and waits as
+// k_xupdate (chunk-major, owner-interleaved; flag D, then the owner's chunk flag),
+// then one 16-byte peer load and one local store per thread.  The reduced values
+// are copied whether or not a gradient was non-finite (the status says so).
+// Measured (k = 2, 51 MB): 123 us for the whole exchange, against 137 us with the
+// gather done inside k_xstep1's persistent grid after its reduce.
+__global__ void __launch_bounds__(kThreads) k_xgather(XStep a) {
+    const XArgs& x = a.x;
+    const Ep ep = get_ep(x);
+    const int64_t gsh = x.lay.shard >> 3;
+    const int64_t ups = (gsh + kThreads - 1) / kThreads;
+    const int64_t kcu = (int64_t)x.world * x.lay.cu;
+    const int64_t i = blockIdx.x;
+    const int c = (int)(i / kcu);
+    const int64_t r = i - (int64_t)c * kcu;
+    const int owner = (int)((r % x.world + x.rank) % x.world);
+    const int64_t u = c < x.lay.nchunks ? (int64_t)c * x.lay.cu + r / x.world : ups;
+    __shared__ int s_go;
+    if (threadIdx.x == 0) {
+        int go = spin_flag(x, ep, flag_slot(x, x.rank, FLAG_D)) ? 1 : 0;
+        if (go && u < ups && !spin_flag(x, ep, cflag(x, x.rank, c, owner))) {
+            go = 0;
+            status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+        }
+        s_go = go;
+    }
+    __syncthreads();
+    if (!s_go || u >= ups) return;
+    const int64_t gi = u * kThreads + threadIdx.x;
+    if (gi >= gsh) return;
+    const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
+    const uint4 v = *reinterpret_cast<const uint4*>(Rp);
+    __stcs(reinterpret_cast<uint4*>(a.rout + (((int64_t)owner * gsh + gi) << 3)), v);
+}
+
+// lmsgd_exchange, world == 1: the step's public status record (R = h, no second
+// rounding), and the next call's status slot cleared.
+__global__ void k_xfinal1(const int64_t* st, int64_t* st_next, int64_t* last) {
+    pdl_enter();
+    if (threadIdx.x == 0)
+        store_last(last, st[ST_FIRST], st[ST_PACK_SAT], 0, st[ST_ERROR], st[ST_FIRST] != kNone ? 1 : 0);
+    if (threadIdx.x < ST_WORDS) reset_words(st_next);
 }
 
 // The step's public status record; runs after k_xupdate (every owner's reduce has
@@ -797,11 +843,14 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
         e = cudaLaunchCooperativeKernel((const void*)k_xstep1, dim3((unsigned)L.grid_xstep), dim3(kThreads), params, 0, s);
     }
     if (e != cudaSuccess) return e;
-    const int64_t gsh = a.x.lay.shard >> 3;
-    (void)gsh;
-    const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits);
     const bool pdl = (L.pdl_mask & 4) == 0;   // bit 4 (diagnostics): launch k_xupdate after k_xstep1 completes
-    e = launch_pdl_if(pdl, pick_variant<XUpdateK>(a.c, a.ctab != nullptr), grid, kThreads, s, a);
+    if (a.rout) {   // lmsgd_exchange: the all-gather into the caller's buffer instead of the update
+        const int grid = (int)((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu);
+        e = launch_pdl_if(pdl, k_xgather, grid, kThreads, s, a);
+    } else {
+        const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits);
+        e = launch_pdl_if(pdl, pick_variant<XUpdateK>(a.c, a.ctab != nullptr), grid, kThreads, s, a);
+    }
     if (e != cudaSuccess) return e;
     return launch_pdl_if(true, k_xfinalize, 1, 32, s, a, (unsigned int)L.grid_xstep);
 }
@@ -855,6 +904,10 @@ int64_t host_units(const XArgs& x) {
 
 cudaError_t launch_advance1(cudaStream_t s, const Dev1& dv, int64_t* last, bool fused) {
     return launch_pdl_if(true, k_advance1, 1, 32, s, dv, last, fused ? 1 : 0);
+}
+
+cudaError_t launch_xfinal1(cudaStream_t s, const int64_t* st, int64_t* st_next, int64_t* last) {
+    return launch_pdl_if(true, k_xfinal1, 1, 32, s, st, st_next, last);
 }
 
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last) {

@@ -83,6 +83,8 @@ cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64
 // graph mode, k = 1: publish the fused step's status (fused) and advance the counters
 cudaError_t launch_advance1(cudaStream_t s, const Dev1& dv, int64_t* last, bool fused);
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last);
+// lmsgd_exchange at world == 1: status record of the pack, next slot cleared
+cudaError_t launch_xfinal1(cudaStream_t s, const int64_t* st, int64_t* st_next, int64_t* last);
 int stream_blocks_per_sm();
 
 // ---- world > 1 exchange over peer memory (NVLink / NVSwitch)
@@ -120,6 +122,8 @@ struct XStep {
     const UpdConst* ctab;    // graph mode: device coefficient table (lmsgd_schedule_upload), else NULL
     int64_t ctab_count;
     int64_t* cursor;         // graph mode: device index of the next step's coefficients
+    uint16_t* rout;          // lmsgd_exchange: the caller's [n_pad] all-reduce output (k_xgather
+                             // replaces k_xupdate); NULL for a step
 };
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a);
 int xstep_blocks_per_sm();

@@ -78,6 +78,7 @@ def _load() -> ctypes.CDLL:
         "lmsgd_finalize": (I32, [P]),
         "lmsgd_last_error": (ctypes.c_char_p, [P]),
         "lmsgd_step": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs)]),
+        "lmsgd_exchange": (I32, [P, P, P, P]),
         "lmsgd_step_host": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs), P]),
         "lmsgd_bn_stats_allreduce": (I32, [P, P, P, P, I64]),
         "lmsgd_set_weight_decay": (I32, [P, ctypes.c_double, I64]),
@@ -244,6 +245,19 @@ def lmsgd_step(ctx: Context, params, grads, delta, m, coeffs: Coeffs, stream=Non
     _check(_lib.lmsgd_step(ctx.ptr, _stream(stream), _ptr(params, torch.float32, "params"),
                            _ptr(grads, torch.float32, "grads"), _ptr(delta, torch.float32, "delta"),
                            _ptr(m, torch.float32, "m"), ctypes.byref(coeffs)), ctx)
+
+
+def lmsgd_exchange(ctx: Context, grads, R_out, stream=None):
+    """fp16 all-reduce alone (rows a2-a4): R_out [n_pad] (int16/uint16 tensor of
+    binary16 bits) <- sat16(sum over ranks of sat16(s g)), identical on every rank."""
+    import torch
+    if grads.numel() != ctx.n:
+        raise ValueError(f"grads must have n_params = {ctx.n} elements")
+    _, n_pad = lmsgd_layout(ctx.world, ctx.n)
+    if R_out.numel() != n_pad or R_out.element_size() != 2:
+        raise ValueError(f"R_out must be a 2-byte tensor of n_pad = {n_pad} elements")
+    _check(_lib.lmsgd_exchange(ctx.ptr, _stream(stream), _ptr(grads, torch.float32, "grads"),
+                               _ptr(R_out, None, "R_out")), ctx)
 
 
 def lmsgd_set_weight_decay(ctx: Context, lam: float, n_decay: int = -1):

@@ -184,6 +184,42 @@ def main():
     code, st = L.lmsgd_query_status(ctx)
     assert code == 0 and np.array_equal(-H(d), exchange.exchange(list(g), S).ghat)
 
+    # ---- the fp16 all-reduce alone (lmsgd_exchange, rows a2-a4): R bit-exact on every
+    #      rank, interleaved with steps on the same context (one epoch counter)
+    _, n_pad = L.lmsgd_layout(world, n)
+    Rg = torch.full((n_pad,), -1, dtype=torch.int16, device=dev)
+    for t in (10, 11):
+        g = synth.grads(world, t, n)
+        g[:, 5] = 60000.0 / S                  # the sum saturates
+        L.lmsgd_exchange(ctx, D(g[rank]), Rg)
+        code, st = L.lmsgd_query_status(ctx)
+        ex = exchange.exchange(list(g), S)
+        R = H(Rg).view(np.uint16)
+        assert code == 0 and st.skipped == 0 and np.array_equal(R[:n], ex.R), "exchange R not bit-exact"
+        assert not R[n:].any(), "exchange padding not zero"
+        assert st.pack_saturations == ex.pack_saturations and st.sum_saturations == ex.sum_saturations >= 1
+        replicas_identical(Rg.view(torch.int32))   # NCCL has no int16
+        L.lmsgd_step(ctx, th, D(g[rank]), d, m, L.make_coeffs(1.0, 1.0, 0.0))   # a step in between
+        code, st = L.lmsgd_query_status(ctx)
+        assert code == 0 and np.array_equal(-H(d), ex.ghat)
+    g = synth.grads(world, 12, n)
+    g[world - 1, 777] = np.inf
+    L.lmsgd_exchange(ctx, D(g[rank]), Rg)
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == L.LMSGD_ERR_NONFINITE and st.skipped == 1 and st.first_nonfinite == 777, (code, st.first_nonfinite)
+    for nx in (1, 100, 64 * world + 3, 123_457):
+        cx = L.lmsgd_init(world, rank, local, nx, S)
+        L.connect_process_group(cx)
+        _, npx = L.lmsgd_layout(world, nx)
+        Rx = torch.full((npx,), -1, dtype=torch.int16, device=dev)
+        g = synth.grads(world, 3, nx)
+        L.lmsgd_exchange(cx, D(g[rank]), Rx)
+        code, st = L.lmsgd_query_status(cx)
+        R = H(Rx).view(np.uint16)
+        assert code == 0 and np.array_equal(R[:nx], exchange.exchange(list(g), S).R) and not R[nx:].any(), nx
+        dist.barrier()
+        L.lmsgd_finalize(cx)
+
     # ---- BN last-minibatch statistics average
     for C in (1, 64, sum(synth.resnet_bn_channels(50))):
         mean_all, var_all = synth.bn_stats(world, C, seed=C)

@@ -307,6 +307,39 @@ def test_simulated_k_exchange_bit_exact(k):
     assert np.array_equal(-host(d), ex.ghat)
 
 
+def test_k1_exchange_through_ctx():
+    # lmsgd_exchange at world 1: R = the packed gradient, status of the pack,
+    # interleaved with steps on the same context
+    n, s = 100_003, 1024.0
+    _, n_pad = L.lmsgd_layout(1, n)
+    ctx = L.lmsgd_init(1, 0, 0, n, s)
+    Rg = torch.full((n_pad,), -1, dtype=torch.int16, device=DEV)
+    th, d, m = (dev(np.zeros(n, np.float32)) for _ in range(3))
+    for t in (1, 2, 3):
+        g = synth.grads(1, t, n)
+        g[0, 7] = 70000.0 / s
+        L.lmsgd_exchange(ctx, dev(g[0]), Rg)
+        code, st = L.lmsgd_query_status(ctx)
+        ex = exchange.exchange(list(g), s)
+        R = host(Rg).view(np.uint16)
+        assert code == 0 and st.skipped == 0 and np.array_equal(R[:n], ex.R) and not R[n:].any()
+        assert st.pack_saturations == ex.pack_saturations == 1 and st.sum_saturations == 0
+        L.lmsgd_step(ctx, th, dev(g[0]), d, m, L.make_coeffs(1.0, 1.0, 0.0))
+        code, st = L.lmsgd_query_status(ctx)
+        assert code == 0 and st.skipped == 0 and st.pack_saturations == 1
+    g = synth.grads(1, 4, n)
+    g[0, [99, 12]] = [np.nan, -np.inf]
+    L.lmsgd_exchange(ctx, dev(g[0]), Rg)
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == L.LMSGD_ERR_NONFINITE and st.skipped == 1 and st.first_nonfinite == 12
+    g = synth.grads(1, 5, n)
+    L.lmsgd_exchange(ctx, dev(g[0]), Rg)          # the next call is clean again
+    code, st = L.lmsgd_query_status(ctx)
+    assert code == 0 and st.first_nonfinite == -1 and np.array_equal(host(Rg).view(np.uint16)[:n],
+                                                                       exchange.exchange(list(g), s).R)
+    L.lmsgd_finalize(ctx)
+
+
 def test_fused_step1_matches_pack_update():
     n = 777_777
     th0, d0, m0 = init_state(n)
