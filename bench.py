@@ -491,7 +491,9 @@ def main():
     barrier()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / ke
     e2e = {"value": world * 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 4 * n,
-           "d2h_bytes_per_step": ctypes.sizeof(L.StepStatus), "ms_per_step": e2e_ms, "steps": ke}
+           "d2h_bytes_per_step": ctypes.sizeof(L.StepStatus), "ms_per_step": e2e_ms, "steps": ke,
+           # PCIe-bound: the copy of step t+1 overlaps the kernels of step t (lmsgd_step_host)
+           "h2d_gbs": 4 * n / (e2e_ms * 1e-3) / 1e9}
 
     # N = 1 guarded default: also time the single-pass fused variant (LMSGD_FLAG_NO_SKIP,
     # BASELINE.json configs[1] "fused fp16-pack + blended update"; 28 vs 32 B/elem)

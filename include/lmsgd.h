@@ -200,9 +200,13 @@ lmsgd_status lmsgd_step(lmsgd_ctx* ctx, void* stream, float* params, const float
                         float* delta, float* m, const lmsgd_coeffs* coeffs);
 
 /* The same iteration with the gradient in HOST memory (pinned for full speed):
- * copies grads_host -> device inside the call's stream work, runs lmsgd_step and
- * copies the step status back into *status_host (valid once `stream` has passed
- * this point).  The end-to-end entry point bench.py times as "e2e". */
+ * copies grads_host -> device, runs lmsgd_step and copies the step status back into
+ * *status_host (valid once `stream` has passed this point).  The copy runs on a
+ * library-owned copy stream into one of two device staging buffers and may start as
+ * soon as the call is made (grads_host must be complete then, and unchanged until
+ * `stream` passes this point); `stream` waits for it.  Consecutive calls therefore
+ * overlap the host->device copy of step t+1 with the kernels of step t.  The
+ * end-to-end entry point bench.py times as "e2e". */
 lmsgd_status lmsgd_step_host(lmsgd_ctx* ctx, void* stream, float* params, const float* grads_host,
                              float* delta, float* m, const lmsgd_coeffs* coeffs,
                              lmsgd_step_status* status_host);

@@ -39,7 +39,12 @@ struct lmsgd_ctx {
     int64_t ctab_count = 0, ctab_cap = 0;
     int mode = 0;                     // 0 unused, 1 lmsgd_step, 2 lmsgd_step_graph (not mixed)
     int64_t* last = nullptr;          // device lmsgd_step_status of the last step
-    float* d_grads = nullptr;         // device staging for lmsgd_step_host (lazy)
+    // lmsgd_step_host: two device staging buffers filled by a copy stream, so the
+    // host->device copy of step i+1 overlaps the kernels of step i (lazy)
+    float* d_grads[2] = {nullptr, nullptr};
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_consumed[2] = {nullptr, nullptr};
+    int host_buf = 0;
     uint32_t step = 0, bn_calls = 0;
     cudaStream_t last_stream = nullptr;
     lmsgd::Launch L{};
@@ -344,7 +349,12 @@ lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
         if (c->dstate) cudaFree(c->dstate);
         if (c->d_ctab) cudaFree(c->d_ctab);
         if (c->last) cudaFree(c->last);
-        if (c->d_grads) cudaFree(c->d_grads);
+        for (int b = 0; b < 2; ++b) {
+            if (c->d_grads[b]) cudaFree(c->d_grads[b]);
+            if (c->ev_copied[b]) cudaEventDestroy(c->ev_copied[b]);
+            if (c->ev_consumed[b]) cudaEventDestroy(c->ev_consumed[b]);
+        }
+        if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
         if (c->d_trace) cudaFree(c->d_trace);
         for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
         for (auto e : c->pool) cudaEventDestroy(e);
@@ -500,11 +510,26 @@ lmsgd_status lmsgd_step_host(lmsgd_ctx* c, void* stream, float* params, const fl
     if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
     if (!grads_host || !status_host) return fail(c, LMSGD_ERR_INVALID_ARG, "NULL host pointer");
     DeviceGuard g(c->device);
-    if (!c->d_grads) CK(c, cudaMalloc(&c->d_grads, c->n * sizeof(float)));
+    if (!c->copy_stream) {
+        CK(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+        for (int b = 0; b < 2; ++b) {
+            CK(c, cudaMalloc(&c->d_grads[b], c->n * sizeof(float)));
+            CK(c, cudaEventCreateWithFlags(&c->ev_copied[b], cudaEventDisableTiming));
+            CK(c, cudaEventCreateWithFlags(&c->ev_consumed[b], cudaEventDisableTiming));
+            CK(c, cudaEventRecord(c->ev_consumed[b], c->copy_stream));
+        }
+    }
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    CK(c, cudaMemcpyAsync(c->d_grads, grads_host, c->n * sizeof(float), cudaMemcpyHostToDevice, s));
-    const lmsgd_status st = lmsgd_step(c, stream, params, c->d_grads, delta, m, coeffs);
+    const int b = c->host_buf;
+    c->host_buf ^= 1;
+    // buffer b is free once the step that last read it has passed on its stream
+    CK(c, cudaStreamWaitEvent(c->copy_stream, c->ev_consumed[b], 0));
+    CK(c, cudaMemcpyAsync(c->d_grads[b], grads_host, c->n * sizeof(float), cudaMemcpyHostToDevice, c->copy_stream));
+    CK(c, cudaEventRecord(c->ev_copied[b], c->copy_stream));
+    CK(c, cudaStreamWaitEvent(s, c->ev_copied[b], 0));
+    const lmsgd_status st = lmsgd_step(c, stream, params, c->d_grads[b], delta, m, coeffs);
     if (st != LMSGD_OK) return st;
+    CK(c, cudaEventRecord(c->ev_consumed[b], s));
     CK(c, cudaMemcpyAsync(status_host, c->last, sizeof(lmsgd_step_status), cudaMemcpyDeviceToHost, s));
     return LMSGD_OK;
 }
