@@ -45,6 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
            "-Xlinker", "--no-undefined", "-DLMSGD_BUILD", "-o", LIB + ".tmp", *srcs]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    extra = os.environ.get("LMSGD_NVCC_EXTRA", "").split()   # A/B experiments (e.g. -DLMSGD_XSTEP_MINB=8)
+    cmd[1:1] = extra
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + " ".join(cmd) + "\n" + r.stdout + r.stderr)

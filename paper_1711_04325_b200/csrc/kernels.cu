@@ -480,7 +480,11 @@ __device__ __forceinline__ bool spin_flag(const XArgs& x, const Ep& ep, const ui
 // the update of early chunks overlaps the reduce of later ones.
 // k_xfinalize -- one warp: the step's public status record.
 // Chunk counters in a.ctr are reset by the block that completes them.
-__global__ void __launch_bounds__(kThreads) k_xstep1(XStep a) {
+#ifndef LMSGD_XSTEP_MINB
+#define LMSGD_XSTEP_MINB 8   // k_xstep1 capped at 32 registers: 8 blocks/SM (A/B at k = 4: 214.9 vs
+                             // 225.6 us per step with no cap, 48 registers, 5 blocks/SM)
+#endif
+__global__ void __launch_bounds__(kThreads, LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     pdl_enter();   // wait for the previous step / caller work; let k_xupdate queue up
     const XArgs& x = a.x;
     const Ep ep = get_ep(x);
