@@ -23,10 +23,38 @@
 namespace lmsgd {
 namespace {
 
-constexpr int kThreads = 256;
+constexpr int kThreads = 256;   // LMSGD_LB below spells the same block size
 constexpr int kXUnits = 1;   // k_xupdate: 2048-element units per block
 enum { FLAG_A = 0, FLAG_C = 2, FLAG_D = 3 };  // A: a rank's pack+push is done; C: BN staged;
                                              // D (local): this step's skip decision is stored
+
+// Minimum resident blocks per SM asked of ptxas (register caps), A/B knobs set with
+// LMSGD_NVCC_EXTRA in build.py; 0 = ptxas' default heuristic (which is NOT the same as
+// an explicit 1: that lets ptxas use up to 255 registers, 76 for k_update).  Measured
+// (profiles/r1/ab/update_caps.txt, one box, 5 runs): k_xupdate capped at 6 or 5
+// blocks/SM moves the k = 4 step by -3.5 .. +0.6 us (noise), k_update capped at 5 by
+// +0.7 us, k_fused1 capped at 5 by +7 us -- all stay at the default.  Only k_xstep1
+// gains from its cap (LMSGD_XSTEP_MINB).
+#ifndef LMSGD_UPD_MINB
+#define LMSGD_UPD_MINB 0    // k_update
+#endif
+#ifndef LMSGD_FUSED_MINB
+#define LMSGD_FUSED_MINB 0  // k_fused1
+#endif
+#ifndef LMSGD_XUPD_MINB
+#define LMSGD_XUPD_MINB 0   // k_xupdate
+#endif
+#define LMSGD_LB_0 __launch_bounds__(256)
+#define LMSGD_LB_1 __launch_bounds__(256, 1)
+#define LMSGD_LB_2 __launch_bounds__(256, 2)
+#define LMSGD_LB_3 __launch_bounds__(256, 3)
+#define LMSGD_LB_4 __launch_bounds__(256, 4)
+#define LMSGD_LB_5 __launch_bounds__(256, 5)
+#define LMSGD_LB_6 __launch_bounds__(256, 6)
+#define LMSGD_LB_7 __launch_bounds__(256, 7)
+#define LMSGD_LB_8 __launch_bounds__(256, 8)
+#define LMSGD_LB_(b) LMSGD_LB_##b
+#define LMSGD_LB(b) LMSGD_LB_(b)
 
 // ------------------------------------------------------------------ helpers
 
@@ -270,7 +298,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_local(const uint16_t* __res
 }
 
 template <bool RMS, bool WD, bool KM>
-__global__ void __launch_bounds__(kThreads) k_update(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
+__global__ void LMSGD_LB(LMSGD_UPD_MINB) k_update(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
                                                      float* __restrict__ th, float* __restrict__ d,
                                                      float* __restrict__ m, const int64_t* st,
                                                      int64_t* st_reset, int64_t* last, Dev1 dv) {
@@ -303,7 +331,7 @@ __global__ void __launch_bounds__(kThreads) k_update(const uint16_t* __restrict_
 // k = 1 single pass (LMSGD_FLAG_NO_SKIP): h = sat16(s g) kept in registers,
 // ghat = fp32(h) / s, update.  28 B/elem of HBM traffic.
 template <bool RMS, bool WD, bool KM>
-__global__ void __launch_bounds__(kThreads) k_fused1(const float* __restrict__ g, int64_t n, float s,
+__global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1(const float* __restrict__ g, int64_t n, float s,
                                                      UpdConst c, float* __restrict__ th,
                                                      float* __restrict__ d, float* __restrict__ m,
                                                      int64_t* st, int64_t* st_reset, Dev1 dv) {
@@ -484,7 +512,7 @@ __device__ __forceinline__ bool spin_flag(const XArgs& x, const Ep& ep, const ui
 #define LMSGD_XSTEP_MINB 8   // k_xstep1 capped at 32 registers: 8 blocks/SM (A/B at k = 4: 214.9 vs
                              // 225.6 us per step with no cap, 48 registers, 5 blocks/SM)
 #endif
-__global__ void __launch_bounds__(kThreads, LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
+__global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     pdl_enter();   // wait for the previous step / caller work; let k_xupdate queue up
     const XArgs& x = a.x;
     const Ep ep = get_ep(x);
@@ -592,7 +620,7 @@ __global__ void __launch_bounds__(kThreads, LMSGD_XSTEP_MINB) k_xstep1(XStep a) 
 }
 
 template <bool RMS, bool WD, bool KM>
-__global__ void __launch_bounds__(kThreads) k_xupdate(XStep a) {
+__global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
     // no griddepcontrol.wait: ordering with k_xstep1 is by flags D and cflag.
     // kXUnits units per block: 2 was faster in isolation (tools/xbench.cu, 109 vs
     // 120 us) but slower in the step (225 vs 215 us at k = 4), so 1.
