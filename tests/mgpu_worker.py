@@ -8,6 +8,9 @@ Checks on world = k real GPUs over NVLink, through the C ABI:
   * a non-finite gradient on one rank skips the step on every rank, same status;
   * saturation counts summed over ranks;
   * BN statistics average bit-exact vs the oracle;
+  * lmsgd_exchange (the fp16 all-reduce alone): R bit-exact, interleaved with steps;
+  * 10^4 steps under random per-rank device skew: replicas bit-identical and equal to
+    the same sequence without skew (the flag / epoch / status-slot protocol);
   * the full 25.6M ResNet-50 buffer (sampled check) in bench.py's launch configuration.
 Exit code 0 and "MGPU_OK" on rank 0 when everything passes.
 """
@@ -321,6 +324,45 @@ def main():
             check_state(H(th), H(d), H(m), *prev, exchange.exchange(list(g), S).ghat, schedule.coeffs_at(t))
         replicas_identical(th, d, m)
     L.lmsgd_finalize(ctx)
+
+    # ---- cross-GPU flag protocol under skew: 10^4 steps,
+    #      random per-rank device delays before a step, exchanges and non-finite steps
+    #      interleaved; the final state must be bit-identical on every rank AND to the same
+    #      sequence run without delays
+    n = 100_003
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(77 + rank)
+    pool = [torch.randn(n, generator=gen, device=dev) * 1e-3 for _ in range(8)]
+    bad = pool[0].clone()
+    bad[12_345] = float("nan")
+    rbuf = torch.empty(L.lmsgd_layout(world, n)[1], dtype=torch.int16, device=dev)
+    finals = []
+    for delayed in (False, True):
+        ctx = L.lmsgd_init(world, rank, local, n, S)
+        L.connect_process_group(ctx)
+        th = D(synth.theta0(n, None))
+        d, m = torch.zeros(n, device=dev), torch.zeros(n, device=dev)
+        rng = np.random.default_rng(1234 + (rank if delayed else 0))
+        for it in range(10_000):
+            if delayed and rng.random() < 0.3:
+                torch.cuda._sleep(int(rng.integers(1, 200_000)))   # up to ~100 us of device skew
+            if it % 97 == 13:
+                L.lmsgd_exchange(ctx, pool[it % 8], rbuf)
+            elif it % 501 == 7:
+                L.lmsgd_step(ctx, th, bad if rank == it % world else pool[it % 8], d, m,
+                             L.lmsgd_schedule_at(None, C1_C, 1 + it % 30))
+                code, st = L.lmsgd_query_status(ctx)
+                assert code == L.LMSGD_ERR_NONFINITE and st.first_nonfinite == 12_345, (it, code)
+            else:
+                L.lmsgd_step(ctx, th, pool[it % 8], d, m, L.lmsgd_schedule_at(None, C1_C, 1 + it % 30))
+        code, st = L.lmsgd_query_status(ctx)
+        assert code == 0 and st.skipped == 0, code
+        finals.append((th.clone(), d.clone(), m.clone()))
+        replicas_identical(th, d, m)
+        dist.barrier()
+        L.lmsgd_finalize(ctx)
+    for a_, b_ in zip(*finals):
+        assert torch.equal(a_, b_), "state depends on cross-GPU timing"
 
     # ---- full ResNet-50 buffer, sampled check
     n = synth.resnet_n_params(50)
