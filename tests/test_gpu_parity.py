@@ -272,6 +272,23 @@ def test_pack_vs_oracle_codec_boundary_classes():
         assert st[1] == sat and st[0] == np.iinfo(np.int64).max
 
 
+@pytest.mark.skipif(__import__("os").environ.get("LMSGD_EXHAUSTIVE") != "1", reason="set LMSGD_EXHAUSTIVE=1")
+def test_pack_all_fp32_patterns_vs_oracle():
+    # k_pack (s = 1) on every one of the 2^32 fp32 bit patterns against the oracle codec,
+    # 2^24 patterns per launch; non-finite patterns: only the first-index status counts
+    step = 1 << 24
+    for hi in range(0, 1 << 32, step):
+        pat = np.arange(hi, hi + step, dtype=np.uint64).astype(np.uint32)
+        x = pat.view(np.float32)
+        got, st = _pack_codec_case(x, 1.0)
+        fin = np.isfinite(x)
+        ref, sat = binary16.to_binary16(x[fin], return_saturation=True)
+        assert np.array_equal(got[fin], ref), hex(hi)
+        assert st[1] == sat
+        first = np.iinfo(np.int64).max if fin.all() else int(np.argmin(fin))
+        assert st[0] == first, hex(hi)
+
+
 def test_pack_nonfinite_first_index():
     x = np.ones(1000, np.float32)
     x[[500, 17, 999]] = [np.nan, np.inf, -np.inf]
