@@ -358,6 +358,25 @@ def main():
             trace = {"us_median_per_rank": allr}
             worst = {k: max(r[k] for r in allr) for k in ("pack", "update", "step")}
             prof = {"pack": (worst["pack"] * 1e-3, 1), "update": (worst["update"] * 1e-3, 1)}
+    # 3) per-step distribution (median, p10, p90): a CUDA event pair
+    #    around each of up to 500 steps, the max over ranks per step
+    dist_us = None
+    if not args.no_profile and not args.full_schedule:
+        ks = min(args.steps, 500)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(ks)]
+        barrier()
+        torch.cuda.synchronize()
+        for i in range(ks):
+            evs[i][0].record(stream)
+            step(args.warmup + i)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        per = torch.tensor([a.elapsed_time(b) * 1e3 for a, b in evs], dtype=torch.float64, device=devc)
+        if world > 1:
+            dist.all_reduce(per, op=dist.ReduceOp.MAX)
+        q = torch.quantile(per.cpu(), torch.tensor([0.1, 0.5, 0.9], dtype=torch.float64)).tolist()
+        dist_us = {"steps": ks, "p10": q[0], "median": q[1], "p90": q[2],
+                   "note": "one event pair per step (breaks the launch overlap between steps); max over ranks"}
     ms_per_step = ms / args.steps
     global_steps_per_s = 1e3 / ms_per_step
     value = global_steps_per_s * world
@@ -581,6 +600,7 @@ def main():
             "cpu_baseline": cpu, "e2e": e2e,
             "clocks": ck, "gpu_launches": kernels_per_step * args.steps,
             "profile_pass_ms_per_step": (ms_prof / args.steps) if ms_prof else None,
+            "step_us_distribution": dist_us,
             "host_enqueue_us_per_step": host_us_per_step,
             "full_schedule": ({"steps": args.steps, "bn_syncs": len(bn_at), "total_s": ms / 1e3,
                                "note": "config C5: whole 90-epoch slow-start / RMSprop warm-up schedule"}
