@@ -39,3 +39,13 @@ def test_exchange_three_ranks():
 def test_exchange_two_ranks_and_timeout():
     # a rank that never steps makes the other time out (status, no hang)
     _run(2, 29535, {"LMSGD_TEST_TIMEOUT": "1", "LMSGD_TIMEOUT_MS": "3000"})
+
+
+@pytest.mark.skipif(not (2 <= NGPU < 8), reason="needs 2..7 GPUs (8 GPUs run world 8 natively)")
+def test_world8_oversubscribed():
+    # world = 8 code paths with two or more ranks per GPU (time-sliced; correctness only)
+    env = dict(os.environ, LMSGD_TIMEOUT_MS="120000", PYTHONPATH=ROOT)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr=127.0.0.1", "--master-port=29536", os.path.join(ROOT, "tests", "oversub_worker.py")]
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0 and "OVERSUB_OK world=8" in r.stdout, r.stdout[-4000:] + r.stderr[-4000:]
