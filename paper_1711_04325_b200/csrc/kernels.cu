@@ -490,6 +490,29 @@ __device__ __forceinline__ bool spin_flag(const XArgs& x, const Ep& ep, const ui
     return true;
 }
 
+// Chunk flags carry the step's skip decision with the epoch: value 2 e + skip.  A
+// consumer then needs one acquire load (no separate wait for flag D and no status
+// reads before its update).  The value is exactly 2 e or 2 e + 1 once ready: the next
+// step's reduce cannot publish before every rank has finished this step's update.
+__device__ __forceinline__ bool spin_cflag(const XArgs& x, const Ep& ep, const uint32_t* f, uint32_t& v) {
+    const uint64_t t0 = globaltimer();
+    const uint32_t want = ep.e << 1;
+    while ((int32_t)((v = ld_acquire_sys(f)) - want) < 0) {
+        __nanosleep(32);
+        if ((int64_t)(globaltimer() - t0) > x.timeout_ns) return false;
+    }
+    return true;
+}
+
+// The chunk-flag value of this step: waits for the local decision (flag D, stored by
+// block 0 long before any chunk completes) and encodes skip.
+__device__ __forceinline__ uint32_t cflag_value(const XArgs& x, const Ep& ep) {
+    if (!spin_flag(x, ep, flag_slot(x, x.rank, FLAG_D))) return (ep.e << 1) | 1u;
+    const volatile int64_t* vm = status_of(x, ep, x.rank);
+    const bool skip = vm[ST_G_FIRST] != kNone || vm[ST_G_ERROR] != 0;
+    return (ep.e << 1) | (skip ? 1u : 0u);
+}
+
 // The world > 1 step in two kernels.
 //
 // k_xstep1 -- persistent, cooperatively launched (all blocks co-resident, so blocks
@@ -604,13 +627,15 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     __threadfence_system();
     __syncthreads();
     if (t0) {
+        uint32_t fv = 0;
         for (int64_t u = blockIdx.x; u < ups; u += gridDim.x) {
             const int c = (int)(u / x.lay.cu);
             const int64_t rem = ups - (int64_t)c * x.lay.cu;
             const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
             if (atomicAdd(a.ctr + 4 + c, 1u) + 1u == cnt) {
                 a.ctr[4 + c] = 0;
-                for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, c, x.rank), ep.e);
+                if (!fv) fv = cflag_value(x, ep);
+                for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, c, x.rank), fv);
             }
         }
     }
@@ -621,7 +646,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
 
 template <bool RMS, bool WD, bool KM>
 __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
-    // no griddepcontrol.wait: ordering with k_xstep1 is by flags D and cflag.
+    // no griddepcontrol.wait: ordering with k_xstep1 is by the chunk flags.
     // kXUnits units per block: 2 was faster in isolation (tools/xbench.cu, 109 vs
     // 120 us) but slower in the step (225 vs 215 us at k = 4), so 1.
     const XArgs& x = a.x;
@@ -655,18 +680,19 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
     }
     if (threadIdx.x == 0) {
         if (blockIdx.x == 0) stamp(x, TR_UPD_START);
-        int go = spin_flag(x, ep, flag_slot(x, x.rank, FLAG_D)) ? 1 : 0;
-        if (go) {
-            // wait for the owners' chunks even when the step is skipped: the step may
-            // end only after every owner's reduce has finished reading its receive slots
-            for (int v = 0; v < kXUnits; ++v)
-                if (us[v] < ups && !spin_flag(x, ep, cflag(x, x.rank, cch[v], owner[v]))) {
-                    go = 0;
-                    status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-                    break;
-                }
-            const volatile int64_t* vm = status_of(x, ep, x.rank);
-            if (vm[ST_G_FIRST] != kNone || vm[ST_G_ERROR] != 0) go = 0;   // skipped step
+        // wait for the owners' chunks even when the step is skipped: the step may end
+        // only after every owner's reduce has finished reading its receive slots.  The
+        // chunk flag carries the skip decision (spin_cflag).
+        int go = 1;
+        for (int v = 0; v < kXUnits; ++v) {
+            if (us[v] >= ups) continue;
+            uint32_t fv;
+            if (!spin_cflag(x, ep, cflag(x, x.rank, cch[v], owner[v]), fv)) {
+                go = 0;
+                status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+                break;
+            }
+            if (fv & 1u) go = 0;   // skipped step
         }
         if (blockIdx.x == 0) stamp(x, TR_UPD_GO);
         s_go = go;
@@ -688,7 +714,7 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
 
 // lmsgd_exchange, world > 1: the all-gather half of the fp16 all-reduce (row a4) on
 // its own, as a flat pull into the caller's buffer.  Same unit order and waits as
-// k_xupdate (chunk-major, owner-interleaved; flag D, then the owner's chunk flag),
+// k_xupdate (chunk-major, owner-interleaved; the owner's chunk flag),
 // then one 16-byte peer load and one local store per thread.  The reduced values
 // are copied whether or not a gradient was non-finite (the status says so).
 // Measured (k = 2, 51 MB): 123 us for the whole exchange, against 137 us with the
@@ -706,8 +732,9 @@ __global__ void __launch_bounds__(kThreads) k_xgather(XStep a) {
     const int64_t u = c < x.lay.nchunks ? (int64_t)c * x.lay.cu + r / x.world : ups;
     __shared__ int s_go;
     if (threadIdx.x == 0) {
-        int go = spin_flag(x, ep, flag_slot(x, x.rank, FLAG_D)) ? 1 : 0;
-        if (go && u < ups && !spin_flag(x, ep, cflag(x, x.rank, c, owner))) {
+        int go = 1;
+        uint32_t fv;
+        if (u < ups && !spin_cflag(x, ep, cflag(x, x.rank, c, owner), fv)) {
             go = 0;
             status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
         }
