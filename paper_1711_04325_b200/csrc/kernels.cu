@@ -24,7 +24,10 @@ namespace lmsgd {
 namespace {
 
 constexpr int kThreads = 256;   // LMSGD_LB below spells the same block size
-constexpr int kXUnits = 1;   // k_xupdate: 2048-element units per block
+#ifndef LMSGD_XUNITS
+#define LMSGD_XUNITS 2   // A/B at k = 4 (profiles/r1/ab/xunits_n4.txt): 201.9 vs 206.8 us per step with 1
+#endif
+constexpr int kXUnits = LMSGD_XUNITS;   // k_xupdate: 2048-element units per block
 enum { FLAG_A = 0, FLAG_C = 2, FLAG_D = 3 };  // A: a rank's pack+push is done; C: BN staged;
                                              // D (local): this step's skip decision is stored
 
@@ -647,8 +650,9 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
 template <bool RMS, bool WD, bool KM>
 __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
     // no griddepcontrol.wait: ordering with k_xstep1 is by the chunk flags.
-    // kXUnits units per block: 2 was faster in isolation (tools/xbench.cu, 109 vs
-    // 120 us) but slower in the step (225 vs 215 us at k = 4), so 1.
+    // kXUnits units per block (LMSGD_XUNITS): with one acquire per unit (chunk flags
+    // carrying the decision), 2 units beat 1 in the step; with the older flag-D protocol
+    // 1 had been faster (225 vs 215 us at k = 4).
     const XArgs& x = a.x;
     const Ep ep = get_ep(x);
     __shared__ UpdConst s_c;
@@ -662,43 +666,49 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
             s_c = a.ctab[s_range ? a.ctab_count - 1 : idx];
         }
     }
-    __shared__ int s_go;
+    __shared__ int s_ok[kXUnits];
     const int64_t gsh = x.lay.shard >> 3;
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
     const int64_t kcu = (int64_t)x.world * x.lay.cu;
+    auto unit_of = [&](int v, int& owner, int64_t& u, int& c) {   // chunk-major, owner-interleaved
+        const int64_t i = (int64_t)blockIdx.x * kXUnits + v;
+        c = (int)(i / kcu);
+        const int64_t r = i - (int64_t)c * kcu;
+        owner = (int)((r % x.world + x.rank) % x.world);
+        u = c < x.lay.nchunks ? (int64_t)c * x.lay.cu + r / x.world : ups;   // ups: past the last unit
+    };
     int owner[kXUnits];
     int64_t us[kXUnits];
     int cch[kXUnits];
 #pragma unroll
-    for (int v = 0; v < kXUnits; ++v) {
-        const int64_t i = (int64_t)blockIdx.x * kXUnits + v;
-        cch[v] = (int)(i / kcu);
-        const int64_t r = i - (int64_t)cch[v] * kcu;
-        owner[v] = (int)((r % x.world + x.rank) % x.world);
-        us[v] = (int64_t)cch[v] * x.lay.cu + r / x.world;
-        if (cch[v] >= x.lay.nchunks) us[v] = ups;   // past the last unit
-    }
-    if (threadIdx.x == 0) {
-        if (blockIdx.x == 0) stamp(x, TR_UPD_START);
-        // wait for the owners' chunks even when the step is skipped: the step may end
-        // only after every owner's reduce has finished reading its receive slots.  The
-        // chunk flag carries the skip decision (spin_cflag).
-        int go = 1;
-        for (int v = 0; v < kXUnits; ++v) {
-            if (us[v] >= ups) continue;
+    for (int v = 0; v < kXUnits; ++v) unit_of(v, owner[v], us[v], cch[v]);
+    // lane 0 of warp v waits for unit v's chunk flag (the waits overlap), even when the
+    // step is skipped: the step may end only after every owner's reduce has finished
+    // reading its receive slots.  The chunk flag carries the skip decision (spin_cflag).
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0 && w < kXUnits) {
+        if (blockIdx.x == 0 && w == 0) stamp(x, TR_UPD_START);
+        int ow, c;
+        int64_t u;
+        unit_of(w, ow, u, c);
+        int ok = 1;
+        if (u < ups) {
             uint32_t fv;
-            if (!spin_cflag(x, ep, cflag(x, x.rank, cch[v], owner[v]), fv)) {
-                go = 0;
+            if (!spin_cflag(x, ep, cflag(x, x.rank, c, ow), fv)) {
+                ok = 0;
                 status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-                break;
+            } else if (fv & 1u) {
+                ok = 0;   // skipped step
             }
-            if (fv & 1u) go = 0;   // skipped step
         }
-        if (blockIdx.x == 0) stamp(x, TR_UPD_GO);
-        s_go = go;
+        s_ok[w] = ok;
     }
     __syncthreads();
-    if (!s_go || s_range) return;
+    int go = 1;
+#pragma unroll
+    for (int v = 0; v < kXUnits; ++v) go &= s_ok[v];
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_UPD_GO);
+    if (!go || s_range) return;
     const UpdConst c = s_c;
 #pragma unroll
     for (int v = 0; v < kXUnits; ++v) {
