@@ -614,7 +614,8 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     }
 
     // ---- 3. exact reduce of this rank's shard, chunk-major over blocks (unit u on
-    //         block u % grid), each chunk released as soon as its units are done.
+    //         block u % grid); a chunk is released when the last block holding one of
+    //         its units has finished all its units.
     //         Runs even for a step that will be skipped (its R is then never read).
     if (blockIdx.x == 0 && t0) stamp(x, TR_RED_GO);
     const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
@@ -625,8 +626,10 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
         if (gi < gsh) reduce8(recv, x.lay.shard, x.world, gi << 3, R, sat);
     }
     flush_status(kNone, sat, mine, ST_SUM_SAT);
-    // one system fence per block (a fence per unit stalls behind the concurrent
-    // update's peer loads), then count this block's units into their chunks
+    // one system fence per block, then count this block's units into their chunks.  A
+    // fence + release after every round (so early chunks go out while later rounds run)
+    // measured slower: reduce 12 -> 34 us, step 204 -> 215 us at k = 4
+    // (profiles/r1/ab/reduce_fence_per_round_n4.txt).
     __threadfence_system();
     __syncthreads();
     if (t0) {
