@@ -731,7 +731,11 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
 // then one 16-byte peer load and one local store per thread.  The reduced values
 // are copied whether or not a gradient was non-finite (the status says so).
 // Measured (k = 2, 51 MB): 123 us for the whole exchange, against 137 us with the
-// gather done inside k_xstep1's persistent grid after its reduce.
+// gather done inside k_xstep1's persistent grid after its reduce; 2, 4 or 8 units per
+// block with overlapped flag waits change nothing (k = 4, 158.5-159.7 us,
+// profiles/r1/ab/gather_units_n4.txt): the pull is NVLink-bound (~600 GB/s in).  The
+// exchange moves 2 x 2 N (k-1)/k bytes out of every GPU (push, then R served to the
+// peers), 76.7 MB at k = 4: 118 us at the ~650 GB/s an SM store stream reaches.
 __global__ void __launch_bounds__(kThreads) k_xgather(XStep a) {
     const XArgs& x = a.x;
     const Ep ep = get_ep(x);
