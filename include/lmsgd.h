@@ -224,7 +224,7 @@ lmsgd_status lmsgd_step_host(lmsgd_ctx* ctx, void* stream, float* params, const 
  * Enqueued on `stream`.  lmsgd_query_status reports the saturation counts and the
  * first non-finite index; a non-finite gradient sets skipped = 1 and error =
  * LMSGD_ERR_NONFINITE and leaves R_out's values unspecified.  world == 1: R_out is
- * the packed gradient (one kernel).  Errors: INVALID_ARG (NULL / misaligned),
+ * the packed gradient (k_pack + a one-warp status kernel).  Errors: INVALID_ARG (NULL / misaligned),
  * STATE (before lmsgd_connect, or on a context that runs lmsgd_step_graph). */
 lmsgd_status lmsgd_exchange(lmsgd_ctx* ctx, void* stream, const float* grads, uint16_t* R_out);
 
