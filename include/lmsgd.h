@@ -245,7 +245,7 @@ lmsgd_status lmsgd_schedule_upload(lmsgd_ctx* ctx, const lmsgd_hyper* hyper, con
  * device at the end of the step.  Safe to capture in a CUDA graph (e.g.
  * torch.cuda.graph): every replay runs the next iteration.  Past the end of the table
  * the update is skipped and the status reports LMSGD_ERR_RANGE.  A context uses
- * either lmsgd_step or lmsgd_step_graph (LMSGD_ERR_STATE otherwise). */
+ * either lmsgd_step / lmsgd_exchange or lmsgd_step_graph (LMSGD_ERR_STATE otherwise). */
 lmsgd_status lmsgd_step_graph(lmsgd_ctx* ctx, void* stream, float* params, const float* grads,
                               float* delta, float* m);
 

@@ -416,6 +416,7 @@ lmsgd_status lmsgd_exchange(lmsgd_ctx* c, void* stream, const float* grads, uint
     const uint32_t epoch = ++c->step;   // one collective epoch, shared with lmsgd_step
     const int parity = static_cast<int>(epoch & 1u);
     c->last_stream = s;
+    c->mode = 1;   // host-mode epochs and status slots, like lmsgd_step (not mixed with graph mode)
     if (c->world == 1) {
         CK(c, timed(c, s, 0, [&] {
                return lmsgd::launch_pack(s, c->L, grads, c->n, c->n_pad, c->scale, R_out, status_slot(c, parity));
@@ -474,7 +475,7 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
         return fail(c, LMSGD_ERR_INVALID_ARG, "params/grads/delta/m must be non-NULL and 16-byte aligned");
     if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
     if (c->ctab_count == 0) return fail(c, LMSGD_ERR_STATE, "lmsgd_schedule_upload has not been called");
-    if (c->mode == 1) return fail(c, LMSGD_ERR_STATE, "this context already runs lmsgd_step");
+    if (c->mode == 1) return fail(c, LMSGD_ERR_STATE, "this context already runs lmsgd_step / lmsgd_exchange");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     UpdConst u{};         // every coefficient comes from the device table; n_wd selects the kernel variant

@@ -354,6 +354,10 @@ def test_k1_exchange_through_ctx():
     code, st = L.lmsgd_query_status(ctx)
     assert code == 0 and st.first_nonfinite == -1 and np.array_equal(host(Rg).view(np.uint16)[:n],
                                                                        exchange.exchange(list(g), s).R)
+    L.lmsgd_schedule_upload(ctx, None, C1_C, 1, 4)
+    with pytest.raises(L.LmsgdError) as e:        # host-mode epochs: no switch to graph mode
+        L.lmsgd_step_graph(ctx, th, dev(g[0]), d, m)
+    assert e.value.status == L.LMSGD_ERR_STATE
     L.lmsgd_finalize(ctx)
 
 
