@@ -349,6 +349,11 @@ def main():
             segs = {"pack": ("pack_start", "pack_end"), "wait_all_packs": ("pack_end", "reduce_start"),
                     "reduce_block0": ("reduce_go", "reduce_end"), "update_first_wait": ("update_start", "update_go"),
                     "update": ("update_go", "update_end"), "step": ("pack_start", "update_end"),
+                    # the update kernel's whole span: its first block's start (which may
+                    # precede the last reduce blocks) to the status record -- used for the
+                    # roofline; "update" starts at block 0's go and can undercount, because
+                    # other blocks run while block 0 still waits for its chunks
+                    "update_span": ("update_start", "update_end"),
                     "publish": ("pack_end", "publish_end")}
             segs.update({f"flag_A_from_{p}": ("pack_end", f"a_seen_{p}") for p in range(world)})
             body = tr[len(tr) // 4:]
@@ -356,8 +361,8 @@ def main():
             allr = [None] * world
             dist.all_gather_object(allr, mine)
             trace = {"us_median_per_rank": allr}
-            worst = {k: max(r[k] for r in allr) for k in ("pack", "update", "step")}
-            prof = {"pack": (worst["pack"] * 1e-3, 1), "update": (worst["update"] * 1e-3, 1)}
+            worst = {k: max(r[k] for r in allr) for k in ("pack", "update_span", "step")}
+            prof = {"pack": (worst["pack"] * 1e-3, 1), "update": (worst["update_span"] * 1e-3, 1)}
     # 3) per-step distribution (median, p10, p90): a CUDA event pair
     #    around each of up to 500 steps, the max over ranks per step
     dist_us = None
@@ -388,7 +393,7 @@ def main():
         if cnt:
             phases[ph] = {"us_per_launch": (max_over_ranks(pms / cnt * 1e3) if world == 1 else pms * 1e3),
                           "launches": cnt if world == 1 else args.steps,
-                          "source": "cuda events" if world == 1 else "in-kernel %globaltimer trace, max over ranks"}
+                          "source": "cuda events" if world == 1 else ("in-kernel %globaltimer trace, max over ranks; update = the k_xupdate span from its first block's start" if ph == "update" else "in-kernel %globaltimer trace, max over ranks")}
     if flags:
         dom, dom_bytes, kname = "pack", FUSED_BYTES_PER_ELEM, "k_fused1"   # phase 0 = the fused kernel
     else:
