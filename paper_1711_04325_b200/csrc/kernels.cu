@@ -24,9 +24,6 @@ namespace lmsgd {
 namespace {
 
 constexpr int kThreads = 256;   // LMSGD_LB below spells the same block size
-#ifndef LMSGD_PUSH_BULK
-#define LMSGD_PUSH_BULK 0   // k_xstep1 push through cp.async.bulk (A/B knob)
-#endif
 #ifndef LMSGD_XUNITS
 #define LMSGD_XUNITS 2   // A/B at k = 4 (profiles/r1/ab/xunits_n4.txt): 201.9 vs 206.8 us per step with 1
 #endif
@@ -552,49 +549,10 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
     int64_t* mine = status_of(x, ep, x.rank);
 
-    // ---- 1. pack + push
-#if LMSGD_PUSH_BULK
-    // variant: the block packs a unit into shared memory and one thread pushes it to
-    // the owner with a 4 KB cp.async.bulk (TMA engine), double-buffered
-    {
-        __shared__ alignas(128) uint4 s_buf[2][kThreads];
-        int64_t first = kNone;
-        unsigned sat = 0;
-        int buf = 0;
-        const int64_t units = (int64_t)x.world * ups;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
-            const int owner = (int)((u % x.world + x.rank) % x.world);
-            const int64_t ubase = (u / x.world) * kThreads;   // first group of the unit
-            if (ubase >= gsh) continue;                       // uniform over the block
-            const int64_t gi = ubase + threadIdx.x;
-            const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
-            float xv[8];
-            if (gi < gsh) {
-                load8_g(a.g, j0, x.n, xv);
-                s_buf[buf][threadIdx.x] = pack8(xv, a.scale, j0, first, sat);
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            __syncthreads();
-            if (t0) {
-                const int64_t ng = gsh - ubase < kThreads ? gsh - ubase : kThreads;
-                uint16_t* dst = reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
-                                (int64_t)x.rank * x.lay.shard + (ubase << 3);
-                const uint32_t src = (uint32_t)__cvta_generic_to_shared(&s_buf[buf][0]);
-                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                             ::"l"(dst), "r"(src), "r"((uint32_t)(ng * 16)) : "memory");
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");   // the other buffer is free
-            }
-            __syncthreads();
-            buf ^= 1;
-        }
-        if (t0) {
-            asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-        }
-        flush_status(first, sat, mine, ST_PACK_SAT);
-    }
-#else
+    // ---- 1. pack + push (16-byte SM stores to the owners; pushing each packed unit as
+    //         one 4 KB cp.async.bulk from shared memory instead measured the same, 66.2
+    //         vs 65.4 us at k = 4: the all-to-all is NVLink-bound at ~575 GB/s per
+    //         direction, profiles/r1/ab/push_bulk_n4.txt)
     {
         int64_t first = kNone;
         unsigned sat = 0;
@@ -612,7 +570,6 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
         }
         flush_status(first, sat, mine, ST_PACK_SAT);
     }
-#endif
     __threadfence_system();
     __syncthreads();
     if (t0 && atomicAdd(a.ctr + 0, 1u) + 1u == gridDim.x) {
