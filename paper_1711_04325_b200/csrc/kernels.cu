@@ -442,30 +442,35 @@ __device__ void publish(const XArgs& x, const Ep& ep, int which) {
 }
 
 
-// One thread: wait until every rank has published `which` for this epoch (bounded
-// spin; on timeout record LMSGD_ERR_TIMEOUT in this rank's words and return false).
-__device__ bool thread_wait_all(const XArgs& x, const Ep& ep, int which, bool trace_seen = false) {
-    const uint64_t t0 = globaltimer();
-    for (int p = 0; p < x.world; ++p) {
+// Warp 0: wait until every rank has published `which` for this epoch, lane p polling
+// rank p's slot (the k acquire round trips overlap instead of running back to back).
+// Bounded spin; on timeout record LMSGD_ERR_TIMEOUT in this rank's words.  Call with all
+// 32 lanes of warp 0; every lane returns the same result.
+__device__ bool warp_wait_all(const XArgs& x, const Ep& ep, int which, bool trace_seen = false) {
+    const int p = threadIdx.x & 31;
+    bool ok = true;
+    if (p < x.world) {
         const uint32_t* f = flag_slot(x, x.rank, which) + p;
-        if (trace_seen && x.trace) {   // per-peer arrival, diagnostics only
-            while ((int32_t)(ld_acquire_sys(f) - ep.e) < 0) {}
-            x.trace[TR_A_SEEN + p] = (int64_t)globaltimer();
-        }
+        const uint64_t t0 = globaltimer();
         while ((int32_t)(ld_acquire_sys(f) - ep.e) < 0) {
             __nanosleep(64);
             if ((int64_t)(globaltimer() - t0) > x.timeout_ns) {
-                int64_t* mine = status_of(x, ep, x.rank);
-                mine[ST_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-                mine[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-                __threadfence_system();
-                return false;
+                ok = false;
+                break;
             }
         }
+        if (ok && trace_seen && x.trace) x.trace[TR_A_SEEN + p] = (int64_t)globaltimer();   // diagnostics
     }
-    // no trailing fence: each ld.acquire.sys orders this thread's later accesses, and
-    // the callers' bar.sync extends that to the rest of the block
-    return true;
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok && p == 0) {
+        int64_t* mine = status_of(x, ep, x.rank);
+        mine[ST_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+        mine[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+        __threadfence_system();
+    }
+    // no trailing fence: each lane's ld.acquire.sys orders its later accesses, and the
+    // callers' bar.sync extends that to the rest of the block
+    return ok;
 }
 
 // Work units of the exchange kernels: a unit is kThreads consecutive 8-element groups
@@ -581,7 +586,10 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
 
     // ---- 2. all ranks packed; block 0 makes the global skip decision (identical on
     //         every rank) and releases the local flag D.  The reduce does not need it.
-    if (t0) s_ok = thread_wait_all(x, ep, FLAG_A, blockIdx.x == 0) ? 1 : 0;
+    if (threadIdx.x < 32) {
+        const bool ok = warp_wait_all(x, ep, FLAG_A, blockIdx.x == 0);
+        if (t0) s_ok = ok ? 1 : 0;
+    }
     __syncthreads();
     if (blockIdx.x == 0) {
         __shared__ int64_t s_st[3 * LMSGD_MAX_WORLD];
@@ -824,7 +832,10 @@ __global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs x, float* __res
         publish(x, ep, FLAG_C);
         *x.dev_epoch = ep.e;   // every block has read the call counter by now
     }
-    if (threadIdx.x == 0) s_ok = thread_wait_all(x, ep, FLAG_C) ? 1 : 0;
+    if (threadIdx.x < 32) {
+        const bool ok = warp_wait_all(x, ep, FLAG_C);
+        if (threadIdx.x == 0) s_ok = ok ? 1 : 0;
+    }
     __syncthreads();
     if (!s_ok) return;
     // one float4 of every rank per thread, all peer loads issued before the sums

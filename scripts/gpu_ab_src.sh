@@ -13,7 +13,7 @@ import json, sys
 v = sys.argv[1]
 l = [x for x in open(f"gpurun_out/abs_{v}.log") if x.startswith("{")]
 d = json.loads(l[-1]); t = d["trace"]["us_median_per_rank"][0]; nv = d["nvlink"]
-print(f"{v}: ms={d['ms_per_step']*1e3:.1f}us p50={d['step_us_distribution']['median']:.1f} pack={t['pack']:.1f} wait={t['wait_all_packs']:.1f} red={t['reduce_block0']:.1f} fw={t['update_first_wait']:.1f} upd={t['update']:.1f} xchg={nv['lmsgd_exchange_us']:.1f} nccl={nv['nccl_fp16_allreduce_us']:.1f} sgd={d['variants']['sgd_phase']['ms_per_step']*1e3:.1f}", flush=True)
+print(f"{v}: bn={d["bn_stats_allreduce"]["us_per_call"]:.1f} ms={d["ms_per_step"]*1e3:.1f}us p50={d['step_us_distribution']['median']:.1f} pack={t['pack']:.1f} wait={t['wait_all_packs']:.1f} red={t['reduce_block0']:.1f} fw={t['update_first_wait']:.1f} upd={t['update']:.1f} xchg={nv['lmsgd_exchange_us']:.1f} nccl={nv['nccl_fp16_allreduce_us']:.1f} sgd={d['variants']['sgd_phase']['ms_per_step']*1e3:.1f}", flush=True)
 PY
 done > gpurun_out/ab_src.txt 2>&1
 cp abtmp/kernels_new.cu paper_1711_04325_b200/csrc/kernels.cu
