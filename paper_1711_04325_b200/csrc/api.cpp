@@ -158,8 +158,6 @@ Layout make_layout(int world, int64_t n) {
     L.nchunks = static_cast<int32_t>((units_per_shard + L.cu - 1) / L.cu);
     L.off_cflags = off;
     if (world > 1) off = align_up(off + int64_t(L.nchunks) * LMSGD_MAX_WORLD * 4, 256);
-    L.off_bnflags = off;
-    if (world > 1) off = align_up(off + int64_t(lmsgd::kBnBlocks) * LMSGD_MAX_WORLD * 4, 256);
     L.bytes = off;
     return L;
 }

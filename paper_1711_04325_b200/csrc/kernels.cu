@@ -28,7 +28,7 @@ constexpr int kThreads = 256;   // LMSGD_LB below spells the same block size
 #define LMSGD_XUNITS 2   // A/B at k = 4 (profiles/r1/ab/xunits_n4.txt): 201.9 vs 206.8 us per step with 1
 #endif
 constexpr int kXUnits = LMSGD_XUNITS;   // k_xupdate: 2048-element units per block
-enum { FLAG_A = 0, FLAG_C = 2, FLAG_D = 3 };  // A: a rank's pack+push is done; C: BN ticket slot;
+enum { FLAG_A = 0, FLAG_C = 2, FLAG_D = 3 };  // A: a rank's pack+push is done; C: BN staged;
                                              // D (local): this step's skip decision is stored
 
 // Minimum resident blocks per SM asked of ptxas (register caps), A/B knobs set with
@@ -812,15 +812,11 @@ __global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
     *a.x.dev_epoch = ep.e;
 }
 
-// BN statistics without moving averages, R16: every block owns a fixed
-// set of float4 slots of the [mean | var] vector (stride gridDim x 256).  It stages them
-// in this rank's exchange buffer, fences once, releases its own flag (block b, this
-// rank) into every rank, waits -- warp 0, lane p -- for block b's flag of every rank, and
-// averages exactly those slots over the ranks' staging buffers in rank order, in fp64,
-// one rounding to fp32.  Blocks never wait for each other, so a plain (non-cooperative)
-// launch suffices.  Staging is double-buffered by call parity: a rank's next call can
-// only stage after every rank has finished this call's kernel (stream order, no PDL).
-// The last block to finish (ticket) advances the device call counter.
+// BN statistics without moving averages, one cooperative kernel
+// (all blocks co-resident): stage [mean | var] in this rank's exchange buffer, one
+// system fence per block, the last block releases flag C, every block acquires C of
+// all ranks, then averages its slice over the ranks' staging buffers in rank order,
+// in fp64, one rounding to fp32 (R16).  Double-buffered by call parity.
 __global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs x, float* __restrict__ mean,
                                                            float* __restrict__ var, int64_t C) {
     const Ep ep = get_ep(x);
@@ -828,61 +824,40 @@ __global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs x, float* __res
     const int64_t Cp = (C + 3) & ~int64_t(3);   // var staged at a 16-B aligned offset
     const int64_t off = (int64_t)ep.par * 2 * LMSGD_MAX_BN_CHANNELS;
     float* stage = reinterpret_cast<float*>(x.peers.base[x.rank] + x.lay.off_bn) + off;
-    const int64_t F = Cp / 2;                    // float4 slots of [mean | var]
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    auto src = [&](int64_t i) -> float {        // element i of [mean (Cp) | var (Cp)]
-        return i < Cp ? (i < C ? mean[i] : 0.0f) : (i - Cp < C ? var[i - Cp] : 0.0f);
-    };
-    for (int64_t f = gtid(); f < F; f += stride) {
+    for (int64_t i = gtid(); i < C; i += gstride()) {
+        stage[i] = mean[i];
+        stage[Cp + i] = var[i];
+    }
+    if (grid_last(x, FLAG_C)) {
+        publish(x, ep, FLAG_C);
+        *x.dev_epoch = ep.e;   // every block has read the call counter by now
+    }
+    if (threadIdx.x < 32) {
+        const bool ok = warp_wait_all(x, ep, FLAG_C);
+        if (threadIdx.x == 0) s_ok = ok ? 1 : 0;
+    }
+    __syncthreads();
+    if (!s_ok) return;
+    // one float4 of every rank per thread, all peer loads issued before the sums
+    for (int64_t f = gtid(); f < Cp / 2; f += gstride()) {
+        float4 v[LMSGD_MAX_WORLD];
+#pragma unroll
+        for (int p = 0; p < LMSGD_MAX_WORLD; ++p)
+            if (p < x.world)
+                v[p] = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x.peers.base[p] + x.lay.off_bn) + off)[f];
+        double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+        for (int p = 0; p < LMSGD_MAX_WORLD; ++p)
+            if (p < x.world) { a0 += v[p].x; a1 += v[p].y; a2 += v[p].z; a3 += v[p].w; }
+        const double kk = (double)x.world;
+        const float o[4] = {(float)(a0 / kk), (float)(a1 / kk), (float)(a2 / kk), (float)(a3 / kk)};
         const int64_t e0 = f * 4;
-        reinterpret_cast<float4*>(stage)[f] = make_float4(src(e0), src(e0 + 1), src(e0 + 2), src(e0 + 3));
-    }
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x < x.world) {
-        uint32_t* fl = reinterpret_cast<uint32_t*>(x.peers.base[threadIdx.x] + x.lay.off_bnflags) +
-                       blockIdx.x * LMSGD_MAX_WORLD + x.rank;
-        st_relaxed_sys(fl, ep.e);
-    }
-    if (threadIdx.x < 32) {   // lane p waits for block blockIdx.x of rank p
-        const int p = threadIdx.x;
-        bool ok = true;
-        if (p < x.world) {
-            const uint32_t* fl = reinterpret_cast<const uint32_t*>(x.peers.base[x.rank] + x.lay.off_bnflags) +
-                                 blockIdx.x * LMSGD_MAX_WORLD + p;
-            const uint64_t t0 = globaltimer();
-            while ((int32_t)(ld_acquire_sys(fl) - ep.e) < 0) {
-                __nanosleep(32);
-                if ((int64_t)(globaltimer() - t0) > x.timeout_ns) { ok = false; break; }
-            }
-        }
-        ok = __all_sync(0xffffffffu, ok);
-        if (p == 0) s_ok = ok ? 1 : 0;
-    }
-    __syncthreads();
-    if (s_ok) {
-        // one float4 of every rank per thread, all peer loads issued before the sums
-        for (int64_t f = gtid(); f < F; f += stride) {
-            float4 v[LMSGD_MAX_WORLD];
-#pragma unroll
-            for (int p = 0; p < LMSGD_MAX_WORLD; ++p)
-                if (p < x.world)
-                    v[p] = reinterpret_cast<const float4*>(reinterpret_cast<const float*>(x.peers.base[p] + x.lay.off_bn) + off)[f];
-            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-#pragma unroll
-            for (int p = 0; p < LMSGD_MAX_WORLD; ++p)
-                if (p < x.world) { a0 += v[p].x; a1 += v[p].y; a2 += v[p].z; a3 += v[p].w; }
-            const double kk = (double)x.world;
-            const float o[4] = {(float)(a0 / kk), (float)(a1 / kk), (float)(a2 / kk), (float)(a3 / kk)};
-            const int64_t e0 = f * 4;
-            for (int e = 0; e < 4; ++e) {
-                const int64_t i = e0 + e;
-                if (i < C) mean[i] = o[e];
-                else if (i >= Cp && i - Cp < C) var[i - Cp] = o[e];
-            }
+        for (int e = 0; e < 4; ++e) {
+            const int64_t i = e0 + e;
+            if (i < C) mean[i] = o[e];
+            else if (i >= Cp && i - Cp < C) var[i - Cp] = o[e];
         }
     }
-    if (grid_last(x, FLAG_C)) *x.dev_epoch = ep.e;   // every block has read the call counter
 }
 
 // Flat grids: one 8-element group per thread, one wave of short-lived blocks.
@@ -1034,9 +1009,10 @@ cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* la
 
 cudaError_t launch_bn_allreduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C) {
     int grid = (int)(((C + 3) / 4 * 2 + kThreads - 1) / kThreads);   // one float4 per thread
-    grid = grid > kBnBlocks ? kBnBlocks : (grid < 1 ? 1 : grid);
-    k_bn_allreduce<<<grid, kThreads, 0, s>>>(x, mean, var, C);
-    return cudaGetLastError();
+    grid = grid > 148 ? 148 : (grid < 1 ? 1 : grid);
+    XArgs xa = x;
+    void* params[] = {&xa, &mean, &var, &C};
+    return cudaLaunchCooperativeKernel((const void*)k_bn_allreduce, dim3((unsigned)grid), dim3(kThreads), params, 0, s);
 }
 
 }  // namespace lmsgd

@@ -9,7 +9,6 @@
 namespace lmsgd {
 
 constexpr int64_t kNone = INT64_MAX;  // "no non-finite index" in device status words
-constexpr int kBnBlocks = 148;         // max blocks of the BN average (one per SM)
 
 // Device status words of a step: this rank's {first_nonfinite, pack_saturations,
 // sum_saturations, error} and, world > 1, the global decision {first, pack_sat,
@@ -36,8 +35,7 @@ struct Layout {
     int64_t off_status;   // int64 [2 parity][ST_WORDS]
     int64_t off_flags;    // uint32: A at +0, B at +128 B, C at +256 B, D at +384 B, each [LMSGD_MAX_WORLD]
     int64_t off_bn;       // float [2 parity][2 * LMSGD_MAX_BN_CHANNELS]
-    int64_t off_cflags;   // uint32 [nchunks][LMSGD_MAX_WORLD]: owner o's "R chunk c ready" = 2 epoch + skip
-    int64_t off_bnflags;  // uint32 [kBnBlocks][LMSGD_MAX_WORLD]: rank r staged BN block b = call number
+    int64_t off_cflags;   // uint32 [nchunks][LMSGD_MAX_WORLD]: owner o's "R chunk c ready" = epoch
     int32_t cu;           // work units (2048 elements) per reduce chunk
     int32_t nchunks;      // chunks per shard
     int64_t bytes;

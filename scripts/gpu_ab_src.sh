@@ -18,4 +18,4 @@ PY
 done > gpurun_out/ab_src.txt 2>&1
 cp abtmp/kernels_new.cu paper_1711_04325_b200/csrc/kernels.cu
 python paper_1711_04325_b200/build.py --force > /dev/null 2>&1
-timeout 1200 python -m pytest tests/test_multigpu.py tests/test_gpu_parity.py tests/test_optim_gpu.py -q -x > gpurun_out/abs_tests.log 2>&1; echo "rc=$?" >> gpurun_out/abs_tests.log
+timeout 1200 python -m pytest tests/test_multigpu.py tests/test_gpu_parity.py -q -x > gpurun_out/abs_tests.log 2>&1; echo "rc=$?" >> gpurun_out/abs_tests.log
