@@ -530,13 +530,13 @@ __device__ __forceinline__ uint32_t cflag_value(const XArgs& x, const Ep& ep) {
 //   2. every block acquires A of all ranks; block 0 computes the global skip
 //      decision from the (now final) pack status words of all ranks, stores it and
 //      releases the local flag D;
-//   3. exact reduce of this rank's shard over contiguous unit ranges per block; a
-//      64K-element chunk is released to every rank (cflag[c][rank] = epoch) as soon
-//      as all its units are reduced.
+//   3. exact reduce of this rank's shard, unit u on block u % grid; a 64K-element
+//      chunk is released to every rank (cflag[c][rank] = 2 epoch + skip) once all
+//      its units are reduced and fenced.
 // k_xupdate -- flat grid, launched with programmatic dependent launch so its blocks
-// take SMs as soon as k_xstep1's blocks retire: one unit per block, chunk-major and
-// owner-interleaved; a block waits only for D and for its owner's chunk flag, so
-// the update of early chunks overlaps the reduce of later ones.
+// take SMs as soon as k_xstep1's blocks retire: kXUnits units per block, chunk-major
+// and owner-interleaved; a block waits only for its units' chunk flags (which carry
+// the skip decision), so the update of early chunks overlaps the reduce of later ones.
 // k_xfinalize -- one warp: the step's public status record.
 // Chunk counters in a.ctr are reset by the block that completes them.
 #ifndef LMSGD_XSTEP_MINB
