@@ -242,6 +242,45 @@ def test_c1_twenty_steps_resynced():
     assert run.scaled_error(host(th), free.theta, scale) < 1e-4
 
 
+def test_full_schedule_resynced_every_step():
+    """The whole 90-epoch 32k schedule (T = 3,519 iterations: the RMSprop warm-up, the
+    switch to SGD at t = 490 and the LR drops at t = 1565, 2738, 3325) through the
+    context path, every step checked against the oracle resynced to the GPU's state;
+    then the same run through the CUDA-graph entry point (coefficients from the device
+    table) must end bit-identical."""
+    n, s = 4099, 1024.0
+    T = L.lmsgd_schedule_steps(K32_C)
+    assert T == 3519
+    a = synth.grad_scale(n)
+    th0 = synth.theta0(n, None)
+    z = np.zeros(n, np.float32)
+    grads = [None] + [synth.grads(1, t, n, a)[0] for t in range(1, T + 1)]
+    ctx = L.lmsgd_init(1, 0, 0, n, s)
+    th, d, m = dev(th0), dev(z), dev(z)
+    worst = 0.0
+    for t in range(1, T + 1):
+        prev = host(th), host(d), host(m)
+        L.lmsgd_step(ctx, th, dev(grads[t]), d, m, L.lmsgd_schedule_at(None, K32_C, t))
+        e = check_state(host(th), host(d), host(m), *prev, exchange.exchange([grads[t]], s).ghat,
+                        schedule.coeffs_at(t))
+        worst = max(worst, max(e.values()))
+    code, _ = L.lmsgd_query_status(ctx)
+    assert code == 0 and worst <= TOL
+    L.lmsgd_finalize(ctx)
+    # graph entry point over the same schedule, eagerly (the table and counters are on the device)
+    ctxg = L.lmsgd_init(1, 0, 0, n, s)
+    L.lmsgd_schedule_upload(ctxg, None, K32_C, 1, T)
+    thg, dg, mg = dev(th0), dev(z), dev(z)
+    gbuf = dev(z)
+    for t in range(1, T + 1):
+        gbuf.copy_(dev(grads[t]))
+        L.lmsgd_step_graph(ctxg, thg, gbuf, dg, mg)
+    code, _ = L.lmsgd_query_status(ctxg)
+    assert code == 0
+    assert torch.equal(thg, th) and torch.equal(dg, d) and torch.equal(mg, m)
+    L.lmsgd_finalize(ctxg)
+
+
 # ------------------------------------------------------------------ sub-steps / simulated k
 
 def _pack_codec_case(x32, s):
