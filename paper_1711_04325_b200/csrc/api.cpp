@@ -14,6 +14,8 @@
 #include "lmsgd.h"
 #include "lmsgd_internal.h"
 
+#include <nvtx3/nvToolsExt.h>   // header-only; ranges are no-ops unless a profiler is attached
+
 using lmsgd::Layout;
 using lmsgd::UpdConst;
 
@@ -63,6 +65,13 @@ struct lmsgd_ctx {
 namespace {
 
 thread_local std::string g_err;  // for context-free calls
+
+// NVTX range around a host entry point (nsys / Nsight timelines: which library call
+// enqueued which kernels).
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 lmsgd_status fail(lmsgd_ctx* c, lmsgd_status s, const std::string& msg) {
     if (c) c->err = msg; else g_err = msg;
@@ -365,6 +374,7 @@ lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
 
 lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* grads, float* delta,
                         float* m, const lmsgd_coeffs* coeffs) {
+    NvtxRange nvtx_("lmsgd_step");
     if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
     if (!aligned16(params) || !aligned16(grads) || !aligned16(delta) || !aligned16(m))
         return fail(c, LMSGD_ERR_INVALID_ARG, "params/grads/delta/m must be non-NULL and 16-byte aligned");
@@ -406,6 +416,7 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
 }
 
 lmsgd_status lmsgd_exchange(lmsgd_ctx* c, void* stream, const float* grads, uint16_t* R_out) {
+    NvtxRange nvtx_("lmsgd_exchange");
     if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
     if (!aligned16(grads) || !aligned16(R_out))
         return fail(c, LMSGD_ERR_INVALID_ARG, "grads/R_out must be non-NULL and 16-byte aligned");
@@ -470,6 +481,7 @@ lmsgd_status lmsgd_schedule_upload(lmsgd_ctx* c, const lmsgd_hyper* hyper, const
 
 lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const float* grads, float* delta,
                               float* m) {
+    NvtxRange nvtx_("lmsgd_step_graph");
     if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
     if (!aligned16(params) || !aligned16(grads) || !aligned16(delta) || !aligned16(m))
         return fail(c, LMSGD_ERR_INVALID_ARG, "params/grads/delta/m must be non-NULL and 16-byte aligned");
@@ -508,6 +520,7 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
 lmsgd_status lmsgd_step_host(lmsgd_ctx* c, void* stream, float* params, const float* grads_host,
                              float* delta, float* m, const lmsgd_coeffs* coeffs,
                              lmsgd_step_status* status_host) {
+    NvtxRange nvtx_("lmsgd_step_host");
     if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
     if (!grads_host || !status_host) return fail(c, LMSGD_ERR_INVALID_ARG, "NULL host pointer");
     DeviceGuard g(c->device);
@@ -546,6 +559,7 @@ lmsgd_status lmsgd_query_status(lmsgd_ctx* c, lmsgd_step_status* out) {
 }
 
 lmsgd_status lmsgd_bn_stats_allreduce(lmsgd_ctx* c, void* stream, float* mean, float* var, int64_t C) {
+    NvtxRange nvtx_("lmsgd_bn_stats_allreduce");
     if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
     if (!mean || !var || C < 1 || C > LMSGD_MAX_BN_CHANNELS)
         return fail(c, LMSGD_ERR_INVALID_ARG, "mean/var must be non-NULL, 0 < C <= LMSGD_MAX_BN_CHANNELS");
