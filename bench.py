@@ -544,6 +544,41 @@ def main():
                                               "reported but not skipped"}}
         L.lmsgd_finalize(ctxf)
         del thf, df, mf
+        # the guarded step in one pass, out of place (lmsgd_step_out_of_place): the state
+        # ping-pongs between two buffer sets, the non-finite guard costs no extra pass
+        ctxo = L.lmsgd_init(1, 0, local, n, LOSS_SCALE)
+        sets = [(theta.clone(), delta.clone(), m.clone()), (torch.empty_like(theta), torch.empty_like(delta),
+                                                            torch.empty_like(m))]
+        pset = [tuple(P(x.data_ptr()) for x in st_) for st_ in sets]
+        gp_ = P(grads.data_ptr())
+
+        def step_oop(i):
+            a_, b_ = pset[i & 1], pset[(i & 1) ^ 1]
+            r_ = lib.lmsgd_step_out_of_place(ctxo.ptr, sp, a_[0], b_[0], gp_, a_[1], b_[1], a_[2], b_[2],
+                                             ctypes.byref(coeffs[i]))
+            if r_ != 0:
+                raise L.LmsgdError(r_, lib.lmsgd_last_error(ctxo.ptr).decode())
+
+        for i in range(args.warmup):
+            step_oop(i)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(args.steps):
+            step_oop(args.warmup + i)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        oms = e0.elapsed_time(e1) / args.steps
+        codeo, _ = L.lmsgd_query_status(ctxo)
+        assert codeo == 0
+        variants["guarded_out_of_place"] = {
+            "ms_per_step": oms, "value": 1e3 / oms, "unit": UNIT,
+            "hbm_gbs_algorithmic": FUSED_BYTES_PER_ELEM * n / (oms * 1e-3) / 1e9,
+            "frac_of_measured_hbm": FUSED_BYTES_PER_ELEM * n / (oms * 1e-3) / 1e9 / peak,
+            "gpu_launches_per_step": 2,
+            "note": "lmsgd_step_out_of_place: same results and non-finite skip as the headline, one pass "
+                    "(28 B/elem) with the state alternating between two buffer sets"}
+        L.lmsgd_finalize(ctxo)
+        del sets
 
     # SGD phase (alpha_RMSprop = 0, t >= 490 at 32k: 86% of the 3,519 steps), with and
     # without LMSGD_FLAG_FREEZE_M (m not touched: 18 instead of 26 B/elem in the update)

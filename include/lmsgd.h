@@ -199,6 +199,21 @@ lmsgd_status lmsgd_set_weight_decay(lmsgd_ctx* ctx, double lambda, int64_t n_dec
 lmsgd_status lmsgd_step(lmsgd_ctx* ctx, void* stream, float* params, const float* grads,
                         float* delta, float* m, const lmsgd_coeffs* coeffs);
 
+/* The same iteration out of place, world == 1: reads theta, Delta, m from the *_in
+ * buffers and writes the new state to the *_out buffers (device fp32 [n] each; outputs
+ * must not overlap the inputs or grads).  The non-finite guard of lmsgd_step then costs
+ * no extra pass: pack and update run as ONE pass (28 instead of 32 B/elem of HBM
+ * traffic), and if a gradient turns out non-finite the outputs receive a copy of the
+ * inputs (skipped = 1, LMSGD_ERR_NONFINITE from lmsgd_query_status).  Either way the
+ * *_out buffers hold the state after the step, so the caller alternates two buffer sets
+ * (ping-pong) without synchronising.  Results are bit-identical to lmsgd_step.
+ * Errors: INVALID_ARG (NULL / misaligned / overlapping buffers, bad coeffs),
+ * UNSUPPORTED (world > 1 -- there lmsgd_step's skip decision is free -- or weight decay
+ * set), STATE (a context that runs lmsgd_step_graph). */
+lmsgd_status lmsgd_step_out_of_place(lmsgd_ctx* ctx, void* stream, const float* params_in, float* params_out,
+                                     const float* grads, const float* delta_in, float* delta_out,
+                                     const float* m_in, float* m_out, const lmsgd_coeffs* coeffs);
+
 /* The same iteration with the gradient in HOST memory (pinned for full speed):
  * copies grads_host -> device, runs lmsgd_step and copies the step status back into
  * *status_host (valid once `stream` has passed this point).  The copy runs on a

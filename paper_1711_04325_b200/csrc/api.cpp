@@ -415,6 +415,45 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     return LMSGD_OK;
 }
 
+lmsgd_status lmsgd_step_out_of_place(lmsgd_ctx* c, void* stream, const float* params_in, float* params_out,
+                                      const float* grads, const float* delta_in, float* delta_out,
+                                      const float* m_in, float* m_out, const lmsgd_coeffs* coeffs) {
+    NvtxRange nvtx_("lmsgd_step_out_of_place");
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (!aligned16(params_in) || !aligned16(params_out) || !aligned16(grads) || !aligned16(delta_in) ||
+        !aligned16(delta_out) || !aligned16(m_in) || !aligned16(m_out))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "all pointers must be non-NULL and 16-byte aligned");
+    const int64_t bytes = c->n * 4;
+    auto overlap = [&](const void* a, const void* b) {
+        const char* x = static_cast<const char*>(a);
+        const char* y = static_cast<const char*>(b);
+        return x < y + bytes && y < x + bytes;
+    };
+    const void* ins[] = {params_in, delta_in, m_in, grads};
+    const void* outs[] = {params_out, delta_out, m_out};
+    for (const void* o : outs)
+        for (const void* i : ins)
+            if (overlap(o, i)) return fail(c, LMSGD_ERR_INVALID_ARG, "output buffers must not overlap the inputs");
+    if (!coeffs_ok(coeffs))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "coeffs: need eta > 0, 0 <= alpha_sgd <= 1, alpha_rmsprop >= 0");
+    if (c->world != 1) return fail(c, LMSGD_ERR_UNSUPPORTED, "out-of-place step is world == 1 only (use lmsgd_step)");
+    if (c->wd != 0.0) return fail(c, LMSGD_ERR_UNSUPPORTED, "out-of-place step has no weight decay");
+    if (c->mode == 2) return fail(c, LMSGD_ERR_STATE, "this context runs lmsgd_step_graph");
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const UpdConst u = make_const(c->hyper, *coeffs, 1, c->scale, 0.0, 0);
+    const uint32_t epoch = ++c->step;
+    const int parity = static_cast<int>(epoch & 1u);
+    c->last_stream = s;
+    c->mode = 1;
+    CK(c, timed(c, s, 0, [&] {
+           return lmsgd::launch_step_oop1(s, c->L, grads, c->n, c->scale, u, params_in, delta_in, m_in, params_out,
+                                          delta_out, m_out, status_slot(c, parity), status_slot(c, parity ^ 1),
+                                          c->last);
+       }));
+    return LMSGD_OK;
+}
+
 lmsgd_status lmsgd_exchange(lmsgd_ctx* c, void* stream, const float* grads, uint16_t* R_out) {
     NvtxRange nvtx_("lmsgd_exchange");
     if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");

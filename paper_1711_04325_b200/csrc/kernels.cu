@@ -361,6 +361,83 @@ __global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1(const float* __restrict__ g,
     flush_status(first, sat, st, ST_PACK_SAT);
 }
 
+// Out-of-place variant of update8 (lmsgd_step_out_of_place): reads theta, Delta, m
+// from the *_in buffers and writes the new values to the *_out buffers.
+template <bool RMS>
+__device__ __forceinline__ void update8_oop(uint4 r, int64_t j0, int64_t n, const UpdConst& c,
+                                            const float* __restrict__ thi, const float* __restrict__ di,
+                                            const float* __restrict__ mi, float* __restrict__ tho,
+                                            float* __restrict__ dout, float* __restrict__ mo) {
+    const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+    if (j0 + 8 <= n) {
+        const float4 t0 = __ldcs(reinterpret_cast<const float4*>(thi + j0)), t1 = __ldcs(reinterpret_cast<const float4*>(thi + j0) + 1);
+        const float4 d0 = __ldcs(reinterpret_cast<const float4*>(di + j0)), d1 = __ldcs(reinterpret_cast<const float4*>(di + j0) + 1);
+        const float4 m0 = __ldcs(reinterpret_cast<const float4*>(mi + j0)), m1 = __ldcs(reinterpret_cast<const float4*>(mi + j0) + 1);
+        float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
+        float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+        float mv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) upd1<RMS>(h2f(w[i >> 1], i & 1) * c.inv_ks, tv[i], dv[i], mv[i], c);
+        __stcs(reinterpret_cast<float4*>(tho + j0), make_float4(tv[0], tv[1], tv[2], tv[3]));
+        __stcs(reinterpret_cast<float4*>(tho + j0) + 1, make_float4(tv[4], tv[5], tv[6], tv[7]));
+        __stcs(reinterpret_cast<float4*>(dout + j0), make_float4(dv[0], dv[1], dv[2], dv[3]));
+        __stcs(reinterpret_cast<float4*>(dout + j0) + 1, make_float4(dv[4], dv[5], dv[6], dv[7]));
+        __stcs(reinterpret_cast<float4*>(mo + j0), make_float4(mv[0], mv[1], mv[2], mv[3]));
+        __stcs(reinterpret_cast<float4*>(mo + j0) + 1, make_float4(mv[4], mv[5], mv[6], mv[7]));
+    } else {
+        for (int i = 0; i < 8 && j0 + i < n; ++i) {
+            float t = thi[j0 + i], dd = di[j0 + i], mm = mi[j0 + i];
+            upd1<RMS>(h2f(w[i >> 1], i & 1) * c.inv_ks, t, dd, mm, c);
+            tho[j0 + i] = t; dout[j0 + i] = dd; mo[j0 + i] = mm;
+        }
+    }
+}
+
+// lmsgd_step_out_of_place, k = 1: the guarded step in ONE pass over the state (28 B/elem,
+// like k_fused1) -- the new state goes to separate buffers, so a non-finite gradient,
+// found only at the end, costs nothing but a repair copy (k_repair1).
+template <bool RMS>
+__global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1_oop(const float* __restrict__ g, int64_t n, float s,
+                                                         UpdConst c, const float* __restrict__ thi,
+                                                         const float* __restrict__ di, const float* __restrict__ mi,
+                                                         float* __restrict__ tho, float* __restrict__ dout,
+                                                         float* __restrict__ mo, int64_t* st, int64_t* st_reset) {
+    pdl_enter();
+    reset_status(st_reset);
+    int64_t first = kNone;
+    unsigned sat = 0;
+    const int64_t nv = (n + 7) >> 3;
+    for (int64_t v = gtid(); v < nv; v += gstride()) {
+        const int64_t j0 = v << 3;
+        float x[8];
+        load8_g(g, j0, n, x);
+        update8_oop<RMS>(pack8(x, s, j0, first, sat), j0, n, c, thi, di, mi, tho, dout, mo);
+    }
+    flush_status(first, sat, st, ST_PACK_SAT);
+}
+
+// After k_fused1_oop: if a gradient was non-finite the step is skipped -- the output
+// buffers receive the unchanged input state (rare path: a grid-stride copy); block 0
+// publishes the status record.  On a clean step every block returns at once.
+__global__ void k_repair1(const int64_t* st, const float* __restrict__ thi, const float* __restrict__ di,
+                          const float* __restrict__ mi, float* __restrict__ tho, float* __restrict__ dout,
+                          float* __restrict__ mo, int64_t n, int64_t* last) {
+    pdl_enter();
+    const int64_t first = *reinterpret_cast<volatile const int64_t*>(st + ST_FIRST);
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        store_last(last, first, st[ST_PACK_SAT], 0, st[ST_ERROR], first != kNone ? 1 : 0);
+    if (first == kNone) return;
+    const int64_t nv = n >> 2;
+    for (int64_t v = gtid(); v < nv; v += gstride()) {
+        reinterpret_cast<float4*>(tho)[v] = reinterpret_cast<const float4*>(thi)[v];
+        reinterpret_cast<float4*>(dout)[v] = reinterpret_cast<const float4*>(di)[v];
+        reinterpret_cast<float4*>(mo)[v] = reinterpret_cast<const float4*>(mi)[v];
+    }
+    for (int64_t j = (nv << 2) + gtid(); j < n; j += gstride()) {
+        tho[j] = thi[j]; dout[j] = di[j]; mo[j] = mi[j];
+    }
+}
+
 // Publishes the fused step's status (never skipped) into the public `last` record.
 // A separate 1-warp launch: a per-block fence + ticket in k_fused1 cost 16% of it.
 __global__ void k_finalize_fused(const int64_t* st, int64_t* last) {
@@ -998,6 +1075,17 @@ cudaError_t launch_advance1(cudaStream_t s, const Dev1& dv, int64_t* last, bool 
 
 cudaError_t launch_xfinal1(cudaStream_t s, const int64_t* st, int64_t* st_next, int64_t* last) {
     return launch_pdl_if(true, k_xfinal1, 1, 32, s, st, st_next, last);
+}
+
+cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
+                             const UpdConst& c, const float* thi, const float* di, const float* mi, float* tho,
+                             float* dout, float* mo, int64_t* st, int64_t* st_reset, int64_t* last) {
+    const int grid = grid_for(L, (n + 7) >> 3);
+    cudaError_t e = launch_pdl(c.a_rms != 0.0f ? k_fused1_oop<true> : k_fused1_oop<false>, grid, kThreads, s, g, n,
+                               scale, c, thi, di, mi, tho, dout, mo, st, st_reset);
+    if (e != cudaSuccess) return e;
+    return launch_pdl_if(true, k_repair1, 4 * L.sm_count, kThreads, s, (const int64_t*)st, thi, di, mi, tho, dout,
+                         mo, n, last);
 }
 
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last) {

@@ -79,6 +79,7 @@ def _load() -> ctypes.CDLL:
         "lmsgd_last_error": (ctypes.c_char_p, [P]),
         "lmsgd_step": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs)]),
         "lmsgd_exchange": (I32, [P, P, P, P]),
+        "lmsgd_step_out_of_place": (I32, [P, P, P, P, P, P, P, P, P, ctypes.POINTER(Coeffs)]),
         "lmsgd_step_host": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs), P]),
         "lmsgd_bn_stats_allreduce": (I32, [P, P, P, P, I64]),
         "lmsgd_set_weight_decay": (I32, [P, ctypes.c_double, I64]),
@@ -245,6 +246,19 @@ def lmsgd_step(ctx: Context, params, grads, delta, m, coeffs: Coeffs, stream=Non
     _check(_lib.lmsgd_step(ctx.ptr, _stream(stream), _ptr(params, torch.float32, "params"),
                            _ptr(grads, torch.float32, "grads"), _ptr(delta, torch.float32, "delta"),
                            _ptr(m, torch.float32, "m"), ctypes.byref(coeffs)), ctx)
+
+
+def lmsgd_step_out_of_place(ctx: Context, params_in, params_out, grads, delta_in, delta_out, m_in, m_out,
+                            coeffs: Coeffs, stream=None):
+    """world == 1: the guarded step in one pass, state read from *_in and written to *_out."""
+    import torch
+    ts = ((params_in, "params_in"), (params_out, "params_out"), (grads, "grads"), (delta_in, "delta_in"),
+          (delta_out, "delta_out"), (m_in, "m_in"), (m_out, "m_out"))
+    for t, nm in ts:
+        if t.numel() != ctx.n:
+            raise ValueError(f"{nm} must have n_params = {ctx.n} elements")
+    _check(_lib.lmsgd_step_out_of_place(ctx.ptr, _stream(stream), *(_ptr(t, torch.float32, nm) for t, nm in ts),
+                                        ctypes.byref(coeffs)), ctx)
 
 
 def lmsgd_exchange(ctx: Context, grads, R_out, stream=None):

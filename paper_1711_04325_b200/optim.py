@@ -13,6 +13,12 @@ tensor with more than one dimension -- conv and fc weights; BN and biases exclud
 Goyal et al.'s convention) are placed first in the flat buffer so the library's
 decayed prefix covers exactly them.
 
+Out of place (world 1, the default there without weight decay): the parameters,
+Delta and m live in two buffer sets; each step reads one set and writes the other
+through ``lmsgd_step_out_of_place`` (the guarded step in one pass over HBM, 28 instead
+of 32 B/elem), then the parameters' ``.data`` are re-pointed at the new set.  Results
+are bit-identical to the in-place step.
+
 Checkpoint/resume: ``state_dict`` holds the step counter t and the optimizer state
 (Delta, m) -- with the parameters, everything the next step depends on.
 """
@@ -33,7 +39,7 @@ class LMSGD:
     def __init__(self, params: Iterable[torch.Tensor], *, cluster: L.Cluster | None = None,
                  hyper: L.Hyper | None = None, loss_scale: float = 1024.0, weight_decay: float = 0.0,
                  decay: Callable[[torch.Tensor], bool] = _default_decay, flags: int = 0,
-                 group=None, t_start: int = 1):
+                 group=None, t_start: int = 1, out_of_place: bool | None = None):
         params = [p for p in params if p.requires_grad]
         if not params:
             raise ValueError("no trainable parameters")
@@ -45,20 +51,30 @@ class LMSGD:
         self.params = decayed + [p for p in params if id(p) not in ids]
         self.n = sum(p.numel() for p in self.params)
         self.n_decay = sum(p.numel() for p in decayed)
-        self.flat_p = torch.empty(self.n, dtype=torch.float32, device=dev)
-        self.flat_g = torch.zeros(self.n, dtype=torch.float32, device=dev)
-        off = 0
-        with torch.no_grad():
-            for p in self.params:   # row a1: parameters and gradients become views
-                k = p.numel()
-                self.flat_p[off:off + k].copy_(p.reshape(-1))
-                p.data = self.flat_p[off:off + k].view_as(p)
-                p.grad = self.flat_g[off:off + k].view_as(p)
-                off += k
         import torch.distributed as dist
         dist_on = dist.is_available() and dist.is_initialized()
         world = dist.get_world_size(group) if dist_on else 1
         rank = dist.get_rank(group) if dist_on else 0
+        if out_of_place is None:
+            out_of_place = world == 1 and not weight_decay and flags == 0
+        if out_of_place and (world != 1 or weight_decay):
+            raise ValueError("out_of_place needs world == 1 and no weight decay")
+        self.out_of_place = bool(out_of_place)
+        nsets = 2 if self.out_of_place else 1
+        self._p = [torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(nsets)]
+        self.flat_g = torch.zeros(self.n, dtype=torch.float32, device=dev)
+        self._cur = 0
+        self._views = [[] for _ in range(nsets)]
+        off = 0
+        with torch.no_grad():
+            for p in self.params:   # row a1: parameters and gradients become views
+                k = p.numel()
+                self._p[0][off:off + k].copy_(p.reshape(-1))
+                for b in range(nsets):
+                    self._views[b].append(self._p[b][off:off + k].view_as(p))
+                p.data = self._views[0][-1]
+                p.grad = self.flat_g[off:off + k].view_as(p)
+                off += k
         self.cluster = cluster if cluster is not None else L.make_cluster()
         self.hyper = hyper
         self.ctx = L.lmsgd_init(world, rank, dev.index if dev.index is not None else torch.cuda.current_device(),
@@ -66,10 +82,23 @@ class LMSGD:
         L.connect_process_group(self.ctx, group)
         if weight_decay:
             L.lmsgd_set_weight_decay(self.ctx, weight_decay, self.n_decay)
-        self.delta = torch.zeros(self.n, dtype=torch.float32, device=dev)
-        self.m = torch.zeros(self.n, dtype=torch.float32, device=dev)
+        self._d = [torch.zeros(self.n, dtype=torch.float32, device=dev) for _ in range(nsets)]
+        self._m = [torch.zeros(self.n, dtype=torch.float32, device=dev) for _ in range(nsets)]
         self.t = int(t_start)
         self.steps_total = L.lmsgd_schedule_steps(self.cluster)
+
+    # the current buffer set (the one the parameters view)
+    @property
+    def flat_p(self) -> torch.Tensor:
+        return self._p[self._cur]
+
+    @property
+    def delta(self) -> torch.Tensor:
+        return self._d[self._cur]
+
+    @property
+    def m(self) -> torch.Tensor:
+        return self._m[self._cur]
 
     # ------------------------------------------------------------------ training
     def zero_grad(self):
@@ -92,7 +121,15 @@ class LMSGD:
         current stream; returns before completion)."""
         self._check_views()
         c = self.coeffs()
-        L.lmsgd_step(self.ctx, self.flat_p, self.flat_g, self.delta, self.m, c, stream)
+        if self.out_of_place:
+            a, b = self._cur, self._cur ^ 1
+            L.lmsgd_step_out_of_place(self.ctx, self._p[a], self._p[b], self.flat_g, self._d[a], self._d[b],
+                                      self._m[a], self._m[b], c, stream)
+            for p, v in zip(self.params, self._views[b]):   # the step's output is the new parameter set
+                p.data = v
+            self._cur = b
+        else:
+            L.lmsgd_step(self.ctx, self.flat_p, self.flat_g, self.delta, self.m, c, stream)
         self.t += 1
         return c
 

@@ -400,6 +400,52 @@ def test_k1_exchange_through_ctx():
     L.lmsgd_finalize(ctx)
 
 
+@pytest.mark.parametrize("n", [1, 9, 65, 10_007, (1 << 20) + 13])
+def test_step_out_of_place_matches_step(n):
+    # one-pass guarded step, ping-pong buffers: bit-identical to the in-place lmsgd_step,
+    # a non-finite gradient leaves out = in (skipped), the next step continues from there
+    s = 1024.0
+    th0, d0, m0 = init_state(n)
+    ref = L.lmsgd_init(1, 0, 0, n, s)
+    oop = L.lmsgd_init(1, 0, 0, n, s)
+    th, d, m = dev(th0), dev(d0), dev(m0)
+    bufs = [[dev(th0), dev(d0), dev(m0)], [dev(np.zeros(n, np.float32)) for _ in range(3)]]
+    a = synth.grad_scale(n)
+    cur = 0
+    for i, t in enumerate((1, 12, 15, 16, 17)):
+        g = synth.grads(1, t, n, a)[0]
+        if i == 3:
+            g[n // 2] = np.nan
+        co = L.lmsgd_schedule_at(None, C1_C, t)
+        prev = host(th), host(d), host(m)
+        L.lmsgd_step(ref, th, dev(g), d, m, co)
+        code_r, _ = L.lmsgd_query_status(ref)
+        src, dst = bufs[cur], bufs[cur ^ 1]
+        L.lmsgd_step_out_of_place(oop, src[0], dst[0], dev(g), src[1], dst[1], src[2], dst[2], co)
+        code, st = L.lmsgd_query_status(oop)
+        cur ^= 1
+        assert code == code_r
+        assert all(torch.equal(x, y) for x, y in zip(dst, (th, d, m))), t
+        if i == 3:
+            assert code == L.LMSGD_ERR_NONFINITE and st.skipped == 1 and st.first_nonfinite == n // 2
+            assert all(torch.equal(x, y) for x, y in zip(dst, src))
+        else:
+            assert code == 0 and st.skipped == 0
+            check_state(host(dst[0]), host(dst[1]), host(dst[2]), *prev, exchange.exchange([g], s).ghat,
+                        schedule.coeffs_at(t, schedule.Hyper(), C1))
+    with pytest.raises(L.LmsgdError) as e:        # outputs overlapping the inputs
+        L.lmsgd_step_out_of_place(oop, bufs[0][0], bufs[0][0], dev(g), bufs[0][1], bufs[1][1], bufs[0][2],
+                                  bufs[1][2], co)
+    assert e.value.status == L.LMSGD_ERR_INVALID_ARG
+    L.lmsgd_set_weight_decay(oop, 1e-4)
+    with pytest.raises(L.LmsgdError) as e:
+        L.lmsgd_step_out_of_place(oop, *(bufs[0][0], bufs[1][0]), dev(g), bufs[0][1], bufs[1][1], bufs[0][2],
+                                  bufs[1][2], co)
+    assert e.value.status == L.LMSGD_ERR_UNSUPPORTED
+    L.lmsgd_finalize(ref)
+    L.lmsgd_finalize(oop)
+
+
 def test_fused_step1_matches_pack_update():
     n = 777_777
     th0, d0, m0 = init_state(n)

@@ -92,3 +92,26 @@ def test_lmsgd_detached_grad_fails_loudly():
 def test_lmsgd_rejects_cpu_params():
     with pytest.raises(ValueError):
         L.LMSGD(torch.nn.Linear(4, 4).parameters())
+
+
+def test_lmsgd_out_of_place_matches_in_place(monkeypatch):
+    # world 1 without weight decay defaults to the out-of-place one-pass step: the
+    # parameters alternate between two flat buffers, results bit-identical to in place
+    monkeypatch.setattr(torch.backends.cudnn, "deterministic", True)
+    monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
+    nets = [_net(), _net()]
+    opts = [L.LMSGD(nets[0].parameters(), cluster=L.make_cluster(2, 32, 64)),
+            L.LMSGD(nets[1].parameters(), cluster=L.make_cluster(2, 32, 64), out_of_place=False)]
+    assert opts[0].out_of_place and not opts[1].out_of_place
+    for t in range(1, 8):
+        for net, opt in zip(nets, opts):
+            _train_step(net, opt, t)
+            opt.step()
+        torch.cuda.synchronize()
+        assert torch.equal(opts[0].flat_p, opts[1].flat_p), t
+        assert torch.equal(opts[0].delta, opts[1].delta) and torch.equal(opts[0].m, opts[1].m), t
+        # the module sees the step's output buffer
+        assert nets[0][0].weight.data_ptr() == opts[0].flat_p.data_ptr()
+        assert all(torch.equal(a, b) for a, b in zip(nets[0].parameters(), nets[1].parameters()))
+    for o in opts:
+        o.close()
