@@ -44,9 +44,11 @@ def parse():
     p.add_argument("--warmup", type=int, default=20)
     p.add_argument("--impl", choices=["lmsgd", "reference"], default="lmsgd")
     p.add_argument("--depth", type=int, default=50, choices=[50, 152])
-    p.add_argument("--mode", choices=["guarded", "fused"], default="guarded",
-                   help="N=1: guarded = pack + update with global non-finite skip (default); "
-                        "fused = single-pass pack+update (LMSGD_FLAG_NO_SKIP)")
+    p.add_argument("--mode", choices=["out_of_place", "guarded", "fused"], default="out_of_place",
+                   help="N=1: out_of_place = the guarded step in one pass, state ping-ponging between two "
+                        "buffer sets (lmsgd_step_out_of_place, the default; what LMSGD uses at world 1); "
+                        "guarded = in-place lmsgd_step, pack + update with the global non-finite skip; "
+                        "fused = in-place single pass without the skip (LMSGD_FLAG_NO_SKIP)")
     p.add_argument("--t-start", type=int, default=1, help="first schedule step timed (1 = RMSprop warm-up)")
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--full-schedule", action="store_true",
@@ -270,8 +272,18 @@ def main():
     ptrs = (P(theta.data_ptr()), P(grads.data_ptr()), P(delta.data_ptr()), P(m.data_ptr()))
     lib = L.lib()
 
+    oop = args.mode == "out_of_place" and world == 1
+    if oop:   # the second buffer set of the out-of-place step (the state alternates)
+        theta2, delta2, m2 = torch.empty_like(theta), torch.empty_like(delta), torch.empty_like(m)
+        sets = (ptrs, (P(theta2.data_ptr()), ptrs[1], P(delta2.data_ptr()), P(m2.data_ptr())))
+
     def step(i):
-        st = lib.lmsgd_step(ctx.ptr, sp, *ptrs, ctypes.byref(coeffs[i]))
+        if oop:
+            a_, b_ = sets[i & 1], sets[(i & 1) ^ 1]
+            st = lib.lmsgd_step_out_of_place(ctx.ptr, sp, a_[0], b_[0], ptrs[1], a_[2], b_[2], a_[3], b_[3],
+                                             ctypes.byref(coeffs[i]))
+        else:
+            st = lib.lmsgd_step(ctx.ptr, sp, *ptrs, ctypes.byref(coeffs[i]))
         if st != 0:
             raise L.LmsgdError(st, lib.lmsgd_last_error(ctx.ptr).decode())
 
@@ -293,9 +305,10 @@ def main():
         code, st = L.lmsgd_query_status(ctx)
         assert code == 0, f"warm-up step status {code}"
 
-    # kernels launched per step: fused = k_fused1 + status finalize; guarded k=1 = k_pack
+    # kernels launched per step: out of place = k_fused1_oop + k_repair1 (status; copies
+    # only on a skipped step); fused = k_fused1 + status finalize; guarded k=1 = k_pack
     # + k_update; world > 1 = k_xstep1 + k_xupdate + k_xfinalize
-    kernels_per_step = 2 if flags else (2 if world == 1 else 3)
+    kernels_per_step = 2 if (flags or oop) else (2 if world == 1 else 3)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 
     host_s = [0.0]
@@ -394,7 +407,9 @@ def main():
             phases[ph] = {"us_per_launch": (max_over_ranks(pms / cnt * 1e3) if world == 1 else pms * 1e3),
                           "launches": cnt if world == 1 else args.steps,
                           "source": "cuda events" if world == 1 else ("in-kernel %globaltimer trace, max over ranks; update = the k_xupdate span from its first block's start" if ph == "update" else "in-kernel %globaltimer trace, max over ranks")}
-    if flags:
+    if oop:   # phase 0 = k_fused1_oop + k_repair1 (the latter ~2 us: a slightly pessimistic time)
+        dom, dom_bytes, kname = "pack", FUSED_BYTES_PER_ELEM, "k_fused1_oop"
+    elif flags:
         dom, dom_bytes, kname = "pack", FUSED_BYTES_PER_ELEM, "k_fused1"   # phase 0 = the fused kernel
     else:
         dom, dom_bytes, kname = "update", UPDATE_BYTES_PER_ELEM, "k_update" if world == 1 else "k_xupdate"
@@ -406,7 +421,7 @@ def main():
                     "frac": achieved / peak, "traffic": committed_traffic(kname),
                     "algorithmic_bytes_per_launch": dom_bytes * n, "peak_source": peak_src,
                     "share_of_step": us * 1e-3 / ms_per_step}
-    if "pack" in phases and not flags and world == 1:
+    if "pack" in phases and not flags and not oop and world == 1:
         phases["pack"]["gbs_algorithmic"] = PACK_BYTES_PER_ELEM * n / (phases["pack"]["us_per_launch"] * 1e-6) / 1e9
     if "update" in phases:
         phases["update"]["gbs_algorithmic"] = UPDATE_BYTES_PER_ELEM * n / (phases["update"]["us_per_launch"] * 1e-6) / 1e9
@@ -519,8 +534,9 @@ def main():
            # PCIe-bound: the copy of step t+1 overlaps the kernels of step t (lmsgd_step_host)
            "h2d_gbs": 4 * n / (e2e_ms * 1e-3) / 1e9}
 
-    # N = 1 guarded default: also time the single-pass fused variant (LMSGD_FLAG_NO_SKIP,
-    # BASELINE.json configs[1] "fused fp16-pack + blended update"; 28 vs 32 B/elem)
+    # N = 1: also time the in-place single-pass variant without the skip (LMSGD_FLAG_NO_SKIP,
+    # BASELINE.json configs[1] "fused fp16-pack + blended update") and the guarded mode the
+    # headline does not use
     variants = None
     if world == 1 and not flags and not args.no_profile:
         ctxf = L.lmsgd_init(1, 0, local, n, LOSS_SCALE, None, L.LMSGD_FLAG_NO_SKIP)
@@ -544,41 +560,45 @@ def main():
                                               "reported but not skipped"}}
         L.lmsgd_finalize(ctxf)
         del thf, df, mf
-        # the guarded step in one pass, out of place (lmsgd_step_out_of_place): the state
-        # ping-pongs between two buffer sets, the non-finite guard costs no extra pass
+        # the guarded step the headline does not run: in place (lmsgd_step, pack + update,
+        # 32 B/elem) when the headline is out of place, and vice versa
         ctxo = L.lmsgd_init(1, 0, local, n, LOSS_SCALE)
-        sets = [(theta.clone(), delta.clone(), m.clone()), (torch.empty_like(theta), torch.empty_like(delta),
-                                                            torch.empty_like(m))]
-        pset = [tuple(P(x.data_ptr()) for x in st_) for st_ in sets]
+        vs = [(theta.clone(), delta.clone(), m.clone()), (torch.empty_like(theta), torch.empty_like(delta),
+                                                          torch.empty_like(m))]
+        pset = [tuple(P(x.data_ptr()) for x in st_) for st_ in vs]
         gp_ = P(grads.data_ptr())
 
-        def step_oop(i):
+        def step_other(i):
             a_, b_ = pset[i & 1], pset[(i & 1) ^ 1]
-            r_ = lib.lmsgd_step_out_of_place(ctxo.ptr, sp, a_[0], b_[0], gp_, a_[1], b_[1], a_[2], b_[2],
-                                             ctypes.byref(coeffs[i]))
+            if oop:
+                r_ = lib.lmsgd_step(ctxo.ptr, sp, a_[0], gp_, a_[1], a_[2], ctypes.byref(coeffs[i]))
+            else:
+                r_ = lib.lmsgd_step_out_of_place(ctxo.ptr, sp, a_[0], b_[0], gp_, a_[1], b_[1], a_[2], b_[2],
+                                                 ctypes.byref(coeffs[i]))
             if r_ != 0:
                 raise L.LmsgdError(r_, lib.lmsgd_last_error(ctxo.ptr).decode())
 
         for i in range(args.warmup):
-            step_oop(i)
+            step_other(i)
         torch.cuda.synchronize()
         e0.record(stream)
         for i in range(args.steps):
-            step_oop(args.warmup + i)
+            step_other(args.warmup + i)
         e1.record(stream)
         torch.cuda.synchronize()
         oms = e0.elapsed_time(e1) / args.steps
         codeo, _ = L.lmsgd_query_status(ctxo)
         assert codeo == 0
-        variants["guarded_out_of_place"] = {
+        vb = UPDATE_BYTES_PER_ELEM + PACK_BYTES_PER_ELEM if oop else FUSED_BYTES_PER_ELEM
+        variants["guarded_in_place" if oop else "guarded_out_of_place"] = {
             "ms_per_step": oms, "value": 1e3 / oms, "unit": UNIT,
-            "hbm_gbs_algorithmic": FUSED_BYTES_PER_ELEM * n / (oms * 1e-3) / 1e9,
-            "frac_of_measured_hbm": FUSED_BYTES_PER_ELEM * n / (oms * 1e-3) / 1e9 / peak,
-            "gpu_launches_per_step": 2,
-            "note": "lmsgd_step_out_of_place: same results and non-finite skip as the headline, one pass "
-                    "(28 B/elem) with the state alternating between two buffer sets"}
+            "hbm_gbs_algorithmic": vb * n / (oms * 1e-3) / 1e9,
+            "frac_of_measured_hbm": vb * n / (oms * 1e-3) / 1e9 / peak, "gpu_launches_per_step": 2,
+            "note": ("lmsgd_step in place: k_pack + k_update (32 B/elem), the same results and skip" if oop else
+                     "lmsgd_step_out_of_place: the same results and skip in one pass (28 B/elem), the state "
+                     "alternating between two buffer sets")}
         L.lmsgd_finalize(ctxo)
-        del sets
+        del vs
 
     # SGD phase (alpha_RMSprop = 0, t >= 490 at 32k: 86% of the 3,519 steps), with and
     # without LMSGD_FLAG_FREEZE_M (m not touched: 18 instead of 26 B/elem in the update)
@@ -591,14 +611,27 @@ def main():
             L.connect_process_group(ctxv)
             thv, dv_, mv = theta.clone(), delta.clone(), m.clone()
             pv = (P(thv.data_ptr()), P(grads.data_ptr()), P(dv_.data_ptr()), P(mv.data_ptr()))
+            vo = oop and name == "sgd_phase"   # the headline's own mode, out of place at N = 1
+            if vo:
+                thw, dw, mw = torch.empty_like(thv), torch.empty_like(dv_), torch.empty_like(mv)
+                pw = (P(thw.data_ptr()), pv[1], P(dw.data_ptr()), P(mw.data_ptr()))
+
+            def vstep(i):
+                if vo:
+                    a_, b_ = (pv, pw) if i % 2 == 0 else (pw, pv)
+                    lib.lmsgd_step_out_of_place(ctxv.ptr, sp, a_[0], b_[0], pv[1], a_[2], b_[2], a_[3], b_[3],
+                                                ctypes.byref(csgd[i]))
+                else:
+                    lib.lmsgd_step(ctxv.ptr, sp, *pv, ctypes.byref(csgd[i]))
+
             for i in range(args.warmup):
-                lib.lmsgd_step(ctxv.ptr, sp, *pv, ctypes.byref(csgd[i]))
+                vstep(i)
             torch.cuda.synchronize()
             barrier()
             torch.cuda.synchronize()
             e0.record(stream)
             for i in range(args.steps):
-                lib.lmsgd_step(ctxv.ptr, sp, *pv, ctypes.byref(csgd[args.warmup + i]))
+                vstep(args.warmup + i)
             e1.record(stream)
             torch.cuda.synchronize()
             barrier()
@@ -608,8 +641,9 @@ def main():
             variants[name] = {"ms_per_step": vms, "value": world * 1e3 / vms, "unit": UNIT, "t_from": t_sgd,
                               "note": ("alpha_RMSprop = 0: the SGD instantiation of the same step"
                                        if name == "sgd_phase" else
-                                       "LMSGD_FLAG_FREEZE_M: theta and Delta bit-identical to the full rule, "
-                                       "m left at its last RMSprop-phase value (not the paper's m_t)")}
+                                       "LMSGD_FLAG_FREEZE_M (in-place lmsgd_step): theta and Delta bit-identical "
+                                       "to the full rule, m left at its last RMSprop-phase value (not the "
+                                       "paper's m_t)")}
             barrier()
             L.lmsgd_finalize(ctxv)
             del thv, dv_, mv
