@@ -60,6 +60,13 @@ def parse():
     return p.parse_args()
 
 
+def workload_name(depth: int, world: int, mode: str) -> str:
+    """config.workload, identical on both arms (the oracle computes the same step)."""
+    if world == 1:
+        return f"resnet{depth}_grad_buffer_fused_pack_update_1gpu_{mode}"
+    return f"resnet{depth}_grad_buffer_fp16_allreduce_update"
+
+
 def env_rank():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -207,7 +214,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3 * (n / ns),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (synth recipe, seeded)",
-        "config": {"workload": f"resnet{args.depth}_grad_buffer_k{k}", "n_params": n, "k": k,
+        "config": {"workload": workload_name(args.depth, k, args.mode), "n_params": n, "k": k,
                    "loss_scale": LOSS_SCALE, "schedule_t": 1},
         "cpu_baseline": {"value": steps_per_s, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
                          "sample": sample},
@@ -662,8 +669,7 @@ def main():
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (paper-shaped: ResNet layout, minibatch-32 noise)",
-            "config": {"workload": (f"resnet{args.depth}_grad_buffer_{'fused_pack_update_1gpu' if world == 1 else 'fp16_allreduce_update'}"
-                                    + (f"_{args.mode}" if world == 1 else "")),
+            "config": {"workload": workload_name(args.depth, world, args.mode),
                        "n_params": n, "k": world, "wire": "f16", "loss_scale": LOSS_SCALE,
                        "schedule": "slow-start 32k (n=1024, b_local=32), t from %d" % args.t_start,
                        "l2": f"inputs {inputs_bytes / 1e9:.2f} GB > 126 MB L2 (no flush needed)",
