@@ -51,7 +51,6 @@ struct lmsgd_ctx {
     cudaStream_t last_stream = nullptr;
     lmsgd::Launch L{};
     int64_t timeout_ns = 10'000'000'000LL;
-    bool fold = false;                // world 2: k_xupdate_fold (LMSGD_FOLD2=0 selects the owner reduce)
     std::string err;
     // profiling (lmsgd_profile_enable): event pairs around each kernel launch
     struct Rec { int phase; cudaEvent_t a, b; };
@@ -149,10 +148,7 @@ Layout make_layout(int world, int64_t n) {
     L.shard = align_up((n + world - 1) / world, 64);
     if (L.shard == 0) L.shard = 64;
     L.off_recv = 0;
-    // world > 1: receive slots double-buffered by step parity (the world-2 fold path reads
-    // a peer's slots during its update while that peer may already push the next step)
-    L.recv_par = world > 1 ? align_up(2 * L.shard * world, 256) : 0;
-    int64_t off = align_up(L.off_recv + (world > 1 ? 2 * L.recv_par : 2 * L.shard), 256);
+    int64_t off = align_up(L.off_recv + 2 * L.shard * world, 256);
     if (world > 1) {
         L.off_R = off;
         off = align_up(off + 2 * L.shard, 256);
@@ -289,10 +285,6 @@ lmsgd_status lmsgd_init(lmsgd_ctx** out, int world, int rank, int device, int64_
     c->lay = make_layout(world, n_params);
     c->n_pad = c->lay.shard * world;
     if (const char* t = std::getenv("LMSGD_TIMEOUT_MS")) c->timeout_ns = std::atoll(t) * 1000000LL;
-    {
-        const char* f = std::getenv("LMSGD_FOLD2");
-        c->fold = world == 2 && !(f && f[0] == '0');
-    }
     DeviceGuard g(device);
     auto bail = [&](lmsgd_status s) { c->connected = false; lmsgd_finalize(c); return s; };
     if ((e = cudaMalloc(&c->buf, c->lay.bytes)) != cudaSuccess) { g_err = "cudaMalloc exchange buffer"; return bail(LMSGD_ERR_CUDA); }
@@ -418,8 +410,7 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
         return LMSGD_OK;
     }
     const lmsgd::XArgs x = xargs(c, epoch, &c->dstate->xepoch);
-    lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, nullptr, 0, nullptr, nullptr,
-                   c->fold ? 1 : 0};
+    lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, nullptr, 0, nullptr};
     CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, c->L, a); }));
     return LMSGD_OK;
 }
@@ -560,7 +551,7 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
     lmsgd::XArgs x = xargs(c, 0, &c->dstate->xepoch);
     if (x.trace) { x.trace = nullptr; --c->trace_steps; }   // the trace ring slot would be frozen in a graph
     lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, c->d_ctab, c->ctab_count,
-                   &c->dstate->cursor, nullptr, c->fold ? 1 : 0};
+                   &c->dstate->cursor};
     CK(c, lmsgd::launch_xstep(s, c->L, a));
     return LMSGD_OK;
 }

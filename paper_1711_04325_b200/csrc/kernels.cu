@@ -259,28 +259,6 @@ __device__ __forceinline__ void reduce8(const uint16_t* __restrict__ slots, int6
                                                   o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
 }
 
-// The same exact sum and rounding as reduce8 for K slots, returned as the 8-element
-// wire word.
-template <int K>
-__device__ __forceinline__ uint4 reduce8_word(const uint16_t* slots, int64_t stride, int64_t j0, unsigned& sat) {
-    uint4 q[K];
-#pragma unroll
-    for (int p = 0; p < K; ++p)   // every slot's load in flight before the sums
-        q[p] = *reinterpret_cast<const uint4*>(slots + (int64_t)p * stride + j0);
-    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#pragma unroll
-    for (int p = 0; p < K; ++p) {
-        const uint32_t w[4] = {q[p].x, q[p].y, q[p].z, q[p].w};
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] += (double)h2f(w[e >> 1], e & 1);
-    }
-    unsigned short o[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) o[e] = sat16_f64(acc[e], sat);
-    return make_uint4(o[0] | (uint32_t)o[1] << 16, o[2] | (uint32_t)o[3] << 16, o[4] | (uint32_t)o[5] << 16,
-                      o[6] | (uint32_t)o[7] << 16);
-}
-
 __device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 
@@ -507,11 +485,6 @@ __device__ __forceinline__ int64_t* status_of(const XArgs& x, const Ep& ep, int 
     return reinterpret_cast<int64_t*>(x.peers.base[owner] + x.lay.off_status) + ep.par * ST_WORDS;
 }
 
-// Receive slots of rank r for this step's parity: uint16 [world][shard].
-__device__ __forceinline__ uint16_t* recv_of(const XArgs& x, const Ep& ep, int r) {
-    return reinterpret_cast<uint16_t*>(x.peers.base[r] + x.lay.off_recv + (int64_t)ep.par * x.lay.recv_par);
-}
-
 __device__ __forceinline__ void stamp(const XArgs& x, int which) {
     if (x.trace) x.trace[which] = (int64_t)globaltimer();
 }
@@ -673,7 +646,8 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
             const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
             float xv[8];
             load8_g(a.g, j0, x.n, xv);
-            uint16_t* dst = recv_of(x, ep, owner) + (int64_t)x.rank * x.lay.shard + (gi << 3);
+            uint16_t* dst = reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
+                            (int64_t)x.rank * x.lay.shard + (gi << 3);
             *reinterpret_cast<uint4*>(dst) = pack8(xv, a.scale, j0, first, sat);
         }
         flush_status(first, sat, mine, ST_PACK_SAT);
@@ -722,8 +696,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
             stamp(x, TR_RED_START);
         }
     }
-    if (!s_ok || a.fold) {   // fold (world 2): the update sums the receive slots itself
-        if (a.fold && blockIdx.x == 0 && t0) { stamp(x, TR_RED_GO); stamp(x, TR_RED_END); }
+    if (!s_ok) {
         if (t0) atomicAdd(a.ctr + 1, 1u);
         return;
     }
@@ -733,7 +706,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     //         its units has finished all its units.
     //         Runs even for a step that will be skipped (its R is then never read).
     if (blockIdx.x == 0 && t0) stamp(x, TR_RED_GO);
-    const uint16_t* recv = recv_of(x, ep, x.rank);
+    const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
     uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
     unsigned sat = 0;
     for (int64_t u = blockIdx.x; u < ups; u += gridDim.x) {
@@ -840,72 +813,6 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
     }
 }
 
-// World 2, fold mode: no owner reduce and no R buffer.  Every rank sums, for every
-// element, the two receive slots of the element's owner (its own slots locally, the
-// peer's over NVLink: 4 instead of 2 B per remote element) exactly in fp64 and rounds
-// once -- the same R as the owner would compute -- then updates.  Waits: flag A of both
-// ranks (all pushes landed) and the local decision D, in three lanes at once.
-// Saturations of the sum are counted over all elements on every rank (k_xfinalize then
-// reads only its own count).  The receive slots are double-buffered by step parity, so a
-// peer may push the next step while this rank still reads this one.
-template <bool RMS, bool WD, bool KM>
-__global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate_fold(XStep a) {
-    const XArgs& x = a.x;
-    const Ep ep = get_ep(x);
-    __shared__ UpdConst s_c;
-    __shared__ int s_range;
-    __shared__ int s_ok[32];
-    const int lane = threadIdx.x & 31;
-    if (threadIdx.x == 0) {   // graph mode: this step's coefficients from the device table
-        s_c = a.c;
-        s_range = 0;
-        if (a.ctab) {
-            const int64_t idx = *reinterpret_cast<volatile const int64_t*>(a.cursor);
-            s_range = idx >= a.ctab_count;
-            s_c = a.ctab[s_range ? a.ctab_count - 1 : idx];
-        }
-        if (blockIdx.x == 0) stamp(x, TR_UPD_START);
-    }
-    if (threadIdx.x < 32) {
-        int ok = 1;
-        const uint32_t* f = nullptr;
-        if (lane < x.world) f = flag_slot(x, x.rank, FLAG_A) + lane;
-        else if (lane == 31) f = flag_slot(x, x.rank, FLAG_D);
-        if (f && !spin_flag(x, ep, f)) ok = 0;
-        if (lane == 31 && ok) {
-            const volatile int64_t* vm = status_of(x, ep, x.rank);
-            if (vm[ST_G_FIRST] != kNone || vm[ST_G_ERROR] != 0) ok = 0;   // skipped step
-        }
-        if (f && !ok && lane != 31) status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
-        s_ok[lane] = ok;
-    }
-    __syncthreads();
-    int go = 1;
-    for (int p = 0; p < 32; ++p) go &= s_ok[p];
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_UPD_GO);
-    if (!go || s_range) return;
-    const UpdConst c = s_c;
-    const int64_t gsh = x.lay.shard >> 3;
-    const int64_t ups = (gsh + kThreads - 1) / kThreads;
-    const int64_t kcu = (int64_t)x.world * x.lay.cu;
-    unsigned sat = 0;
-#pragma unroll
-    for (int v = 0; v < kXUnits; ++v) {
-        const int64_t i = (int64_t)blockIdx.x * kXUnits + v;
-        const int cc = (int)(i / kcu);
-        const int64_t r = i - (int64_t)cc * kcu;
-        const int owner = (int)((r % x.world + x.rank) % x.world);
-        const int64_t u = cc < x.lay.nchunks ? (int64_t)cc * x.lay.cu + r / x.world : ups;
-        if (u >= ups) continue;
-        const int64_t gi = u * kThreads + threadIdx.x;
-        if (gi >= gsh) continue;
-        const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
-        const uint4 w = reduce8_word<2>(recv_of(x, ep, owner), x.lay.shard, gi << 3, sat);   // world 2
-        if (j0 < x.n) update8<RMS, WD, KM>(w, j0, x.n, c, a.th, a.d, a.m);
-    }
-    flush_status(kNone, sat, status_of(x, ep, x.rank), ST_SUM_SAT);
-}
-
 // lmsgd_exchange, world > 1: the all-gather half of the fp16 all-reduce (row a4) on
 // its own, as a flat pull into the caller's buffer.  Same unit order and waits as
 // k_xupdate (chunk-major, owner-interleaved; the owner's chunk flag),
@@ -973,9 +880,7 @@ __global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
     if (!err && a.ctab && *a.cursor >= a.ctab_count) err = (int64_t)LMSGD_ERR_RANGE;   // table exhausted
     const bool skip = gfirst != kNone || err != 0;
     int64_t ssat = 0;
-    if (!skip && a.fold)   // every rank counted the saturations of all elements itself
-        ssat = static_cast<const volatile int64_t*>(mine)[ST_SUM_SAT];
-    else if (!skip)
+    if (!skip)
         for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, ep, p))[ST_SUM_SAT];
     store_last(a.last, gfirst, mine[ST_G_PACK_SAT], ssat, err, skip);
     stamp(x, TR_UPD_END);
@@ -1050,7 +955,6 @@ int grid_for(const Launch&, int64_t work_items) {
 struct UpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_update<R, W, K>; } };
 struct Fused1K { template <bool R, bool W, bool K> static constexpr auto get() { return k_fused1<R, W, K>; } };
 struct XUpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_xupdate<R, W, K>; } };
-struct XUpdateFoldK { template <bool R, bool W, bool K> static constexpr auto get() { return k_xupdate_fold<R, W, K>; } };
 template <typename K>
 auto pick_variant(const UpdConst& c, bool graph) {
     const bool rms = c.a_rms != 0.0f || graph, wd = c.n_wd > 0, km = rms || !c.freeze_m;
@@ -1112,8 +1016,7 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
         e = launch_pdl_if(pdl, k_xgather, grid, kThreads, s, a);
     } else {
         const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits);
-        e = a.fold ? launch_pdl_if(pdl, pick_variant<XUpdateFoldK>(a.c, a.ctab != nullptr), grid, kThreads, s, a)
-                   : launch_pdl_if(pdl, pick_variant<XUpdateK>(a.c, a.ctab != nullptr), grid, kThreads, s, a);
+        e = launch_pdl_if(pdl, pick_variant<XUpdateK>(a.c, a.ctab != nullptr), grid, kThreads, s, a);
     }
     if (e != cudaSuccess) return e;
     return launch_pdl_if(true, k_xfinalize, 1, 32, s, a, (unsigned int)L.grid_xstep);

@@ -30,9 +30,7 @@ struct UpdConst {
 // Layout of one rank's exchange buffer (CUDA IPC-shared when world > 1).
 struct Layout {
     int64_t shard;        // elements per rank shard (multiple of 64)
-    int64_t off_recv;     // uint16 [2 parity][world][shard] (world > 1): slot p = rank p's packed
-                          // values of MY shard for steps of that parity; world 1: the packed h
-    int64_t recv_par;     // bytes between the two parity halves of the receive slots (0 at world 1)
+    int64_t off_recv;     // uint16 [world][shard]: slot p = rank p's packed values of MY shard
     int64_t off_R;        // uint16 [shard]: this rank's reduced shard (wire-2 payload)
     int64_t off_status;   // int64 [2 parity][ST_WORDS]
     int64_t off_flags;    // uint32: A at +0, B at +128 B, C at +256 B, D at +384 B, each [LMSGD_MAX_WORLD]
@@ -130,8 +128,6 @@ struct XStep {
     int64_t* cursor;         // graph mode: device index of the next step's coefficients
     uint16_t* rout;          // lmsgd_exchange: the caller's [n_pad] all-reduce output (k_xgather
                              // replaces k_xupdate); NULL for a step
-    int fold;                // world 2 step: no owner reduce; every rank sums both receive slots
-                             // of every element inside the update (k_xupdate_fold)
 };
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a);
 int xstep_blocks_per_sm();
