@@ -207,7 +207,8 @@ lmsgd_status lmsgd_step(lmsgd_ctx* ctx, void* stream, float* params, const float
  * inputs (skipped = 1, LMSGD_ERR_NONFINITE from lmsgd_query_status).  Either way the
  * *_out buffers hold the state after the step, so the caller alternates two buffer sets
  * (ping-pong) without synchronising.  Results are bit-identical to lmsgd_step.
- * Errors: INVALID_ARG (NULL / misaligned / overlapping buffers, bad coeffs),
+ * Like lmsgd_step it bakes the step's status slot into its launches: not for CUDA-graph
+ * capture.  Errors: INVALID_ARG (NULL / misaligned / overlapping buffers, bad coeffs),
  * UNSUPPORTED (world > 1 -- there lmsgd_step's skip decision is free -- or weight decay
  * set), STATE (a context that runs lmsgd_step_graph). */
 lmsgd_status lmsgd_step_out_of_place(lmsgd_ctx* ctx, void* stream, const float* params_in, float* params_out,
