@@ -1084,6 +1084,15 @@ cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, in
     cudaError_t e = launch_pdl(c.a_rms != 0.0f ? k_fused1_oop<true> : k_fused1_oop<false>, grid, kThreads, s, g, n,
                                scale, c, thi, di, mi, tho, dout, mo, st, st_reset);
     if (e != cudaSuccess) return e;
+#ifndef LMSGD_REPAIR_BLOCKS
+// k_repair1 grid: n blocks of 512 threads, or 0 = 4 x SMs.  One block: 105.1 vs 106.4 us
+// per clean step (profiles/r1/ab/repair_grid_n1.txt); the price is a slow copy (a few ms
+// for ResNet-50) on the rare skipped step.
+#define LMSGD_REPAIR_BLOCKS 1
+#endif
+    if (LMSGD_REPAIR_BLOCKS > 0)
+        return launch_pdl_if(true, k_repair1, LMSGD_REPAIR_BLOCKS, 512, s, (const int64_t*)st, thi, di, mi, tho,
+                             dout, mo, n, last);
     return launch_pdl_if(true, k_repair1, 4 * L.sm_count, kThreads, s, (const int64_t*)st, thi, di, mi, tho, dout,
                          mo, n, last);
 }
