@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(256) k_upd_pull(Ptrs P, int world, int rank, i
     if (j0 >= n) return;
     (void)ups;
     const uint4 r = *reinterpret_cast<const uint4*>(P.R[owner] + (gi << 3));
-    update8<true>(r, j0, n, c, th, d, m);
+    update8<true, false>(r, j0, n, c, th, d, m);
 }
 
 // the same with a register cap (more resident blocks per SM to cover the peer-load latency)
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256, MINB) k_upd_pull_lb(Ptrs P, int world, in
     const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
     if (j0 >= n) return;
     const uint4 r = *reinterpret_cast<const uint4*>(P.R[owner] + (gi << 3));
-    update8<true>(r, j0, n, c, th, d, m);
+    update8<true, false>(r, j0, n, c, th, d, m);
 }
 
 // R prefetched with cp.async (LDGSTS) into shared memory for the NEXT unit of a 2-unit block
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(256) k_upd_pull2(Ptrs P, int world, int rank, 
         const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
         if (j0 >= n) continue;
         const uint4 r = *reinterpret_cast<const uint4*>(P.R[owner] + (gi << 3));
-        update8<true>(r, j0, n, c, th, d, m);
+        update8<true, false>(r, j0, n, c, th, d, m);
     }
 }
 
@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(256) k_upd_pull_nc(Ptrs P, int world, int rank
     const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
     if (j0 >= n) return;
     const uint4 r = __ldg(reinterpret_cast<const uint4*>(P.R[owner] + (gi << 3)));
-    update8<true>(r, j0, n, c, th, d, m);
+    update8<true, false>(r, j0, n, c, th, d, m);
 }
 
 // update pull with the unit's R fetched by one bulk copy (TMA engine) into shared memory
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(256) k_upd_pull_bulk(Ptrs P, int world, int ra
     }
     mbar_wait(&bar, 0);
     if (!act) return;
-    if (j0 + 8 > n) { update8<true>(sR[threadIdx.x], j0, n, c, th, d, m); return; }
+    if (j0 + 8 > n) { update8<true, false>(sR[threadIdx.x], j0, n, c, th, d, m); return; }
     const uint4 r = sR[threadIdx.x];
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
     float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
