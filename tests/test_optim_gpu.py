@@ -115,3 +115,33 @@ def test_lmsgd_out_of_place_matches_in_place(monkeypatch):
         assert all(torch.equal(a, b) for a, b in zip(nets[0].parameters(), nets[1].parameters()))
     for o in opts:
         o.close()
+
+
+def test_lmsgd_out_of_place_resume(monkeypatch):
+    # checkpoint/resume in the out-of-place mode: the state lives in whichever buffer set
+    # is current; a fresh optimizer restored from the checkpoint continues bit-identically
+    monkeypatch.setattr(torch.backends.cudnn, "deterministic", True)
+    monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
+    net = _net()
+    opt = L.LMSGD(net.parameters(), cluster=L.make_cluster(2, 32, 64))
+    assert opt.out_of_place
+    for t in range(1, 4):   # odd number of steps: the current set is the second one
+        _train_step(net, opt, t)
+        opt.step()
+    ck_model = {k: v.clone() for k, v in net.state_dict().items()}
+    ck_opt = opt.state_dict()
+    for t in range(4, 7):
+        _train_step(net, opt, t)
+        opt.step()
+    torch.cuda.synchronize()
+    net2 = _net(seed=1)
+    opt2 = L.LMSGD(net2.parameters(), cluster=L.make_cluster(2, 32, 64))
+    net2.load_state_dict(ck_model)
+    opt2.load_state_dict(ck_opt)
+    for t in range(4, 7):
+        _train_step(net2, opt2, t)
+        opt2.step()
+    torch.cuda.synchronize()
+    assert torch.equal(opt.flat_p, opt2.flat_p) and torch.equal(opt.delta, opt2.delta) and torch.equal(opt.m, opt2.m)
+    opt.close()
+    opt2.close()
