@@ -209,8 +209,8 @@ lmsgd_status lmsgd_step(lmsgd_ctx* ctx, void* stream, float* params, const float
  * (ping-pong) without synchronising.  Results are bit-identical to lmsgd_step.
  * Like lmsgd_step it bakes the step's status slot into its launches: not for CUDA-graph
  * capture.  Errors: INVALID_ARG (NULL / misaligned / overlapping buffers, bad coeffs),
- * UNSUPPORTED (world > 1 -- there lmsgd_step's skip decision is free -- or weight decay
- * set), STATE (a context that runs lmsgd_step_graph). */
+ * UNSUPPORTED (world > 1 -- there lmsgd_step's skip decision is free --, weight decay
+ * set, or a context created with flags != 0: the call always guards and keeps m), STATE (a context that runs lmsgd_step_graph). */
 lmsgd_status lmsgd_step_out_of_place(lmsgd_ctx* ctx, void* stream, const float* params_in, float* params_out,
                                      const float* grads, const float* delta_in, float* delta_out,
                                      const float* m_in, float* m_out, const lmsgd_coeffs* coeffs);

@@ -445,6 +445,8 @@ lmsgd_status lmsgd_step_out_of_place(lmsgd_ctx* c, void* stream, const float* pa
         return fail(c, LMSGD_ERR_INVALID_ARG, "coeffs: need eta > 0, 0 <= alpha_sgd <= 1, alpha_rmsprop >= 0");
     if (c->world != 1) return fail(c, LMSGD_ERR_UNSUPPORTED, "out-of-place step is world == 1 only (use lmsgd_step)");
     if (c->wd != 0.0) return fail(c, LMSGD_ERR_UNSUPPORTED, "out-of-place step has no weight decay");
+    if (c->flags != 0)
+        return fail(c, LMSGD_ERR_UNSUPPORTED, "out-of-place step: a context created with flags (NO_SKIP / FREEZE_M)");
     if (c->mode == 2) return fail(c, LMSGD_ERR_STATE, "this context runs lmsgd_step_graph");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -728,6 +728,10 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
             const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
             if (atomicAdd(a.ctr + 4 + c, 1u) + 1u == cnt) {
                 a.ctr[4 + c] = 0;
+                // the other blocks fenced their R writes before their tickets; this fence
+                // orders the observed tickets (hence those writes) before the flag stores
+                // peers acquire (cumulativity), as publish() does after its ticket
+                __threadfence_system();
                 if (!fv) fv = cflag_value(x, ep);
                 for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, c, x.rank), fv);
             }

@@ -13,11 +13,15 @@ tensor with more than one dimension -- conv and fc weights; BN and biases exclud
 Goyal et al.'s convention) are placed first in the flat buffer so the library's
 decayed prefix covers exactly them.
 
-Out of place (world 1, the default there without weight decay): the parameters,
-Delta and m live in two buffer sets; each step reads one set and writes the other
-through ``lmsgd_step_out_of_place`` (the guarded step in one pass over HBM, 28 instead
-of 32 B/elem), then the parameters' ``.data`` are re-pointed at the new set.  Results
-are bit-identical to the in-place step.
+Out of place (``out_of_place=True``; opt-in, world 1, no weight decay, no flags): the
+parameters, Delta and m live in two buffer sets; each step reads one set and writes
+the other through ``lmsgd_step_out_of_place`` (the guarded step in one pass over HBM,
+28 instead of 32 B/elem), then the parameters' ``.data`` are re-pointed at the new
+set.  Results are bit-identical to the in-place step.  The price: every parameter's
+storage address alternates between two buffers from step to step, so anything that
+caches a parameter's storage -- a forward/backward captured in a CUDA graph, a
+saved ``p.data`` or ``flat_p`` -- would keep reading the stale set.  That is why the
+mode is off by default; use the in-place step (the default) with captured graphs.
 
 Checkpoint/resume: ``state_dict`` holds the step counter t and the optimizer state
 (Delta, m) -- with the parameters, everything the next step depends on.
@@ -39,7 +43,7 @@ class LMSGD:
     def __init__(self, params: Iterable[torch.Tensor], *, cluster: L.Cluster | None = None,
                  hyper: L.Hyper | None = None, loss_scale: float = 1024.0, weight_decay: float = 0.0,
                  decay: Callable[[torch.Tensor], bool] = _default_decay, flags: int = 0,
-                 group=None, t_start: int = 1, out_of_place: bool | None = None):
+                 group=None, t_start: int = 1, out_of_place: bool = False):
         params = [p for p in params if p.requires_grad]
         if not params:
             raise ValueError("no trainable parameters")
@@ -55,10 +59,8 @@ class LMSGD:
         dist_on = dist.is_available() and dist.is_initialized()
         world = dist.get_world_size(group) if dist_on else 1
         rank = dist.get_rank(group) if dist_on else 0
-        if out_of_place is None:
-            out_of_place = world == 1 and not weight_decay and flags == 0
-        if out_of_place and (world != 1 or weight_decay):
-            raise ValueError("out_of_place needs world == 1 and no weight decay")
+        if out_of_place and (world != 1 or weight_decay or flags):
+            raise ValueError("out_of_place needs world == 1, no weight decay and flags == 0")
         self.out_of_place = bool(out_of_place)
         nsets = 2 if self.out_of_place else 1
         self._p = [torch.empty(self.n, dtype=torch.float32, device=dev) for _ in range(nsets)]

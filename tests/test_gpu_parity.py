@@ -4,7 +4,7 @@ Bar (BASELINE.json north_star):
   * fp16 wire payloads R and the averaged gradient ghat: bit-exact (the sum is exact);
   * schedule: bit-exact (tests/test_lib_host.py);
   * fp32 state after one step, oracle resynced to the GPU's previous state:
-    |x_gpu - x_oracle| <= 1e-6 * scale_x with scale_m = m_t + (1-mu2) |ghat|^2,
+    |x_gpu - x_oracle| <= 1e-6 * scale_x with scale_m = m_t (+ (1-mu2)(|ghat| + lambda|theta|)^2 with weight decay),
     scale_Delta = mu1 |Delta_{t-1}| + |c ghat|, scale_theta = |theta_{t-1}| + eta scale_Delta;
   * status words (first non-finite index, saturation counts): exact.
 """
@@ -46,7 +46,9 @@ def check_state(th_g, d_g, m_g, th0, d0, m0, ghat, c, hyper=schedule.Hyper(), to
         gh[:k] += wd * np.abs(np.asarray(th0, np.float64)[:k])
     coef = c.alpha_sgd + c.alpha_rmsprop / (np.sqrt(m_o) + hyper.eps)
     scale_d = hyper.mu1 * np.abs(np.asarray(d0, np.float64)) + coef * gh
-    scale_m = m_o + (1.0 - hyper.mu2) * gh * gh
+    # wd = 0: m_t is a sum of non-negative fp32 terms, so m_t itself bounds its rounding;
+    # with wd the fp32 g + lambda theta is exact only to (|g| + lambda|theta|) (R12)
+    scale_m = m_o + (1.0 - hyper.mu2) * gh * gh if wd else m_o
     e = {
         "m": run.scaled_error(m_g, m_o, scale_m),
         "delta": run.scaled_error(d_g, d_o, scale_d),
@@ -442,6 +444,13 @@ def test_step_out_of_place_matches_step(n):
         L.lmsgd_step_out_of_place(oop, *(bufs[0][0], bufs[1][0]), dev(g), bufs[0][1], bufs[1][1], bufs[0][2],
                                   bufs[1][2], co)
     assert e.value.status == L.LMSGD_ERR_UNSUPPORTED
+    for fl in (L.LMSGD_FLAG_NO_SKIP, L.LMSGD_FLAG_FREEZE_M):   # the call always guards and keeps m
+        cf = L.lmsgd_init(1, 0, 0, n, s, None, fl)
+        with pytest.raises(L.LmsgdError) as e:
+            L.lmsgd_step_out_of_place(cf, bufs[0][0], bufs[1][0], dev(g), bufs[0][1], bufs[1][1], bufs[0][2],
+                                      bufs[1][2], co)
+        assert e.value.status == L.LMSGD_ERR_UNSUPPORTED
+        L.lmsgd_finalize(cf)
     L.lmsgd_finalize(ref)
     L.lmsgd_finalize(oop)
 
@@ -492,6 +501,56 @@ def test_resnet_full_size_sampled(depth, t, flags):
     check_state(host(th)[idx], host(d)[idx], host(m)[idx], th0[idx], d0[idx], m0[idx], ex.ghat,
                 schedule.coeffs_at(t))
     L.lmsgd_finalize(ctx)
+
+
+@pytest.mark.parametrize("depth,t0", [(50, 1), (50, 489), (152, 1), (152, 3518)])
+def test_resnet_full_size_out_of_place_sampled(depth, t0):
+    """The N = 1 headline kernel pair (k_fused1_oop + k_repair1, lmsgd_step_out_of_place)
+    at the C2 / C5 sizes, in bench.py's launch configuration, over three steps with the
+    state ping-ponging between two buffer sets: a clean step (sampled oracle parity and
+    full-buffer bit-identity with the in-place lmsgd_step), a step with one non-finite
+    gradient (skipped: the output set equals the input set bit for bit, status exact),
+    and a clean step continuing from the repaired set (sampled parity again)."""
+    n = synth.resnet_n_params(depth)
+    s = 1024.0
+    r = np.random.default_rng(t0)
+    idx = np.unique(np.concatenate([np.arange(1000), np.arange(n - 1000, n), r.integers(0, n, 200_000)]))
+    th0 = synth.theta0(n, depth)
+    d0 = (r.standard_normal(n) * 1e-3).astype(np.float32)
+    m0 = (r.random(n) * 1e-6).astype(np.float32)
+    oop = L.lmsgd_init(1, 0, 0, n, s)
+    ref = L.lmsgd_init(1, 0, 0, n, s)
+    sets = [[dev(th0), dev(d0), dev(m0)], [torch.empty(n, device=DEV) for _ in range(3)]]
+    inplace = [dev(th0), dev(d0), dev(m0)]
+    a = synth.grad_scale(n)
+    cur = 0
+    for i, t in enumerate((t0, t0 + 1, t0 + 2)):
+        g = synth.grads(1, t, n, a)[0]
+        if i == 1:
+            g[n - 5] = np.nan                    # inside the last (ragged) vector group
+            g[n // 3] = -np.inf
+        co = L.lmsgd_schedule_at(None, K32_C, t)
+        src, dst = sets[cur], sets[cur ^ 1]
+        prev = [host(x)[idx] for x in src]
+        gd = dev(g)
+        L.lmsgd_step_out_of_place(oop, src[0], dst[0], gd, src[1], dst[1], src[2], dst[2], co)
+        code, st = L.lmsgd_query_status(oop)
+        L.lmsgd_step(ref, inplace[0], gd, inplace[1], inplace[2], co)
+        code_r, _ = L.lmsgd_query_status(ref)
+        assert code == code_r
+        assert all(torch.equal(x, y) for x, y in zip(dst, inplace)), (depth, t)
+        if i == 1:
+            assert code == L.LMSGD_ERR_NONFINITE and st.skipped == 1 and st.first_nonfinite == n // 3
+            assert all(torch.equal(x, y) for x, y in zip(dst, src))
+        else:
+            assert code == 0 and st.skipped == 0 and st.first_nonfinite == -1
+            ex = exchange.exchange([g[idx]], s)
+            assert st.pack_saturations == exchange.exchange([g], s).pack_saturations
+            check_state(host(dst[0])[idx], host(dst[1])[idx], host(dst[2])[idx], *prev, ex.ghat,
+                        schedule.coeffs_at(t))
+        cur ^= 1
+    L.lmsgd_finalize(oop)
+    L.lmsgd_finalize(ref)
 
 
 # ------------------------------------------------------------------ API behaviour on the GPU

@@ -95,13 +95,13 @@ def test_lmsgd_rejects_cpu_params():
 
 
 def test_lmsgd_out_of_place_matches_in_place(monkeypatch):
-    # world 1 without weight decay defaults to the out-of-place one-pass step: the
-    # parameters alternate between two flat buffers, results bit-identical to in place
+    # out_of_place=True (opt-in, world 1, no weight decay): the parameters alternate
+    # between two flat buffers, results bit-identical to in place (the default)
     monkeypatch.setattr(torch.backends.cudnn, "deterministic", True)
     monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
     nets = [_net(), _net()]
-    opts = [L.LMSGD(nets[0].parameters(), cluster=L.make_cluster(2, 32, 64)),
-            L.LMSGD(nets[1].parameters(), cluster=L.make_cluster(2, 32, 64), out_of_place=False)]
+    opts = [L.LMSGD(nets[0].parameters(), cluster=L.make_cluster(2, 32, 64), out_of_place=True),
+            L.LMSGD(nets[1].parameters(), cluster=L.make_cluster(2, 32, 64))]
     assert opts[0].out_of_place and not opts[1].out_of_place
     for t in range(1, 8):
         for net, opt in zip(nets, opts):
@@ -123,7 +123,7 @@ def test_lmsgd_out_of_place_resume(monkeypatch):
     monkeypatch.setattr(torch.backends.cudnn, "deterministic", True)
     monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
     net = _net()
-    opt = L.LMSGD(net.parameters(), cluster=L.make_cluster(2, 32, 64))
+    opt = L.LMSGD(net.parameters(), cluster=L.make_cluster(2, 32, 64), out_of_place=True)
     assert opt.out_of_place
     for t in range(1, 4):   # odd number of steps: the current set is the second one
         _train_step(net, opt, t)
@@ -135,7 +135,7 @@ def test_lmsgd_out_of_place_resume(monkeypatch):
         opt.step()
     torch.cuda.synchronize()
     net2 = _net(seed=1)
-    opt2 = L.LMSGD(net2.parameters(), cluster=L.make_cluster(2, 32, 64))
+    opt2 = L.LMSGD(net2.parameters(), cluster=L.make_cluster(2, 32, 64), out_of_place=True)
     net2.load_state_dict(ck_model)
     opt2.load_state_dict(ck_opt)
     for t in range(4, 7):
@@ -145,3 +145,41 @@ def test_lmsgd_out_of_place_resume(monkeypatch):
     assert torch.equal(opt.flat_p, opt2.flat_p) and torch.equal(opt.delta, opt2.delta) and torch.equal(opt.m, opt2.m)
     opt.close()
     opt2.close()
+
+
+def test_lmsgd_default_in_place_with_captured_forward(monkeypatch):
+    # the default (in place) keeps every parameter's storage fixed, so a forward pass
+    # captured once in a CUDA graph sees the updated weights on every replay
+    monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
+    net = _net()
+    opt = L.LMSGD(net.parameters(), cluster=L.make_cluster(2, 32, 64))
+    assert not opt.out_of_place
+    ptrs = [p.data_ptr() for p in net.parameters()]
+    x = torch.randn(4, 3, 8, 8, device="cuda")
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        net(x)   # warm-up on the capture stream
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        y_static = net(x)
+    for t in range(1, 4):
+        graph.replay()
+        before = y_static.clone()
+        _train_step(net, opt, t)
+        opt.step()
+        graph.replay()
+        torch.cuda.synchronize()
+        with torch.no_grad():
+            eager = net(x)
+        # the replay used the new weights (eager and captured kernels may differ in rounding)
+        assert not torch.equal(y_static, before), t
+        assert torch.allclose(y_static, eager, rtol=1e-4, atol=1e-5), t
+    assert [p.data_ptr() for p in net.parameters()] == ptrs
+    opt.close()
+
+
+def test_lmsgd_out_of_place_rejects_flags():
+    with pytest.raises(ValueError):
+        L.LMSGD(_net().parameters(), out_of_place=True, flags=L.LMSGD_FLAG_FREEZE_M)

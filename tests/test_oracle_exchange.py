@@ -132,3 +132,44 @@ def test_nonfinite_index_is_minimum_over_workers():
     with pytest.raises(b16.NonFiniteError) as e:
         ex.exchange([a, b])
     assert e.value.index == 25
+
+
+# ------------------------------------------------------------------ pins of exchange.ideal
+# ideal(g) = sum_i g_i / k in float64 (the no-wire reference the fp16 deviation is
+# reported against).  Pinned to exact rational arithmetic, a fixed point and the
+# cases where the fp16 wire is exact.
+
+def test_ideal_matches_exact_rational_mean():
+    from fractions import Fraction
+    r = np.random.default_rng(21)
+    for k in (1, 2, 3, 5, 8):
+        g = [(r.standard_normal(64) * 10.0 ** r.uniform(-6, 2, 64)).astype(np.float32) for _ in range(k)]
+        got = ex.ideal(g)
+        for j in range(64):
+            exact = sum(Fraction(float(gi[j])) for gi in g) / k
+            absum = sum(abs(Fraction(float(gi[j]))) for gi in g) / k
+            # k - 1 float64 additions and one division, each within half an ulp
+            assert abs(Fraction(float(got[j])) - exact) <= Fraction(k + 1, 2 ** 53) * absum, (k, j)
+
+
+def test_ideal_of_identical_workers_is_the_gradient():
+    g = (np.random.default_rng(22).standard_normal(1000) * 1e-3).astype(np.float32)
+    for k in (1, 2, 3, 4, 8):
+        assert np.array_equal(ex.ideal([g] * k), g.astype(np.float64))
+
+
+def test_ideal_equals_ghat_where_the_wire_is_exact():
+    # small integer gradients at s = 1: every pack, sum and 1/k (k a power of two) is exact
+    r = np.random.default_rng(23)
+    for k in (1, 2, 4, 8):
+        g = [r.integers(-100, 101, 500).astype(np.float32) for _ in range(k)]
+        assert np.array_equal(ex.exchange(g, 1.0).ghat.astype(np.float64), ex.ideal(g))
+
+
+def test_ideal_is_permutation_invariant_and_linear():
+    r = np.random.default_rng(24)
+    g = [(r.standard_normal(300) * 1e-2).astype(np.float32) for _ in range(4)]
+    base = ex.ideal(g)
+    for perm in itertools.permutations(range(4)):
+        assert np.allclose(ex.ideal([g[i] for i in perm]), base, rtol=4 * 2.0 ** -52, atol=0)
+    assert np.array_equal(ex.ideal([x * np.float32(2.0) for x in g]), 2.0 * base)   # power-of-two scaling

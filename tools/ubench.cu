@@ -8,7 +8,7 @@
 
 namespace lmsgd {
 namespace {
-#include "../paper_1711_04325_b200/csrc/stream_tma.cuh"
+#include "stream_tma.cuh"
 }  // namespace
 }  // namespace lmsgd
 
