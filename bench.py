@@ -11,9 +11,10 @@ warm-up schedule of the 32k run.
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl lmsgd|reference]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-Prints ONE JSON line on rank 0.  value = whole-job update steps/s: global
-synchronous steps/s x N (every GPU applies the update to its replica of the
-buffer each step; per-GPU work is fixed as N grows: weak scaling).
+Prints ONE JSON line on rank 0.  value = global synchronous update steps/s (one step
+= every rank's gradient exchanged and every replica updated; per-GPU work is fixed
+as N grows: weak scaling).  The N-replica figure (steps/s x N) and the aggregate
+gradient elements/s are separate keys.
 """
 from __future__ import annotations
 
@@ -101,7 +102,7 @@ class ClockSampler:
                0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x2: "applications_clocks_setting",
                0x10: "sync_boost"}
 
-    def __init__(self, index: int, period_s: float = 0.01):
+    def __init__(self, index: int, period_s: float = 0.002):
         self.index, self.period = index, period_s
         self.samples, self.reasons = [], set()
         self.max_mhz = None
@@ -147,28 +148,43 @@ class ClockSampler:
 
 # ------------------------------------------------------------------ oracle timing (CPU)
 
-def oracle_rate(k: int, n_full: int, budget_s: float, max_elems: int = 1 << 21):
-    """Time the CPU oracle (as it stands) on slices of the workload; returns
-    (steps/s extrapolated to the full buffer, elems per timed call, calls, seconds)."""
+def oracle_steps(k: int, n_full: int, budget_s: float, n_steps: int | None = None, depth: int = 50,
+                 n_warm: int = 0):
+    """Time the CPU oracle (as it stands) on whole steps of the workload: k workers'
+    pack + exact reduce + fp16 wire + fp64 update of the n_full-element buffer.  If a
+    full-size step does not fit the budget (n_steps steps in budget_s seconds, or at
+    least 2 steps), each step runs on the largest leading slice that does and the
+    rate is extrapolated per element.  Returns (steps/s, elems per step, steps,
+    seconds, extrapolated)."""
     import numpy as np
 
     import synth
     from oracle import exchange, schedule, update
-    ns = min(max_elems, n_full)
-    g = synth.grads(k, 1, ns)
-    th = synth.theta0(ns, None).astype(np.float64)
-    d = np.zeros(ns)
-    m = np.zeros(ns)
+    # calibrate the per-element cost on a 1M slice (one step)
+    cal = min(n_full, 1 << 20)
+    gc = synth.grads(k, 1, cal)
+    t0 = time.perf_counter()
+    ex = exchange.exchange(list(gc), LOSS_SCALE)
     c = schedule.coeffs_at(1)
-    calls, t0 = 0, time.perf_counter()
-    while True:
+    update.step(np.zeros(cal), ex.ghat, np.zeros(cal), np.zeros(cal), c.eta, c.alpha_sgd, c.alpha_rmsprop)
+    per_elem = (time.perf_counter() - t0) / cal
+    want = n_steps if n_steps else max(2, int(budget_s / (per_elem * n_full)))
+    ns = n_full if per_elem * n_full * want <= budget_s * 1.25 else \
+        max(1 << 16, int(budget_s / want / per_elem))
+    g = synth.grads(k, 1, ns)
+    th = synth.theta0(n_full, depth)[:ns].astype(np.float64)
+    d, m = np.zeros(ns), np.zeros(ns)
+    for i in range(n_warm):    # untimed
+        c = schedule.coeffs_at(1 + i)
         ex = exchange.exchange(list(g), LOSS_SCALE)
         th, d, m = update.step(th, ex.ghat, m, d, c.eta, c.alpha_sgd, c.alpha_rmsprop)
-        calls += 1
-        el = time.perf_counter() - t0
-        if el >= budget_s:
-            break
-    return (ns * calls / el) / n_full, ns, calls, el
+    t0 = time.perf_counter()
+    for i in range(want):
+        c = schedule.coeffs_at(1 + i)
+        ex = exchange.exchange(list(g), LOSS_SCALE)
+        th, d, m = update.step(th, ex.ghat, m, d, c.eta, c.alpha_sgd, c.alpha_rmsprop)
+    el = time.perf_counter() - t0
+    return (ns * want / el) / n_full, ns, want, el, ns < n_full
 
 
 def cpu_cores_used():
@@ -179,49 +195,39 @@ def run_reference(args):
     rank, world, _ = env_rank()
     if rank != 0:
         return 0
-    import numpy as np
-
     import synth
-    from oracle import exchange, schedule, update
     k = max(1, args.gpus)
     n = synth.resnet_n_params(args.depth)
-    # calibrate the per-element cost, then size each step's slice so the run ends in ~3 min
-    rate, ns0, calls0, el0 = oracle_rate(k, n, 2.0, 1 << 18)
-    sec_per_elem = 1.0 / (rate * n)
-    total = args.steps + args.warmup
-    ns = int(max(4096, min(n, 1 << 21, 90.0 / total / sec_per_elem)))
-    g = synth.grads(k, 1, ns)
-    th = synth.theta0(ns, None).astype(np.float64)
-    d, m = np.zeros(ns), np.zeros(ns)
-    c = schedule.coeffs_at(1)
-
-    def one():
-        nonlocal th, d, m
-        ex = exchange.exchange(list(g), LOSS_SCALE)
-        th, d, m = update.step(th, ex.ghat, m, d, c.eta, c.alpha_sgd, c.alpha_rmsprop)
-
-    for _ in range(args.warmup):
-        one()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        one()
-    el = time.perf_counter() - t0
-    steps_per_s = (ns * args.steps / el) / n * k        # whole-buffer update steps/s, x k workers
-    sample = (f"each step: oracle pack x{k} workers + exact fp64 reduce + fp16 wire + fp64 update on a "
-              f"{ns}-element slice of the {n}-param buffer; value extrapolated per element to the full buffer")
+    # one untimed warm-up step (the oracle has nothing to warm beyond page faults), then
+    # exactly --steps timed oracle steps; whole steps of the full workload unless the
+    # timed steps would exceed ~3 minutes
+    rate, ns, calls, el, extrap = oracle_steps(k, n, 180.0, args.steps, args.depth, n_warm=min(args.warmup, 1))
+    what = (f"pack x{k} workers + exact fp64 reduce + fp16 wire + fp64 update, NumPy on one core, "
+            f"{calls} steps on ")
+    sample = what + (f"a {ns}-element leading slice of the {n}-param buffer, extrapolated per element"
+                     if extrap else f"the whole {n}-param buffer (no extrapolation)")
     line = {
-        "impl": "reference", "metric": METRIC, "value": steps_per_s, "unit": UNIT, "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps * 1e3 * (n / ns),
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 / rate,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (synth recipe, seeded)",
-        "config": {"workload": workload_name(args.depth, k, args.mode), "n_params": n, "k": k,
-                   "loss_scale": LOSS_SCALE, "schedule_t": 1},
-        "cpu_baseline": {"value": steps_per_s, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
+        "data": DATA,
+        "config": bench_config(args, k, n),
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
                          "sample": sample},
-        "e2e": {"value": steps_per_s, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+def bench_config(args, world: int, n: int) -> dict:
+    """config of the JSON line -- static, identical on both arms."""
+    return {"workload": workload_name(args.depth, world, args.mode), "n_params": n, "k": world, "wire": "f16",
+            "loss_scale": LOSS_SCALE, "schedule": "slow-start 32k (n=1024, b_local=32), t from %d" % args.t_start,
+            "l2": f"inputs {n * 16 / 1e9:.2f} GB > 126 MB L2 (no flush needed)"}
+
+
+DATA = "synthetic (paper-shaped: ResNet layout, minibatch-32 noise)"
 
 
 # ------------------------------------------------------------------ GPU arm
@@ -356,7 +362,22 @@ def main():
     #    between the step's kernels would serialise their overlap.
     prof, trace, ms_prof = {}, None, None
     if not args.no_profile:
-        if world == 1:
+        if oop:
+            # k_fused1_oop's start (block 0) and end (k_repair1 past its dependency wait)
+            # as %globaltimer stamps inside the step stream: no events between the
+            # kernels, so the per-step durations sum to at most the pass's elapsed time
+            import statistics
+            L.lmsgd_trace_enable(ctx, args.steps)
+            ms_prof, _ = timed(False)
+            tr = L.lmsgd_trace_read(ctx, args.steps)
+            L.lmsgd_trace_enable(ctx, 0)
+            dur = [(t["update_end"] - t["pack_start"]) / 1e3 for t in tr]
+            prof = {"pack": (sum(dur) * 1e-3, len(dur))}
+            trace = {"k_fused1_oop_us": {"mean": sum(dur) / len(dur), "median": statistics.median(dur),
+                                         "min": min(dur), "max": max(dur), "launches": len(dur)},
+                     "source": "in-kernel %globaltimer: k_fused1_oop block 0 start -> k_repair1 start (after "
+                               "its griddepcontrol.wait, i.e. every k_fused1_oop block done)"}
+        elif world == 1:
             ms_prof, prof = timed(True)
         else:
             import statistics
@@ -404,17 +425,20 @@ def main():
                    "note": "one event pair per step (breaks the launch overlap between steps); max over ranks"}
     ms_per_step = ms / args.steps
     global_steps_per_s = 1e3 / ms_per_step
-    value = global_steps_per_s * world
+    value = global_steps_per_s      # synchronous steps/s of the whole job (every replica updated)
 
     # per-kernel roofline (dominant kernel = the update; fused kernel when --mode fused)
     peak, peak_src = measured_peaks()
     phases = {}
     for ph, (pms, cnt) in prof.items():
         if cnt:
+            src = ("in-kernel %globaltimer stamps (k_fused1_oop start -> end), mean over the timed steps" if oop
+                   else "cuda events around each kernel" if world == 1 else
+                   "in-kernel %globaltimer trace, max over ranks; update = the k_xupdate span from its first "
+                   "block's start" if ph == "update" else "in-kernel %globaltimer trace, max over ranks")
             phases[ph] = {"us_per_launch": (max_over_ranks(pms / cnt * 1e3) if world == 1 else pms * 1e3),
-                          "launches": cnt if world == 1 else args.steps,
-                          "source": "cuda events" if world == 1 else ("in-kernel %globaltimer trace, max over ranks; update = the k_xupdate span from its first block's start" if ph == "update" else "in-kernel %globaltimer trace, max over ranks")}
-    if oop:   # phase 0 = k_fused1_oop + k_repair1 (the latter ~2 us: a slightly pessimistic time)
+                          "launches": cnt if world == 1 else args.steps, "source": src}
+    if oop:   # phase 0 = k_fused1_oop alone (in-kernel stamps)
         dom, dom_bytes, kname = "pack", FUSED_BYTES_PER_ELEM, "k_fused1_oop"
     elif flags:
         dom, dom_bytes, kname = "pack", FUSED_BYTES_PER_ELEM, "k_fused1"   # phase 0 = the fused kernel
@@ -426,8 +450,14 @@ def main():
         achieved = dom_bytes * n / (us * 1e-6) / 1e9
         roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak, "unit": "GB/s",
                     "frac": achieved / peak, "traffic": committed_traffic(kname),
-                    "algorithmic_bytes_per_launch": dom_bytes * n, "peak_source": peak_src,
-                    "share_of_step": us * 1e-3 / ms_per_step}
+                    "traffic_source": "profiles/traffic.json (ncu --set full capture, dram__bytes_read.sum + "
+                                      "dram__bytes_write.sum per launch)",
+                    "algorithmic_bytes_per_launch": dom_bytes * n, "bytes_per_elem": dom_bytes, "elems": n,
+                    "us_per_launch": us, "peak_source": peak_src,
+                    # the kernel's share of the step it was measured in (profile pass) and of the
+                    # headline pass
+                    "share_of_step": us * 1e-3 / (ms_prof / args.steps if ms_prof else ms_per_step),
+                    "share_of_headline_step": us * 1e-3 / ms_per_step}
     if "pack" in phases and not flags and not oop and world == 1:
         phases["pack"]["gbs_algorithmic"] = PACK_BYTES_PER_ELEM * n / (phases["pack"]["us_per_launch"] * 1e-6) / 1e9
     if "update" in phases:
@@ -512,19 +542,28 @@ def main():
         bn = {"channels": C, "bytes": 8 * C, "us_per_call": bn_us,
               "nccl_fp32_allreduce_plus_scale_us": max_over_ranks(e0.elapsed_time(e1) / 200 * 1e3)}
 
-    # e2e through the public host-buffer entry point: H2D of this step's gradient from
-    # pinned memory + the whole step + D2H of the step status, every step
+    # e2e through the public host-buffer entry points, every step: H2D of this step's
+    # gradient from pinned memory, the whole step, D2H of theta_t and the status record
+    # (N = 1: lmsgd_step_out_of_place_host, the one-pass guarded step; N > 1:
+    # lmsgd_step_host)
     g_host = grads.cpu().pin_memory()
     st_host = torch.zeros(4, dtype=torch.int64).pin_memory()
-    gp, sh = P(g_host.data_ptr()), P(st_host.data_ptr())
+    th_host = torch.empty(n, dtype=torch.float32).pin_memory()
+    gp, sh, thp = P(g_host.data_ptr()), P(st_host.data_ptr()), P(th_host.data_ptr())
     ke = max(1, min(args.e2e_steps, args.steps))
 
     def step_host(i):
-        s_ = lib.lmsgd_step_host(ctx.ptr, sp, ptrs[0], gp, ptrs[2], ptrs[3], ctypes.byref(coeffs[i % len(coeffs)]), sh)
+        if oop:
+            a_, b_ = sets[i & 1], sets[(i & 1) ^ 1]
+            s_ = lib.lmsgd_step_out_of_place_host(ctx.ptr, sp, a_[0], b_[0], gp, a_[2], b_[2], a_[3], b_[3],
+                                                  ctypes.byref(coeffs[i % len(coeffs)]), thp, sh)
+        else:
+            s_ = lib.lmsgd_step_host(ctx.ptr, sp, ptrs[0], gp, ptrs[2], ptrs[3], ctypes.byref(coeffs[i % len(coeffs)]),
+                                     thp, sh)
         if s_ != 0:
             raise L.LmsgdError(s_, lib.lmsgd_last_error(ctx.ptr).decode())
 
-    for i in range(3):
+    for i in range(4):
         step_host(i)
     torch.cuda.synchronize()
     barrier()
@@ -535,11 +574,13 @@ def main():
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
+    assert L.decode_status(st_host).error == 0
     e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / ke
-    e2e = {"value": world * 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 4 * n,
-           "d2h_bytes_per_step": ctypes.sizeof(L.StepStatus), "ms_per_step": e2e_ms, "steps": ke,
-           # PCIe-bound: the copy of step t+1 overlaps the kernels of step t (lmsgd_step_host)
-           "h2d_gbs": 4 * n / (e2e_ms * 1e-3) / 1e9}
+    e2e = {"value": 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": 4 * n,
+           "d2h_bytes_per_step": 4 * n + ctypes.sizeof(L.StepStatus), "ms_per_step": e2e_ms, "steps": ke,
+           "api": "lmsgd_step_out_of_place_host" if oop else "lmsgd_step_host",
+           # PCIe-bound: the H2D of step t+1 overlaps the kernels and the D2H of step t
+           "pcie_gbs_per_dir": 4 * n / (e2e_ms * 1e-3) / 1e9}
 
     # N = 1: also time the in-place single-pass variant without the skip (LMSGD_FLAG_NO_SKIP,
     # BASELINE.json configs[1] "fused fp16-pack + blended update") and the guarded mode the
@@ -645,7 +686,7 @@ def main():
             vms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
             codev, _ = L.lmsgd_query_status(ctxv)
             assert codev == 0
-            variants[name] = {"ms_per_step": vms, "value": world * 1e3 / vms, "unit": UNIT, "t_from": t_sgd,
+            variants[name] = {"ms_per_step": vms, "value": 1e3 / vms, "unit": UNIT, "t_from": t_sgd,
                               "note": ("alpha_RMSprop = 0: the SGD instantiation of the same step"
                                        if name == "sgd_phase" else
                                        "LMSGD_FLAG_FREEZE_M (in-place lmsgd_step): theta and Delta bit-identical "
@@ -657,24 +698,22 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, ns, calls, el = oracle_rate(1, n, 15.0)
+        rate, ns, calls, el, extrap = oracle_steps(1, n, 15.0, None, args.depth)
         cpu = {"value": rate, "unit": UNIT, "cores": cpu_cores_used(), "kind": "oracle",
-               "sample": f"{calls} oracle steps (pack + exact reduce + fp16 wire + fp64 update, k=1) on a "
-                         f"{ns}-element slice of the {n}-param buffer in {el:.1f} s, extrapolated per element",
+               "sample": f"{calls} whole oracle steps (pack + exact reduce + fp16 wire + fp64 update, k=1) on "
+                         + (f"a {ns}-element slice of the {n}-param buffer, extrapolated per element" if extrap
+                            else f"the whole {n}-param buffer") + f", {el:.1f} s",
                "host_cores_available": len(os.sched_getaffinity(0))}
 
     if rank == 0:
-        inputs_bytes = n * (4 + 12)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic (paper-shaped: ResNet layout, minibatch-32 noise)",
-            "config": {"workload": workload_name(args.depth, world, args.mode),
-                       "n_params": n, "k": world, "wire": "f16", "loss_scale": LOSS_SCALE,
-                       "schedule": "slow-start 32k (n=1024, b_local=32), t from %d" % args.t_start,
-                       "l2": f"inputs {inputs_bytes / 1e9:.2f} GB > 126 MB L2 (no flush needed)",
-                       "global_steps_per_s": global_steps_per_s,
-                       "grad_elems_per_s": global_steps_per_s * world * n},
+            "vs_baseline": None, "dtype": "f32", "data": DATA,
+            "config": bench_config(args, world, n),
+            # every step updates N replicas of the n-element buffer from N gradients
+            "replica_update_steps_per_s": global_steps_per_s * world,
+            "grad_elems_per_s": global_steps_per_s * world * n,
             "roofline": roofline, "phases": phases, "nvlink": nvlink, "bn_stats_allreduce": bn,
             "variants": variants,
             "cpu_baseline": cpu, "e2e": e2e,

@@ -215,17 +215,29 @@ lmsgd_status lmsgd_step_out_of_place(lmsgd_ctx* ctx, void* stream, const float* 
                                      const float* grads, const float* delta_in, float* delta_out,
                                      const float* m_in, float* m_out, const lmsgd_coeffs* coeffs);
 
-/* The same iteration with the gradient in HOST memory (pinned for full speed):
- * copies grads_host -> device, runs lmsgd_step and copies the step status back into
- * *status_host (valid once `stream` has passed this point).  The copy runs on a
- * library-owned copy stream into one of two device staging buffers and may start as
- * soon as the call is made (grads_host must be complete then, and unchanged until
- * `stream` passes this point); `stream` waits for it.  Consecutive calls therefore
- * overlap the host->device copy of step t+1 with the kernels of step t.  The
- * end-to-end entry point bench.py times as "e2e". */
+/* The same iteration with the gradient in HOST memory (pinned for full speed), end
+ * to end: copies grads_host -> device, runs lmsgd_step, then copies the step's
+ * parameters theta_t (n fp32, if params_host != NULL) and status record back into
+ * params_host / *status_host (valid once `stream` has passed this point).  The
+ * host->device copy runs on a library-owned copy stream into one of two device
+ * staging buffers and may start as soon as the call is made (grads_host must be
+ * complete then, and unchanged until `stream` passes this point); `stream` waits
+ * for it, and the device->host copies run on `stream` after the step.  Consecutive
+ * calls therefore overlap the host->device copy of step t+1 with the kernels and the
+ * device->host copy of step t.  Errors as lmsgd_step, INVALID_ARG for NULL
+ * grads_host / status_host. */
 lmsgd_status lmsgd_step_host(lmsgd_ctx* ctx, void* stream, float* params, const float* grads_host,
-                             float* delta, float* m, const lmsgd_coeffs* coeffs,
+                             float* delta, float* m, const lmsgd_coeffs* coeffs, float* params_host,
                              lmsgd_step_status* status_host);
+
+/* lmsgd_step_out_of_place end to end from host memory, as lmsgd_step_host: grads_host
+ * -> device, the one-pass guarded step (world == 1), then params_out (theta_t) ->
+ * params_host (if not NULL) and the status record -> *status_host on `stream`.  The
+ * entry point bench.py times as "e2e" at N = 1.  Errors as lmsgd_step_out_of_place. */
+lmsgd_status lmsgd_step_out_of_place_host(lmsgd_ctx* ctx, void* stream, const float* params_in, float* params_out,
+                                          const float* grads_host, const float* delta_in, float* delta_out,
+                                          const float* m_in, float* m_out, const lmsgd_coeffs* coeffs,
+                                          float* params_host, lmsgd_step_status* status_host);
 
 /* The fp16 all-reduce of the step on its own -- rows a2-a4 (pack, reduce-scatter,
  * all-gather) without the update; PAPER.md:82-87 ("half-precision floats for
@@ -294,7 +306,11 @@ lmsgd_status lmsgd_profile_read(lmsgd_ctx* ctx, double* ms, int64_t* launches);
  * -- pack start, pack end (last block, before its flag release), decision made
  * (all ranks' packs observed), reduce start, reduce end, update start, update go,
  * update end, flag release done, and the arrival of each rank's pack flag (8) --
- * into a ring of max_steps steps (0 disables).  Synchronous. */
+ * into a ring of max_steps steps (0 disables).  lmsgd_step_out_of_place (world 1)
+ * records two of them: word 0 = k_fused1_oop's start (block 0, after its dependency
+ * wait) and word 7 = its end (seen by k_repair1 after its dependency wait), so the
+ * kernel's duration is measured inside the step stream without events between the
+ * kernels.  Synchronous. */
 lmsgd_status lmsgd_trace_enable(lmsgd_ctx* ctx, int64_t max_steps);
 
 /* Copy up to max_steps recorded steps (17 int64 each, oldest first until the ring

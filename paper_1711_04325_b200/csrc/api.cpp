@@ -455,10 +455,15 @@ lmsgd_status lmsgd_step_out_of_place(lmsgd_ctx* c, void* stream, const float* pa
     const int parity = static_cast<int>(epoch & 1u);
     c->last_stream = s;
     c->mode = 1;
+    int64_t* trace = nullptr;   // lmsgd_trace_enable: the kernel's start and end stamps
+    if (c->d_trace) {
+        trace = c->d_trace + (c->trace_steps % c->trace_cap) * lmsgd::TR_WORDS;
+        ++c->trace_steps;
+    }
     CK(c, timed(c, s, 0, [&] {
            return lmsgd::launch_step_oop1(s, c->L, grads, c->n, c->scale, u, params_in, delta_in, m_in, params_out,
                                           delta_out, m_out, status_slot(c, parity), status_slot(c, parity ^ 1),
-                                          c->last);
+                                          c->last, trace);
        }));
     return LMSGD_OK;
 }
@@ -565,13 +570,10 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
     return LMSGD_OK;
 }
 
-lmsgd_status lmsgd_step_host(lmsgd_ctx* c, void* stream, float* params, const float* grads_host,
-                             float* delta, float* m, const lmsgd_coeffs* coeffs,
-                             lmsgd_step_status* status_host) {
-    NvtxRange nvtx_("lmsgd_step_host");
-    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
-    if (!grads_host || !status_host) return fail(c, LMSGD_ERR_INVALID_ARG, "NULL host pointer");
-    DeviceGuard g(c->device);
+namespace {
+// Host->device copy of this step's gradient into one of two device staging buffers on
+// the library's copy stream; `stream` waits for it.  Returns the staging buffer.
+lmsgd_status stage_grads(lmsgd_ctx* c, cudaStream_t s, const float* grads_host, int* b_out) {
     if (!c->copy_stream) {
         CK(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
         for (int b = 0; b < 2; ++b) {
@@ -581,7 +583,6 @@ lmsgd_status lmsgd_step_host(lmsgd_ctx* c, void* stream, float* params, const fl
             CK(c, cudaEventRecord(c->ev_consumed[b], c->copy_stream));
         }
     }
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
     const int b = c->host_buf;
     c->host_buf ^= 1;
     // buffer b is free once the step that last read it has passed on its stream
@@ -589,11 +590,54 @@ lmsgd_status lmsgd_step_host(lmsgd_ctx* c, void* stream, float* params, const fl
     CK(c, cudaMemcpyAsync(c->d_grads[b], grads_host, c->n * sizeof(float), cudaMemcpyHostToDevice, c->copy_stream));
     CK(c, cudaEventRecord(c->ev_copied[b], c->copy_stream));
     CK(c, cudaStreamWaitEvent(s, c->ev_copied[b], 0));
-    const lmsgd_status st = lmsgd_step(c, stream, params, c->d_grads[b], delta, m, coeffs);
-    if (st != LMSGD_OK) return st;
+    *b_out = b;
+    return LMSGD_OK;
+}
+
+// After the step on `s`: staging buffer b is free again; the step's parameters (if
+// params_host) and status record go back to the host on `s`.
+lmsgd_status finish_host_step(lmsgd_ctx* c, cudaStream_t s, int b, const float* params_dev, float* params_host,
+                              lmsgd_step_status* status_host) {
     CK(c, cudaEventRecord(c->ev_consumed[b], s));
+    if (params_host)
+        CK(c, cudaMemcpyAsync(params_host, params_dev, c->n * sizeof(float), cudaMemcpyDeviceToHost, s));
     CK(c, cudaMemcpyAsync(status_host, c->last, sizeof(lmsgd_step_status), cudaMemcpyDeviceToHost, s));
     return LMSGD_OK;
+}
+}  // namespace
+
+lmsgd_status lmsgd_step_host(lmsgd_ctx* c, void* stream, float* params, const float* grads_host,
+                             float* delta, float* m, const lmsgd_coeffs* coeffs, float* params_host,
+                             lmsgd_step_status* status_host) {
+    NvtxRange nvtx_("lmsgd_step_host");
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (!grads_host || !status_host) return fail(c, LMSGD_ERR_INVALID_ARG, "NULL host pointer");
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int b = 0;
+    lmsgd_status st = stage_grads(c, s, grads_host, &b);
+    if (st != LMSGD_OK) return st;
+    st = lmsgd_step(c, stream, params, c->d_grads[b], delta, m, coeffs);
+    if (st != LMSGD_OK) return st;
+    return finish_host_step(c, s, b, params, params_host, status_host);
+}
+
+lmsgd_status lmsgd_step_out_of_place_host(lmsgd_ctx* c, void* stream, const float* params_in, float* params_out,
+                                          const float* grads_host, const float* delta_in, float* delta_out,
+                                          const float* m_in, float* m_out, const lmsgd_coeffs* coeffs,
+                                          float* params_host, lmsgd_step_status* status_host) {
+    NvtxRange nvtx_("lmsgd_step_out_of_place_host");
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (!grads_host || !status_host) return fail(c, LMSGD_ERR_INVALID_ARG, "NULL host pointer");
+    DeviceGuard g(c->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    int b = 0;
+    lmsgd_status st = stage_grads(c, s, grads_host, &b);
+    if (st != LMSGD_OK) return st;
+    st = lmsgd_step_out_of_place(c, stream, params_in, params_out, c->d_grads[b], delta_in, delta_out, m_in, m_out,
+                                 coeffs);
+    if (st != LMSGD_OK) return st;
+    return finish_host_step(c, s, b, params_out, params_host, status_host);
 }
 
 lmsgd_status lmsgd_query_status(lmsgd_ctx* c, lmsgd_step_status* out) {

@@ -401,8 +401,11 @@ __global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1_oop(const float* __restrict_
                                                          UpdConst c, const float* __restrict__ thi,
                                                          const float* __restrict__ di, const float* __restrict__ mi,
                                                          float* __restrict__ tho, float* __restrict__ dout,
-                                                         float* __restrict__ mo, int64_t* st, int64_t* st_reset) {
+                                                         float* __restrict__ mo, int64_t* st, int64_t* st_reset,
+                                                         int64_t* trace) {
     pdl_enter();
+    // lmsgd_trace_enable: block 0's start (it runs in the first wave) ...
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR_PACK_START] = (int64_t)globaltimer();
     reset_status(st_reset);
     int64_t first = kNone;
     unsigned sat = 0;
@@ -421,8 +424,11 @@ __global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1_oop(const float* __restrict_
 // publishes the status record.  On a clean step every block returns at once.
 __global__ void k_repair1(const int64_t* st, const float* __restrict__ thi, const float* __restrict__ di,
                           const float* __restrict__ mi, float* __restrict__ tho, float* __restrict__ dout,
-                          float* __restrict__ mo, int64_t n, int64_t* last) {
+                          float* __restrict__ mo, int64_t n, int64_t* last, int64_t* trace) {
     pdl_enter();
+    // ... and the end of k_fused1_oop: this kernel passes griddepcontrol.wait once every
+    // k_fused1_oop block has completed and its memory is visible
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR_UPD_END] = (int64_t)globaltimer();
     const int64_t first = *reinterpret_cast<volatile const int64_t*>(st + ST_FIRST);
     if (blockIdx.x == 0 && threadIdx.x == 0)
         store_last(last, first, st[ST_PACK_SAT], 0, st[ST_ERROR], first != kNone ? 1 : 0);
@@ -1083,10 +1089,11 @@ cudaError_t launch_xfinal1(cudaStream_t s, const int64_t* st, int64_t* st_next, 
 
 cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                              const UpdConst& c, const float* thi, const float* di, const float* mi, float* tho,
-                             float* dout, float* mo, int64_t* st, int64_t* st_reset, int64_t* last) {
+                             float* dout, float* mo, int64_t* st, int64_t* st_reset, int64_t* last,
+                             int64_t* trace) {
     const int grid = grid_for(L, (n + 7) >> 3);
     cudaError_t e = launch_pdl(c.a_rms != 0.0f ? k_fused1_oop<true> : k_fused1_oop<false>, grid, kThreads, s, g, n,
-                               scale, c, thi, di, mi, tho, dout, mo, st, st_reset);
+                               scale, c, thi, di, mi, tho, dout, mo, st, st_reset, trace);
     if (e != cudaSuccess) return e;
 #ifndef LMSGD_REPAIR_BLOCKS
 // k_repair1 grid: n blocks of 512 threads, or 0 = 4 x SMs.  One block: 105.1 vs 106.4 us
@@ -1096,9 +1103,9 @@ cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, in
 #endif
     if (LMSGD_REPAIR_BLOCKS > 0)
         return launch_pdl_if(true, k_repair1, LMSGD_REPAIR_BLOCKS, 512, s, (const int64_t*)st, thi, di, mi, tho,
-                             dout, mo, n, last);
+                             dout, mo, n, last, trace);
     return launch_pdl_if(true, k_repair1, 4 * L.sm_count, kThreads, s, (const int64_t*)st, thi, di, mi, tho, dout,
-                         mo, n, last);
+                         mo, n, last, trace);
 }
 
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last) {

@@ -86,7 +86,8 @@ cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* la
 // lmsgd_step_out_of_place, k = 1: one pass in -> out, then the repair/status kernel
 cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                              const UpdConst& c, const float* thi, const float* di, const float* mi, float* tho,
-                             float* dout, float* mo, int64_t* st, int64_t* st_reset, int64_t* last);
+                             float* dout, float* mo, int64_t* st, int64_t* st_reset, int64_t* last,
+                             int64_t* trace = nullptr);   // trace: TR_PACK_START / TR_UPD_END stamps
 // lmsgd_exchange at world == 1: status record of the pack, next slot cleared
 cudaError_t launch_xfinal1(cudaStream_t s, const int64_t* st, int64_t* st_next, int64_t* last);
 int stream_blocks_per_sm();

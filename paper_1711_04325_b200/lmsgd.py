@@ -80,7 +80,8 @@ def _load() -> ctypes.CDLL:
         "lmsgd_step": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs)]),
         "lmsgd_exchange": (I32, [P, P, P, P]),
         "lmsgd_step_out_of_place": (I32, [P, P, P, P, P, P, P, P, P, ctypes.POINTER(Coeffs)]),
-        "lmsgd_step_host": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs), P]),
+        "lmsgd_step_host": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs), P, P]),
+        "lmsgd_step_out_of_place_host": (I32, [P, P, P, P, P, P, P, P, P, ctypes.POINTER(Coeffs), P, P]),
         "lmsgd_bn_stats_allreduce": (I32, [P, P, P, P, I64]),
         "lmsgd_set_weight_decay": (I32, [P, ctypes.c_double, I64]),
         "lmsgd_schedule_upload": (I32, [P, ctypes.POINTER(Hyper), ctypes.POINTER(Cluster), I64, I64]),
@@ -294,21 +295,49 @@ def lmsgd_step_graph(ctx: Context, params, grads, delta, m, stream=None):
                                  _ptr(m, torch.float32, "m")), ctx)
 
 
-def lmsgd_step_host(ctx: Context, params, grads_host, delta, m, coeffs: Coeffs, status_host,
-                    stream=None):
-    """grads_host: CPU float32 tensor (pinned for full speed); status_host: a
-    pinned CPU int64 tensor of 4 elements (lmsgd_step_status layout) filled when the
-    stream passes this point."""
+def _host_buf(t, n, name):
     import torch
-    if grads_host.is_cuda or grads_host.dtype != torch.float32 or not grads_host.is_contiguous() \
-            or grads_host.numel() != ctx.n:
-        raise ValueError("grads_host must be a contiguous CPU float32 tensor of n_params elements")
+    if t is None:
+        return None
+    if t.is_cuda or t.dtype != torch.float32 or not t.is_contiguous() or t.numel() != n:
+        raise ValueError(f"{name} must be a contiguous CPU float32 tensor of n_params elements")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _status_buf(status_host):
     if status_host.is_cuda or status_host.numel() * status_host.element_size() < ctypes.sizeof(StepStatus):
         raise ValueError("status_host must be a CPU buffer of >= 32 bytes")
+    return ctypes.c_void_p(status_host.data_ptr())
+
+
+def lmsgd_step_host(ctx: Context, params, grads_host, delta, m, coeffs: Coeffs, status_host,
+                    params_host=None, stream=None):
+    """grads_host: CPU float32 tensor (pinned for full speed); status_host: a pinned
+    CPU int64 tensor of 4 elements (lmsgd_step_status layout); params_host (optional):
+    a pinned CPU float32 tensor that receives theta_t.  Both are filled when the stream
+    passes this point."""
+    import torch
     _check(_lib.lmsgd_step_host(ctx.ptr, _stream(stream), _ptr(params, torch.float32, "params"),
-                                ctypes.c_void_p(grads_host.data_ptr()), _ptr(delta, torch.float32, "delta"),
+                                _host_buf(grads_host, ctx.n, "grads_host"), _ptr(delta, torch.float32, "delta"),
                                 _ptr(m, torch.float32, "m"), ctypes.byref(coeffs),
-                                ctypes.c_void_p(status_host.data_ptr())), ctx)
+                                _host_buf(params_host, ctx.n, "params_host"), _status_buf(status_host)), ctx)
+
+
+def lmsgd_step_out_of_place_host(ctx: Context, params_in, params_out, grads_host, delta_in, delta_out, m_in, m_out,
+                                 coeffs: Coeffs, status_host, params_host=None, stream=None):
+    """lmsgd_step_out_of_place from a host gradient, theta_t (optional) and the status
+    copied back to the host on the stream."""
+    import torch
+    ts = ((params_in, "params_in"), (params_out, "params_out"), (delta_in, "delta_in"), (delta_out, "delta_out"),
+          (m_in, "m_in"), (m_out, "m_out"))
+    for t, nm in ts:
+        if t.numel() != ctx.n:
+            raise ValueError(f"{nm} must have n_params = {ctx.n} elements")
+    p = [_ptr(t, torch.float32, nm) for t, nm in ts]
+    _check(_lib.lmsgd_step_out_of_place_host(ctx.ptr, _stream(stream), p[0], p[1],
+                                             _host_buf(grads_host, ctx.n, "grads_host"), p[2], p[3], p[4], p[5],
+                                             ctypes.byref(coeffs), _host_buf(params_host, ctx.n, "params_host"),
+                                             _status_buf(status_host)), ctx)
 
 
 def decode_status(buf) -> StepStatus:

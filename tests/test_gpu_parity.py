@@ -194,17 +194,24 @@ def test_determinism_and_step_host_matches_step():
     th0, d0, m0 = init_state(n)
     g = synth.grads(1, 4, n)[0]
     outs = []
-    for use_host in (False, False, True):
+    for use_host in (False, False, True, "oop"):
         ctx = L.lmsgd_init(1, 0, 0, n, 1024.0)
         th, d, m = dev(th0), dev(d0), dev(m0)
         c = L.lmsgd_schedule_at(None, K32_C, 4)
         if use_host:
             gh = torch.from_numpy(g).pin_memory()
             stbuf = torch.zeros(4, dtype=torch.int64).pin_memory()
-            L.lmsgd_step_host(ctx, th, gh, d, m, c, stbuf)
+            ph = torch.full((n,), -1.0).pin_memory()
+            if use_host == "oop":
+                out = [torch.empty_like(x) for x in (th, d, m)]
+                L.lmsgd_step_out_of_place_host(ctx, th, out[0], gh, d, out[1], m, out[2], c, stbuf, ph)
+                th, d, m = out
+            else:
+                L.lmsgd_step_host(ctx, th, gh, d, m, c, stbuf, ph)
             torch.cuda.synchronize()
             s = L.decode_status(stbuf)
             assert s.first_nonfinite == -1 and s.skipped == 0
+            assert torch.equal(ph, th.cpu())          # theta_t came back to the host
         else:
             L.lmsgd_step(ctx, th, dev(g), d, m, c)
         outs.append([host(x) for x in (th, d, m)])
