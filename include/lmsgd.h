@@ -317,6 +317,53 @@ lmsgd_status lmsgd_trace_enable(lmsgd_ctx* ctx, int64_t max_steps);
  * wraps) into host `out`; *steps = how many were copied.  Synchronizes the device. */
 lmsgd_status lmsgd_trace_read(lmsgd_ctx* ctx, int64_t* out, int64_t max_steps, int64_t* steps);
 
+/* ---------------------------------------------------------------- emulated groups
+ * The world > 1 path (the exchange of PAPER.md:79-87 and the BN average of
+ * PAPER.md:68-71) with every rank of the world as a context of ONE process on ONE GPU.
+ * Ranks that wait for one another must run at the same time; separate launches (in
+ * one or several streams or processes) on one GPU do not guarantee that.  So a group
+ * call launches each kernel of the path ONCE for all the listed ranks: the same
+ * kernels (their group instantiations) with every rank's blocks interleaved in one
+ * grid -- cooperative where blocks wait on each other -- each block playing its rank
+ * with that rank's arguments, buffers, flags, counters and status slots.  Results
+ * are those of the same world run one process per GPU (tested bit-identical).  Used to
+ * test the world > 1 kernels where there are fewer GPUs than ranks.
+ *
+ * lmsgd_connect_group: ctxs[0 .. world-1] are the world's contexts (lmsgd_init with
+ * the same world, n_params, loss scale and device, ranks 0 .. world-1 in any order);
+ * connects them in-process (peers = each other's exchange buffers, no CUDA IPC).  A
+ * group-connected context accepts only the group calls (the single-rank calls return
+ * LMSGD_ERR_STATE).  Errors: INVALID_ARG (NULL, mismatched contexts, duplicate rank,
+ * not the whole world), STATE (already connected). */
+lmsgd_status lmsgd_connect_group(lmsgd_ctx* const* ctxs, int world);
+
+/* One lmsgd_step of the `count` listed ranks (1 <= count <= world, each rank at most
+ * once; arrays indexed like ctxs): params[i], grads[i], delta[i], m[i] are rank
+ * ctxs[i]'s device fp32 [n_params] buffers, coeffs is shared.  Ranks that are not
+ * listed do not step, so the listed ones time out (LMSGD_ERR_TIMEOUT, as when a peer
+ * process stops).  Enqueued on `stream`; lmsgd_query_status(ctxs[i]) reports rank i.
+ * Errors as lmsgd_step, INVALID_ARG / STATE as lmsgd_connect_group. */
+lmsgd_status lmsgd_step_group(lmsgd_ctx* const* ctxs, int count, void* stream, float* const* params,
+                              const float* const* grads, float* const* delta, float* const* m,
+                              const lmsgd_coeffs* coeffs);
+
+/* lmsgd_exchange of the listed ranks: R_out[i] is rank ctxs[i]'s device uint16
+ * [n_pad] output. */
+lmsgd_status lmsgd_exchange_group(lmsgd_ctx* const* ctxs, int count, void* stream, const float* const* grads,
+                                  uint16_t* const* R_out);
+
+/* lmsgd_step_graph of the listed ranks (each after lmsgd_schedule_upload).  The first
+ * call with a given set of buffers must be made outside stream capture (it uploads the
+ * ranks' arguments, synchronously); later calls with the same buffers may be captured
+ * (LMSGD_ERR_STATE if they would need an upload during capture). */
+lmsgd_status lmsgd_step_graph_group(lmsgd_ctx* const* ctxs, int count, void* stream, float* const* params,
+                                    const float* const* grads, float* const* delta, float* const* m);
+
+/* lmsgd_bn_stats_allreduce of the listed ranks: mean[i], var[i] device fp32 [C] of rank
+ * ctxs[i], averaged in place. */
+lmsgd_status lmsgd_bn_stats_allreduce_group(lmsgd_ctx* const* ctxs, int count, void* stream, float* const* mean,
+                                            float* const* var, int64_t C);
+
 /* ---------------------------------------------------------------- sub-steps
  * Context-free single-GPU kernels, exported for parity tests and for the
  * simulated-k mode (k workers' payloads on one GPU).  `dstatus` is a device

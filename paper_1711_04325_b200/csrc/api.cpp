@@ -32,6 +32,11 @@ struct lmsgd_ctx {
     char* buf = nullptr;           // own exchange buffer (IPC-shared when world > 1)
     lmsgd::Peers peers{};
     bool connected = false;
+    bool group = false;               // lmsgd_connect_group: peers are in-process buffers (no IPC)
+    lmsgd::XStep* d_group = nullptr;  // device XStep[LMSGD_MAX_WORLD] of a group call led by this ctx
+    lmsgd::XStep* d_group_graph = nullptr;   // the same for graph mode (constant across replays)
+    std::vector<lmsgd::XStep> group_graph_cache;
+    lmsgd::BnArgs* d_group_bn = nullptr;
     unsigned int* tickets = nullptr;  // device [4]
     unsigned int* xctr = nullptr;     // device [4 + nchunks] counters of the world > 1 kernels
     // device-resident step state (so a captured step replays as the next step)
@@ -236,6 +241,34 @@ cudaError_t timed(lmsgd_ctx* c, cudaStream_t s, int phase, F&& launch) {
 
 }  // namespace
 
+namespace {
+lmsgd_status group_check(lmsgd_ctx* const* ctxs, int count, bool need_group) {
+    if (!ctxs || count < 1 || count > LMSGD_MAX_WORLD) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "group: bad ctxs/count");
+    uint32_t seen = 0;
+    for (int i = 0; i < count; ++i) {
+        lmsgd_ctx* c = ctxs[i];
+        if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "group: NULL context");
+        if (c->world < 2 || count > c->world) return fail(c, LMSGD_ERR_INVALID_ARG, "group: world must be >= 2 and >= count");
+        if (c->device != ctxs[0]->device || c->world != ctxs[0]->world || c->n != ctxs[0]->n ||
+            c->scale != ctxs[0]->scale)
+            return fail(c, LMSGD_ERR_INVALID_ARG, "group: contexts differ in device, world, n_params or loss scale");
+        if (seen & (1u << c->rank)) return fail(c, LMSGD_ERR_INVALID_ARG, "group: a rank appears twice");
+        seen |= 1u << c->rank;
+        if (need_group && !(c->connected && c->group))
+            return fail(c, LMSGD_ERR_STATE, "group: lmsgd_connect_group has not been called");
+    }
+    return LMSGD_OK;
+}
+
+// Upload the per-rank arguments (pageable -> device, stream-ordered) into *dbuf.
+template <typename T>
+lmsgd_status group_upload(lmsgd_ctx* lead, cudaStream_t s, T** dbuf, const std::vector<T>& v) {
+    if (!*dbuf) CK(lead, cudaMalloc(dbuf, LMSGD_MAX_WORLD * sizeof(T)));
+    CK(lead, cudaMemcpyAsync(*dbuf, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    return LMSGD_OK;
+}
+}  // namespace
+
 extern "C" {
 
 int lmsgd_abi_version(void) { return LMSGD_ABI_VERSION; }
@@ -358,7 +391,10 @@ lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
         DeviceGuard g(c->device);
         cudaDeviceSynchronize();
         for (int p = 0; p < LMSGD_MAX_WORLD; ++p)
-            if (p != c->rank && c->peers.base[p]) cudaIpcCloseMemHandle(c->peers.base[p]);
+            if (!c->group && p != c->rank && c->peers.base[p]) cudaIpcCloseMemHandle(c->peers.base[p]);
+        if (c->d_group) cudaFree(c->d_group);
+        if (c->d_group_graph) cudaFree(c->d_group_graph);
+        if (c->d_group_bn) cudaFree(c->d_group_bn);
         if (c->buf) cudaFree(c->buf);
         if (c->tickets) cudaFree(c->tickets);
         if (c->xctr) cudaFree(c->xctr);
@@ -388,6 +424,7 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     if (!coeffs_ok(coeffs))
         return fail(c, LMSGD_ERR_INVALID_ARG, "coeffs: need eta > 0, 0 <= alpha_sgd <= 1, alpha_rmsprop >= 0");
     if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
+    if (c->group) return fail(c, LMSGD_ERR_STATE, "group-connected context: use the lmsgd_*_group calls");
     if (c->mode == 2) return fail(c, LMSGD_ERR_STATE, "this context already runs lmsgd_step_graph");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -474,6 +511,7 @@ lmsgd_status lmsgd_exchange(lmsgd_ctx* c, void* stream, const float* grads, uint
     if (!aligned16(grads) || !aligned16(R_out))
         return fail(c, LMSGD_ERR_INVALID_ARG, "grads/R_out must be non-NULL and 16-byte aligned");
     if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
+    if (c->group) return fail(c, LMSGD_ERR_STATE, "group-connected context: use the lmsgd_*_group calls");
     if (c->mode == 2) return fail(c, LMSGD_ERR_STATE, "this context runs lmsgd_step_graph");
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -539,6 +577,7 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
     if (!aligned16(params) || !aligned16(grads) || !aligned16(delta) || !aligned16(m))
         return fail(c, LMSGD_ERR_INVALID_ARG, "params/grads/delta/m must be non-NULL and 16-byte aligned");
     if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
+    if (c->group) return fail(c, LMSGD_ERR_STATE, "group-connected context: use the lmsgd_*_group calls");
     if (c->ctab_count == 0) return fail(c, LMSGD_ERR_STATE, "lmsgd_schedule_upload has not been called");
     if (c->mode == 1) return fail(c, LMSGD_ERR_STATE, "this context already runs lmsgd_step / lmsgd_exchange");
     DeviceGuard g(c->device);
@@ -656,13 +695,14 @@ lmsgd_status lmsgd_bn_stats_allreduce(lmsgd_ctx* c, void* stream, float* mean, f
     if (!mean || !var || C < 1 || C > LMSGD_MAX_BN_CHANNELS)
         return fail(c, LMSGD_ERR_INVALID_ARG, "mean/var must be non-NULL, 0 < C <= LMSGD_MAX_BN_CHANNELS");
     if (!c->connected) return fail(c, LMSGD_ERR_STATE, "lmsgd_connect has not been called");
+    if (c->group) return fail(c, LMSGD_ERR_STATE, "group-connected context: use the lmsgd_*_group calls");
     if (c->world == 1) return LMSGD_OK;  // the average of one worker is itself
     DeviceGuard g(c->device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ++c->bn_calls;
     lmsgd::XArgs x = xargs(c, 0, &c->dstate->bnepoch);   // epoch from the device call counter
     if (x.trace) { x.trace = nullptr; --c->trace_steps; }
-    CK(c, lmsgd::launch_bn_allreduce(s, x, mean, var, C));
+    CK(c, lmsgd::launch_bn_allreduce(s, lmsgd::BnArgs{x, mean, var, C}));
     return LMSGD_OK;
 }
 
@@ -722,6 +762,159 @@ lmsgd_status lmsgd_trace_read(lmsgd_ctx* c, int64_t* out, int64_t max_steps, int
     *steps = have < max_steps ? have : max_steps;
     if (*steps > 0)
         CK(c, cudaMemcpy(out, c->d_trace, *steps * lmsgd::TR_WORDS * sizeof(int64_t), cudaMemcpyDeviceToHost));
+    return LMSGD_OK;
+}
+
+// ---------------------------------------------------------------- emulated groups
+// The ranks of a world as contexts of ONE process on ONE GPU, connected in-process and
+// stepped together: each kernel of the world > 1 path is launched once for all of
+// them (the SIM instantiations), so ranks that wait for one another are co-scheduled.
+
+
+lmsgd_status lmsgd_connect_group(lmsgd_ctx* const* ctxs, int world) {
+    lmsgd_status st = group_check(ctxs, world, false);
+    if (st != LMSGD_OK) return st;
+    if (world != ctxs[0]->world) return fail(ctxs[0], LMSGD_ERR_INVALID_ARG, "connect_group: need all world ranks");
+    for (int i = 0; i < world; ++i)
+        if (ctxs[i]->connected) return fail(ctxs[i], LMSGD_ERR_STATE, "connect_group: already connected");
+    for (int i = 0; i < world; ++i) {
+        lmsgd_ctx* c = ctxs[i];
+        for (int j = 0; j < world; ++j) c->peers.base[ctxs[j]->rank] = ctxs[j]->buf;
+        c->group = true;
+        c->connected = true;
+    }
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_step_group(lmsgd_ctx* const* ctxs, int count, void* stream, float* const* params,
+                              const float* const* grads, float* const* delta, float* const* m,
+                              const lmsgd_coeffs* coeffs) {
+    NvtxRange nvtx_("lmsgd_step_group");
+    lmsgd_status st = group_check(ctxs, count, true);
+    if (st != LMSGD_OK) return st;
+    if (!params || !grads || !delta || !m) return fail(ctxs[0], LMSGD_ERR_INVALID_ARG, "group step: NULL array");
+    if (!coeffs_ok(coeffs))
+        return fail(ctxs[0], LMSGD_ERR_INVALID_ARG, "coeffs: need eta > 0, 0 <= alpha_sgd <= 1, alpha_rmsprop >= 0");
+    for (int i = 0; i < count; ++i) {
+        if (!aligned16(params[i]) || !aligned16(grads[i]) || !aligned16(delta[i]) || !aligned16(m[i]))
+            return fail(ctxs[i], LMSGD_ERR_INVALID_ARG, "params/grads/delta/m must be non-NULL and 16-byte aligned");
+        if (ctxs[i]->mode == 2) return fail(ctxs[i], LMSGD_ERR_STATE, "this context runs lmsgd_step_graph_group");
+    }
+    lmsgd_ctx* lead = ctxs[0];
+    DeviceGuard g(lead->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<lmsgd::XStep> v(static_cast<size_t>(count));
+    for (int i = 0; i < count; ++i) {
+        lmsgd_ctx* c = ctxs[i];
+        UpdConst u = make_const(c->hyper, *coeffs, c->world, c->scale, c->wd, c->n_wd);
+        u.freeze_m = (c->flags & LMSGD_FLAG_FREEZE_M) && u.a_rms == 0.0f;
+        const uint32_t epoch = ++c->step;
+        c->last_stream = s;
+        c->mode = 1;
+        v[i] = lmsgd::XStep{xargs(c, epoch, &c->dstate->xepoch), grads[i], c->scale, u, params[i], delta[i], m[i],
+                            c->last, c->xctr, nullptr, 0, nullptr, nullptr};
+    }
+    if ((st = group_upload(lead, s, &lead->d_group, v)) != LMSGD_OK) return st;
+    CK(lead, lmsgd::launch_xstep(s, lead->L, v[0], lead->d_group, count));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_exchange_group(lmsgd_ctx* const* ctxs, int count, void* stream, const float* const* grads,
+                                  uint16_t* const* R_out) {
+    NvtxRange nvtx_("lmsgd_exchange_group");
+    lmsgd_status st = group_check(ctxs, count, true);
+    if (st != LMSGD_OK) return st;
+    if (!grads || !R_out) return fail(ctxs[0], LMSGD_ERR_INVALID_ARG, "group exchange: NULL array");
+    for (int i = 0; i < count; ++i) {
+        if (!aligned16(grads[i]) || !aligned16(R_out[i]))
+            return fail(ctxs[i], LMSGD_ERR_INVALID_ARG, "grads/R_out must be non-NULL and 16-byte aligned");
+        if (ctxs[i]->mode == 2) return fail(ctxs[i], LMSGD_ERR_STATE, "this context runs lmsgd_step_graph_group");
+    }
+    lmsgd_ctx* lead = ctxs[0];
+    DeviceGuard g(lead->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<lmsgd::XStep> v(static_cast<size_t>(count));
+    for (int i = 0; i < count; ++i) {
+        lmsgd_ctx* c = ctxs[i];
+        const uint32_t epoch = ++c->step;
+        c->last_stream = s;
+        c->mode = 1;
+        v[i] = lmsgd::XStep{xargs(c, epoch, &c->dstate->xepoch), grads[i], c->scale, lmsgd::UpdConst{}, nullptr,
+                            nullptr, nullptr, c->last, c->xctr, nullptr, 0, nullptr, R_out[i]};
+    }
+    if ((st = group_upload(lead, s, &lead->d_group, v)) != LMSGD_OK) return st;
+    CK(lead, lmsgd::launch_xstep(s, lead->L, v[0], lead->d_group, count));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_step_graph_group(lmsgd_ctx* const* ctxs, int count, void* stream, float* const* params,
+                                    const float* const* grads, float* const* delta, float* const* m) {
+    NvtxRange nvtx_("lmsgd_step_graph_group");
+    lmsgd_status st = group_check(ctxs, count, true);
+    if (st != LMSGD_OK) return st;
+    if (!params || !grads || !delta || !m) return fail(ctxs[0], LMSGD_ERR_INVALID_ARG, "group step: NULL array");
+    for (int i = 0; i < count; ++i) {
+        lmsgd_ctx* c = ctxs[i];
+        if (!aligned16(params[i]) || !aligned16(grads[i]) || !aligned16(delta[i]) || !aligned16(m[i]))
+            return fail(c, LMSGD_ERR_INVALID_ARG, "params/grads/delta/m must be non-NULL and 16-byte aligned");
+        if (c->ctab_count == 0) return fail(c, LMSGD_ERR_STATE, "lmsgd_schedule_upload has not been called");
+        if (c->mode == 1) return fail(c, LMSGD_ERR_STATE, "this context already runs host-mode group calls");
+    }
+    lmsgd_ctx* lead = ctxs[0];
+    DeviceGuard g(lead->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<lmsgd::XStep> v(static_cast<size_t>(count));
+    for (int i = 0; i < count; ++i) {
+        lmsgd_ctx* c = ctxs[i];
+        UpdConst u{};
+        u.n_wd = c->ctab_n_wd;
+        c->last_stream = s;
+        ++c->step;
+        c->mode = 2;
+        lmsgd::XArgs x = xargs(c, 0, &c->dstate->xepoch);
+        if (x.trace) { x.trace = nullptr; --c->trace_steps; }
+        v[i] = lmsgd::XStep{x, grads[i], c->scale, u, params[i], delta[i], m[i], c->last, c->xctr, c->d_ctab,
+                            c->ctab_count, &c->dstate->cursor, nullptr};
+    }
+    // the arguments do not change between graph-mode calls (everything per-step is read
+    // from the device): upload once, outside any capture; a capture then records launches only
+    const bool same = lead->group_graph_cache.size() == v.size() &&
+                      std::memcmp(lead->group_graph_cache.data(), v.data(), v.size() * sizeof(lmsgd::XStep)) == 0;
+    if (!same) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        CK(lead, cudaStreamIsCapturing(s, &cs));
+        if (cs != cudaStreamCaptureStatusNone)
+            return fail(lead, LMSGD_ERR_STATE, "graph group: call once outside capture with these buffers first");
+        if (!lead->d_group_graph) CK(lead, cudaMalloc(&lead->d_group_graph, LMSGD_MAX_WORLD * sizeof(lmsgd::XStep)));
+        CK(lead, cudaStreamSynchronize(s));
+        CK(lead, cudaMemcpy(lead->d_group_graph, v.data(), v.size() * sizeof(lmsgd::XStep), cudaMemcpyHostToDevice));
+        lead->group_graph_cache = v;
+    }
+    CK(lead, lmsgd::launch_xstep(s, lead->L, v[0], lead->d_group_graph, count));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_bn_stats_allreduce_group(lmsgd_ctx* const* ctxs, int count, void* stream, float* const* mean,
+                                            float* const* var, int64_t C) {
+    NvtxRange nvtx_("lmsgd_bn_stats_allreduce_group");
+    lmsgd_status st = group_check(ctxs, count, true);
+    if (st != LMSGD_OK) return st;
+    if (!mean || !var || C < 1 || C > LMSGD_MAX_BN_CHANNELS)
+        return fail(ctxs[0], LMSGD_ERR_INVALID_ARG, "mean/var must be non-NULL, 0 < C <= LMSGD_MAX_BN_CHANNELS");
+    lmsgd_ctx* lead = ctxs[0];
+    DeviceGuard g(lead->device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    std::vector<lmsgd::BnArgs> v(static_cast<size_t>(count));
+    for (int i = 0; i < count; ++i) {
+        lmsgd_ctx* c = ctxs[i];
+        if (!mean[i] || !var[i]) return fail(c, LMSGD_ERR_INVALID_ARG, "mean/var must be non-NULL");
+        ++c->bn_calls;
+        lmsgd::XArgs x = xargs(c, 0, &c->dstate->bnepoch);
+        if (x.trace) { x.trace = nullptr; --c->trace_steps; }
+        v[i] = lmsgd::BnArgs{x, mean[i], var[i], C};
+    }
+    if ((st = group_upload(lead, s, &lead->d_group_bn, v)) != LMSGD_OK) return st;
+    CK(lead, lmsgd::launch_bn_allreduce(s, v[0], lead->d_group_bn, count));
     return LMSGD_OK;
 }
 

@@ -496,14 +496,41 @@ __device__ __forceinline__ void stamp(const XArgs& x, int which) {
 }
 
 
+// A block's place in its rank's grid.  A real launch is one rank's grid (b = blockIdx.x,
+// g = gridDim.x).  An emulated-group launch (lmsgd_*_group: the ranks of a world
+// emulated on ONE GPU, every rank's blocks in the same launch so that ranks that wait
+// for one another are co-scheduled) interleaves `nsim` ranks' grids: block blockIdx.x
+// plays rank blockIdx.x % nsim as that rank's block blockIdx.x / nsim.
+// Emulated group: the per-rank launch arguments, a device array indexed by rank slot.
+struct Sim {
+    const void* args;   // XStep[nsim] or BnArgs[nsim]
+    int nsim;
+};
+// (read from the special registers each time: nothing held in registers for a real launch)
+template <bool SIM>
+struct Grid {
+    const Sim& s;
+    __device__ __forceinline__ int64_t b() const { return SIM ? (int64_t)(blockIdx.x / s.nsim) : (int64_t)blockIdx.x; }
+    __device__ __forceinline__ int64_t g() const { return SIM ? (int64_t)(gridDim.x / s.nsim) : (int64_t)gridDim.x; }
+};
+// This block's arguments: the kernel parameter itself (real launch) or its rank's entry
+// of the group array, staged once in shared memory.
+template <bool SIM, typename T>
+__device__ __forceinline__ const T& rank_args(const T& param, const Sim& sim, T& smem) {
+    if (!SIM) return param;
+    if (threadIdx.x == 0) smem = static_cast<const T*>(sim.args)[blockIdx.x % sim.nsim];
+    __syncthreads();
+    return smem;
+}
+
 // Grid-wide "done" ticket: returns true in exactly one thread (thread 0 of the last
 // block to finish), after all blocks' writes are fenced at system scope.
-__device__ bool grid_last(const XArgs& x, int which) {
+__device__ bool grid_last(const XArgs& x, int which, int64_t grid) {
     __threadfence_system();
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned t = atomicAdd(x.ticket + which, 1u);
-        if (t == gridDim.x - 1) {
+        if (t == grid - 1) {
             x.ticket[which] = 0;
             __threadfence_system();
             return true;
@@ -626,13 +653,17 @@ __device__ __forceinline__ uint32_t cflag_value(const XArgs& x, const Ep& ep) {
 #define LMSGD_XSTEP_MINB 8   // k_xstep1 capped at 32 registers: 8 blocks/SM (A/B at k = 4: 214.9 vs
                              // 225.6 us per step with no cap, 48 registers, 5 blocks/SM)
 #endif
-__global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
+template <bool SIM>
+__global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
     pdl_enter();   // wait for the previous step / caller work; let k_xupdate queue up
+    __shared__ XStep s_a;
+    const XStep& a = rank_args<SIM>(a_, sim, s_a);
+    const Grid<SIM> G{sim};
     const XArgs& x = a.x;
     const Ep ep = get_ep(x);
     __shared__ int s_ok;
     const bool t0 = threadIdx.x == 0;
-    if (blockIdx.x == 0 && t0) stamp(x, TR_PACK_START);
+    if (G.b() == 0 && t0) stamp(x, TR_PACK_START);
     const int64_t gsh = x.lay.shard >> 3;
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
     int64_t* mine = status_of(x, ep, x.rank);
@@ -645,7 +676,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
         int64_t first = kNone;
         unsigned sat = 0;
         const int64_t units = (int64_t)x.world * ups;
-        for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+        for (int64_t u = G.b(); u < units; u += G.g()) {
             int owner;
             int64_t gi;
             if (!map_unit(x, u, owner, gi)) continue;
@@ -660,7 +691,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     }
     __threadfence_system();
     __syncthreads();
-    if (t0 && atomicAdd(a.ctr + 0, 1u) + 1u == gridDim.x) {
+    if (t0 && atomicAdd(a.ctr + 0, 1u) + 1u == G.g()) {
         a.ctr[0] = 0;
         stamp(x, TR_PACK_END);
         publish(x, ep, FLAG_A);
@@ -670,11 +701,11 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     // ---- 2. all ranks packed; block 0 makes the global skip decision (identical on
     //         every rank) and releases the local flag D.  The reduce does not need it.
     if (threadIdx.x < 32) {
-        const bool ok = warp_wait_all(x, ep, FLAG_A, blockIdx.x == 0);
+        const bool ok = warp_wait_all(x, ep, FLAG_A, G.b() == 0);
         if (t0) s_ok = ok ? 1 : 0;
     }
     __syncthreads();
-    if (blockIdx.x == 0) {
+    if (G.b() == 0) {
         __shared__ int64_t s_st[3 * LMSGD_MAX_WORLD];
         if (threadIdx.x < x.world) {   // every rank's final pack words, read in parallel
             const volatile int64_t* sp = status_of(x, ep, threadIdx.x);
@@ -711,11 +742,11 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     //         block u % grid); a chunk is released when the last block holding one of
     //         its units has finished all its units.
     //         Runs even for a step that will be skipped (its R is then never read).
-    if (blockIdx.x == 0 && t0) stamp(x, TR_RED_GO);
+    if (G.b() == 0 && t0) stamp(x, TR_RED_GO);
     const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
     uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
     unsigned sat = 0;
-    for (int64_t u = blockIdx.x; u < ups; u += gridDim.x) {
+    for (int64_t u = G.b(); u < ups; u += G.g()) {
         const int64_t gi = u * kThreads + threadIdx.x;
         if (gi < gsh) reduce8(recv, x.lay.shard, x.world, gi << 3, R, sat);
     }
@@ -728,7 +759,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
     __syncthreads();
     if (t0) {
         uint32_t fv = 0;
-        for (int64_t u = blockIdx.x; u < ups; u += gridDim.x) {
+        for (int64_t u = G.b(); u < ups; u += G.g()) {
             const int c = (int)(u / x.lay.cu);
             const int64_t rem = ups - (int64_t)c * x.lay.cu;
             const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
@@ -743,17 +774,20 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a) {
             }
         }
     }
-    if (blockIdx.x == 0 && t0) stamp(x, TR_RED_END);
+    if (G.b() == 0 && t0) stamp(x, TR_RED_END);
 
     if (t0) atomicAdd(a.ctr + 1, 1u);   // k_xfinalize waits for every block of this grid
 }
 
-template <bool RMS, bool WD, bool KM>
-__global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
+template <bool RMS, bool WD, bool KM, bool SIM>
+__global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
     // no griddepcontrol.wait: ordering with k_xstep1 is by the chunk flags.
     // kXUnits units per block (LMSGD_XUNITS): with one acquire per unit (chunk flags
     // carrying the decision), 2 units beat 1 in the step; with the older flag-D protocol
     // 1 had been faster (225 vs 215 us at k = 4).
+    __shared__ XStep s_a;
+    const XStep& a = rank_args<SIM>(a_, sim, s_a);
+    const Grid<SIM> G{sim};
     const XArgs& x = a.x;
     const Ep ep = get_ep(x);
     __shared__ UpdConst s_c;
@@ -772,7 +806,7 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
     const int64_t kcu = (int64_t)x.world * x.lay.cu;
     auto unit_of = [&](int v, int& owner, int64_t& u, int& c) {   // chunk-major, owner-interleaved
-        const int64_t i = (int64_t)blockIdx.x * kXUnits + v;
+        const int64_t i = G.b() * kXUnits + v;
         c = (int)(i / kcu);
         const int64_t r = i - (int64_t)c * kcu;
         owner = (int)((r % x.world + x.rank) % x.world);
@@ -788,7 +822,7 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
     // reading its receive slots.  The chunk flag carries the skip decision (spin_cflag).
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0 && w < kXUnits) {
-        if (blockIdx.x == 0 && w == 0) stamp(x, TR_UPD_START);
+        if (G.b() == 0 && w == 0) stamp(x, TR_UPD_START);
         int ow, c;
         int64_t u;
         unit_of(w, ow, u, c);
@@ -808,7 +842,7 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
     int go = 1;
 #pragma unroll
     for (int v = 0; v < kXUnits; ++v) go &= s_ok[v];
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(x, TR_UPD_GO);
+    if (G.b() == 0 && threadIdx.x == 0) stamp(x, TR_UPD_GO);
     if (!go || s_range) return;
     const UpdConst c = s_c;
 #pragma unroll
@@ -834,13 +868,16 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a) {
 // profiles/r1/ab/gather_units_n4.txt): the pull is NVLink-bound (~600 GB/s in).  The
 // exchange moves 2 x 2 N (k-1)/k bytes out of every GPU (push, then R served to the
 // peers), 76.7 MB at k = 4: 118 us at the ~650 GB/s an SM store stream reaches.
-__global__ void __launch_bounds__(kThreads) k_xgather(XStep a) {
+template <bool SIM>
+__global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
+    __shared__ XStep s_a;
+    const XStep& a = rank_args<SIM>(a_, sim, s_a);
     const XArgs& x = a.x;
     const Ep ep = get_ep(x);
     const int64_t gsh = x.lay.shard >> 3;
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
     const int64_t kcu = (int64_t)x.world * x.lay.cu;
-    const int64_t i = blockIdx.x;
+    const int64_t i = Grid<SIM>{sim}.b();
     const int c = (int)(i / kcu);
     const int64_t r = i - (int64_t)c * kcu;
     const int owner = (int)((r % x.world + x.rank) % x.world);
@@ -875,8 +912,11 @@ __global__ void k_xfinal1(const int64_t* st, int64_t* st_next, int64_t* last) {
 
 // The step's public status record; runs after k_xupdate (every owner's reduce has
 // been observed by then, so every rank's sum saturation count is final).
-__global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
+template <bool SIM>
+__global__ void k_xfinalize(XStep a_, Sim sim, unsigned int xstep1_blocks) {
     pdl_enter();
+    __shared__ XStep s_a;
+    const XStep& a = rank_args<SIM>(a_, sim, s_a);
     const XArgs& x = a.x;
     const Ep ep = get_ep(x);
     if (threadIdx.x != 0) return;
@@ -904,18 +944,26 @@ __global__ void k_xfinalize(XStep a, unsigned int xstep1_blocks) {
 // system fence per block, the last block releases flag C, every block acquires C of
 // all ranks, then averages its slice over the ranks' staging buffers in rank order,
 // in fp64, one rounding to fp32 (R16).  Double-buffered by call parity.
-__global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs x, float* __restrict__ mean,
-                                                           float* __restrict__ var, int64_t C) {
+template <bool SIM>
+__global__ void __launch_bounds__(kThreads) k_bn_allreduce(BnArgs a_, Sim sim) {
+    __shared__ BnArgs s_a;
+    const BnArgs& a = rank_args<SIM>(a_, sim, s_a);
+    const Grid<SIM> G{sim};
+    const XArgs& x = a.x;
+    float* __restrict__ mean = a.mean;
+    float* __restrict__ var = a.var;
+    const int64_t C = a.C;
+    const int64_t gt = G.b() * blockDim.x + threadIdx.x, gs = G.g() * blockDim.x;
     const Ep ep = get_ep(x);
     __shared__ int s_ok;
     const int64_t Cp = (C + 3) & ~int64_t(3);   // var staged at a 16-B aligned offset
     const int64_t off = (int64_t)ep.par * 2 * LMSGD_MAX_BN_CHANNELS;
     float* stage = reinterpret_cast<float*>(x.peers.base[x.rank] + x.lay.off_bn) + off;
-    for (int64_t i = gtid(); i < C; i += gstride()) {
+    for (int64_t i = gt; i < C; i += gs) {
         stage[i] = mean[i];
         stage[Cp + i] = var[i];
     }
-    if (grid_last(x, FLAG_C)) {
+    if (grid_last(x, FLAG_C, G.g())) {
         publish(x, ep, FLAG_C);
         *x.dev_epoch = ep.e;   // every block has read the call counter by now
     }
@@ -926,7 +974,7 @@ __global__ void __launch_bounds__(kThreads) k_bn_allreduce(XArgs x, float* __res
     __syncthreads();
     if (!s_ok) return;
     // one float4 of every rank per thread, all peer loads issued before the sums
-    for (int64_t f = gtid(); f < Cp / 2; f += gstride()) {
+    for (int64_t f = gt; f < Cp / 2; f += gs) {
         float4 v[LMSGD_MAX_WORLD];
 #pragma unroll
         for (int p = 0; p < LMSGD_MAX_WORLD; ++p)
@@ -964,7 +1012,8 @@ int grid_for(const Launch&, int64_t work_items) {
 // on the host in graph mode), WD (weight decay on), KM (m kept: not FREEZE_M).
 struct UpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_update<R, W, K>; } };
 struct Fused1K { template <bool R, bool W, bool K> static constexpr auto get() { return k_fused1<R, W, K>; } };
-struct XUpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_xupdate<R, W, K>; } };
+template <bool SIM>
+struct XUpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_xupdate<R, W, K, SIM>; } };
 template <typename K>
 auto pick_variant(const UpdConst& c, bool graph) {
     const bool rms = c.a_rms != 0.0f || graph, wd = c.n_wd > 0, km = rms || !c.freeze_m;
@@ -993,43 +1042,53 @@ cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), int grid, int bloc
 
 
 
-int xstep_blocks_per_sm() {
+int xstep_blocks_per_sm(bool sim) {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_xstep1, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sim ? k_xstep1<true> : k_xstep1<false>, kThreads, 0);
     return b > 0 ? b : 1;
 }
 
-cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a) {
+// One world > 1 step (or exchange) of this rank: k_xstep1 (cooperative + PDL), then
+// k_xupdate or k_xgather (PDL), then k_xfinalize.  Group mode (d_group != NULL): the
+// same kernels' SIM instantiations carry `nsim` emulated ranks' grids in each launch;
+// `a` is then any rank's arguments (sizes, kernel variant), the kernels read their
+// rank's entry of d_group.
+cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const XStep* d_group, int nsim) {
+    const bool sim = d_group != nullptr;
+    if (!sim) nsim = 1;
+    const Sim sm{d_group, nsim};
+    // per-rank k_xstep1 grid: all nsim grids co-resident
+    const int per_rank = sim ? (L.sm_count * xstep_blocks_per_sm(true)) / nsim : L.grid_xstep;
     XStep arg = a;
-    void* params[] = {&arg};
     cudaError_t e;
-    if (L.pdl_mask & 2) {   // cooperative + programmatic dependent launch (hides the launch latency)
+    {
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)L.grid_xstep);
+        cfg.gridDim = dim3((unsigned)(per_rank * nsim));
         cfg.blockDim = dim3(kThreads);
         cfg.stream = s;
         cudaLaunchAttribute attr[2];
-        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].id = cudaLaunchAttributeCooperative;   // all blocks co-resident: they wait on each other
         attr[0].val.cooperative = 1;
         attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
-        cfg.numAttrs = 2;
-        e = cudaLaunchKernelEx(&cfg, k_xstep1, arg);
-    } else {
-        e = cudaLaunchCooperativeKernel((const void*)k_xstep1, dim3((unsigned)L.grid_xstep), dim3(kThreads), params, 0, s);
+        cfg.numAttrs = (L.pdl_mask & 2) ? 2 : 1;   // + programmatic dependent launch (hides the launch latency)
+        e = sim ? cudaLaunchKernelEx(&cfg, k_xstep1<true>, arg, sm) : cudaLaunchKernelEx(&cfg, k_xstep1<false>, arg, sm);
     }
     if (e != cudaSuccess) return e;
     const bool pdl = (L.pdl_mask & 4) == 0;   // bit 4 (diagnostics): launch k_xupdate after k_xstep1 completes
     if (a.rout) {   // lmsgd_exchange: the all-gather into the caller's buffer instead of the update
-        const int grid = (int)((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu);
-        e = launch_pdl_if(pdl, k_xgather, grid, kThreads, s, a);
+        const int grid = (int)((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu) * nsim;
+        e = sim ? launch_pdl_if(pdl, k_xgather<true>, grid, kThreads, s, a, sm)
+                : launch_pdl_if(pdl, k_xgather<false>, grid, kThreads, s, a, sm);
     } else {
-        const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits);
-        e = launch_pdl_if(pdl, pick_variant<XUpdateK>(a.c, a.ctab != nullptr), grid, kThreads, s, a);
+        const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits) * nsim;
+        e = sim ? launch_pdl_if(pdl, pick_variant<XUpdateK<true>>(a.c, a.ctab != nullptr), grid, kThreads, s, a, sm)
+                : launch_pdl_if(pdl, pick_variant<XUpdateK<false>>(a.c, a.ctab != nullptr), grid, kThreads, s, a, sm);
     }
     if (e != cudaSuccess) return e;
-    return launch_pdl_if(true, k_xfinalize, 1, 32, s, a, (unsigned int)L.grid_xstep);
+    return sim ? launch_pdl_if(true, k_xfinalize<true>, nsim, 32, s, a, sm, (unsigned int)per_rank)
+               : launch_pdl_if(true, k_xfinalize<false>, 1, 32, s, a, sm, (unsigned int)per_rank);
 }
 
 
@@ -1115,12 +1174,25 @@ cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* la
 
 
 
-cudaError_t launch_bn_allreduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C) {
-    int grid = (int)(((C + 3) / 4 * 2 + kThreads - 1) / kThreads);   // one float4 per thread
+cudaError_t launch_bn_allreduce(cudaStream_t s, const BnArgs& a, const BnArgs* d_group, int nsim) {
+    const bool sim = d_group != nullptr;
+    if (!sim) nsim = 1;
+    int grid = (int)(((a.C + 3) / 4 * 2 + kThreads - 1) / kThreads);   // one float4 per thread
     grid = grid > 148 ? 148 : (grid < 1 ? 1 : grid);
-    XArgs xa = x;
-    void* params[] = {&xa, &mean, &var, &C};
-    return cudaLaunchCooperativeKernel((const void*)k_bn_allreduce, dim3((unsigned)grid), dim3(kThreads), params, 0, s);
+    if (sim) {   // every emulated rank's grid co-resident
+        int b = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_bn_allreduce<true>, kThreads, 0);
+        int dev = 0, sms = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int cap = (b > 0 ? b : 1) * sms / nsim;
+        grid = grid > cap ? cap : grid;
+    }
+    BnArgs arg = a;
+    Sim sm{d_group, nsim};
+    void* params[] = {&arg, &sm};
+    return cudaLaunchCooperativeKernel(sim ? (const void*)k_bn_allreduce<true> : (const void*)k_bn_allreduce<false>,
+                                       dim3((unsigned)(grid * nsim)), dim3(kThreads), params, 0, s);
 }
 
 }  // namespace lmsgd

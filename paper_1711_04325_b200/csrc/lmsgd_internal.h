@@ -130,9 +130,17 @@ struct XStep {
     uint16_t* rout;          // lmsgd_exchange: the caller's [n_pad] all-reduce output (k_xgather
                              // replaces k_xupdate); NULL for a step
 };
-cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a);
-int xstep_blocks_per_sm();
+// d_group / nsim: emulated-group mode (lmsgd_*_group): device array of the nsim ranks'
+// XStep, every rank's blocks in one launch per kernel; NULL for a real (one-rank) launch
+cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const XStep* d_group = nullptr,
+                         int nsim = 1);
+int xstep_blocks_per_sm(bool sim = false);
 
-cudaError_t launch_bn_allreduce(cudaStream_t s, const XArgs& x, float* mean, float* var, int64_t C);
+struct BnArgs {
+    XArgs x;
+    float *mean, *var;
+    int64_t C;
+};
+cudaError_t launch_bn_allreduce(cudaStream_t s, const BnArgs& a, const BnArgs* d_group = nullptr, int nsim = 1);
 
 }  // namespace lmsgd

@@ -91,6 +91,14 @@ def _load() -> ctypes.CDLL:
         "lmsgd_profile_read": (I32, [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(I64)]),
         "lmsgd_trace_enable": (I32, [P, I64]),
         "lmsgd_trace_read": (I32, [P, ctypes.POINTER(I64), I64, ctypes.POINTER(I64)]),
+        "lmsgd_connect_group": (I32, [ctypes.POINTER(P), I32]),
+        "lmsgd_step_group": (I32, [ctypes.POINTER(P), I32, P, ctypes.POINTER(P), ctypes.POINTER(P),
+                                   ctypes.POINTER(P), ctypes.POINTER(P), ctypes.POINTER(Coeffs)]),
+        "lmsgd_exchange_group": (I32, [ctypes.POINTER(P), I32, P, ctypes.POINTER(P), ctypes.POINTER(P)]),
+        "lmsgd_step_graph_group": (I32, [ctypes.POINTER(P), I32, P, ctypes.POINTER(P), ctypes.POINTER(P),
+                                         ctypes.POINTER(P), ctypes.POINTER(P)]),
+        "lmsgd_bn_stats_allreduce_group": (I32, [ctypes.POINTER(P), I32, P, ctypes.POINTER(P), ctypes.POINTER(P),
+                                                 I64]),
         "lmsgd_status_reset": (I32, [P, P]),
         "lmsgd_pack": (I32, [P, P, I64, I64, F32, P, P]),
         "lmsgd_reduce_local": (I32, [P, P, I32, I64, P, P]),
@@ -396,6 +404,65 @@ def lmsgd_trace_read(ctx: Context, max_steps: int):
     got = ctypes.c_int64()
     _check(_lib.lmsgd_trace_read(ctx.ptr, buf, int(max_steps), ctypes.byref(got)), ctx)
     return [dict(zip(TRACE_FIELDS, buf[TRACE_WORDS * i:TRACE_WORDS * (i + 1)])) for i in range(got.value)]
+
+
+# ------------------------------------------------------------------ emulated groups
+# (include/lmsgd.h "emulated groups"): a world's ranks as contexts of this process on
+# one GPU, each kernel launched once for all of them.
+
+def _ptrs(items, fn):
+    arr = (ctypes.c_void_p * len(items))()
+    for i, x in enumerate(items):
+        arr[i] = fn(x).value if x is not None else None
+    return arr
+
+
+def _ctxs(ctxs):
+    return _ptrs(ctxs, lambda c: c.ptr)
+
+
+def lmsgd_connect_group(ctxs):
+    _check(_lib.lmsgd_connect_group(_ctxs(ctxs), len(ctxs)), ctxs[0])
+
+
+def lmsgd_step_group(ctxs, params, grads, delta, m, coeffs: Coeffs, stream=None):
+    import torch
+    f = lambda nm: (lambda t: _ptr(t, torch.float32, nm))  # noqa: E731
+    for c, ts in zip(ctxs, zip(params, grads, delta, m)):
+        if any(t.numel() != c.n for t in ts):
+            raise ValueError(f"every buffer must have n_params = {c.n} elements")
+    _check(_lib.lmsgd_step_group(_ctxs(ctxs), len(ctxs), _stream(stream), _ptrs(params, f("params")),
+                                 _ptrs(grads, f("grads")), _ptrs(delta, f("delta")), _ptrs(m, f("m")),
+                                 ctypes.byref(coeffs)), ctxs[0])
+
+
+def lmsgd_exchange_group(ctxs, grads, R_out, stream=None):
+    import torch
+    _, n_pad = lmsgd_layout(ctxs[0].world, ctxs[0].n)
+    for c, g, r in zip(ctxs, grads, R_out):
+        if g.numel() != c.n or r.numel() != n_pad or r.element_size() != 2:
+            raise ValueError(f"grads [n_params] fp32, R_out [n_pad = {n_pad}] 2-byte tensors")
+    _check(_lib.lmsgd_exchange_group(_ctxs(ctxs), len(ctxs), _stream(stream),
+                                     _ptrs(grads, lambda t: _ptr(t, torch.float32, "grads")),
+                                     _ptrs(R_out, lambda t: _ptr(t, None, "R_out"))), ctxs[0])
+
+
+def lmsgd_step_graph_group(ctxs, params, grads, delta, m, stream=None):
+    import torch
+    f = lambda nm: (lambda t: _ptr(t, torch.float32, nm))  # noqa: E731
+    _check(_lib.lmsgd_step_graph_group(_ctxs(ctxs), len(ctxs), _stream(stream), _ptrs(params, f("params")),
+                                       _ptrs(grads, f("grads")), _ptrs(delta, f("delta")), _ptrs(m, f("m"))),
+           ctxs[0])
+
+
+def lmsgd_bn_stats_allreduce_group(ctxs, mean, var, stream=None):
+    import torch
+    C = mean[0].numel()
+    if any(t.numel() != C for t in list(mean) + list(var)):
+        raise ValueError("every mean / var must have the same length")
+    f = lambda nm: (lambda t: _ptr(t, torch.float32, nm))  # noqa: E731
+    _check(_lib.lmsgd_bn_stats_allreduce_group(_ctxs(ctxs), len(ctxs), _stream(stream), _ptrs(mean, f("mean")),
+                                               _ptrs(var, f("var")), C), ctxs[0])
 
 
 # ------------------------------------------------------------------ sub-steps

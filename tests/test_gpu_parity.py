@@ -510,7 +510,7 @@ def test_resnet_full_size_sampled(depth, t, flags):
     L.lmsgd_finalize(ctx)
 
 
-@pytest.mark.parametrize("depth,t0", [(50, 1), (50, 489), (152, 1), (152, 3518)])
+@pytest.mark.parametrize("depth,t0", [(50, 1), (50, 489), (152, 1), (152, 3517)])
 def test_resnet_full_size_out_of_place_sampled(depth, t0):
     """The N = 1 headline kernel pair (k_fused1_oop + k_repair1, lmsgd_step_out_of_place)
     at the C2 / C5 sizes, in bench.py's launch configuration, over three steps with the

@@ -8,8 +8,13 @@ Two ways to get world > 1 ranks:
     k_xgather, k_xfinalize, k_bn_allreduce) then runs its full cross-rank protocol --
     flags, epochs, status slots, owner-computes exact reduce, fused all-gather -- with
     the GPU time-slicing between the ranks' contexts (correctness only, no timing).
-So a 1-GPU box covers worlds 2, 4 and 8; a multi-GPU box additionally runs the
-world = every-GPU case natively.
+The oversubscribed runs are OPT-IN (LMSGD_OVERSUB=1): kernels that wait on one another
+are not guaranteed to be co-scheduled when they are separate launches on one GPU, and the
+pool's profiling guide records Xid 109 (context-switch timeout) for 2 and 4 such ranks as
+processes on one B200.  They passed on a 1-GPU box once
+(profiles/r2/pytest_gpu_1gpu_oversub_processes.txt); the default coverage of the world > 1
+kernels with fewer GPUs than ranks is tests/test_group_gpu.py (every rank's blocks in one
+launch).
 """
 import os
 import subprocess
@@ -24,7 +29,13 @@ pytestmark = [pytest.mark.gpu, pytest.mark.multigpu]
 
 
 NGPU = torch.cuda.device_count() if torch.cuda.is_available() else 0
+OVERSUB = os.environ.get("LMSGD_OVERSUB") == "1"
 needs_gpu = pytest.mark.skipif(NGPU < 1, reason="needs a GPU")
+
+
+def oversub(world):
+    return pytest.mark.skipif(world > NGPU and not OVERSUB,
+                              reason="more ranks than GPUs: opt-in (LMSGD_OVERSUB=1); see test_group_gpu.py")
 
 
 def _run(k, port, worker="mgpu_worker.py", extra_env=None, ok=None, timeout=900):
@@ -49,6 +60,7 @@ def test_exchange_three_ranks():
 
 
 @needs_gpu
+@oversub(2)
 def test_exchange_two_ranks_and_timeout():
     # a rank that never steps makes the other time out (status, no hang); oversubscribed
     # on a 1-GPU box
@@ -56,6 +68,7 @@ def test_exchange_two_ranks_and_timeout():
 
 
 @needs_gpu
+@oversub(2)
 @pytest.mark.skipif(NGPU >= 2, reason="NGPU >= 2 runs world 2 natively (test_exchange_on_all_gpus)")
 def test_world2_oversubscribed():
     # the whole mgpu_worker suite at world 2 with both ranks on GPU 0 (gloo bootstrap)
@@ -63,6 +76,7 @@ def test_world2_oversubscribed():
 
 
 @needs_gpu
+@oversub(4)
 @pytest.mark.skipif(NGPU >= 4, reason="NGPU >= 4 runs world 4 with one GPU per rank")
 def test_world4_oversubscribed():
     # the whole mgpu_worker suite at world 4, ranks time-sharing the visible GPUs
@@ -70,6 +84,7 @@ def test_world4_oversubscribed():
 
 
 @needs_gpu
+@oversub(8)
 @pytest.mark.skipif(NGPU >= 8, reason="8 GPUs run world 8 natively")
 def test_world8_oversubscribed():
     # world = 8 code paths (8 flag slots, 8-way exact reduce, shard layout) with several
