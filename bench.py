@@ -51,6 +51,12 @@ def parse():
                         "guarded = in-place lmsgd_step, pack + update with the global non-finite skip; "
                         "fused = in-place single pass without the skip (LMSGD_FLAG_NO_SKIP)")
     p.add_argument("--t-start", type=int, default=1, help="first schedule step timed (1 = RMSprop warm-up)")
+    p.add_argument("--nvls", choices=["off", "rs", "allreduce"], default="off",
+                   help="N>1: exchange mode of the headline step (include/lmsgd.h NVLS): off = peer-memory "
+                        "push + exact fp64 owner reduce (default); rs = NVSwitch reduction (fp32 accumulation) "
+                        "into the owner's R; allreduce = rs + multicast of R back into every rank's wire. "
+                        "Every available mode is timed in the nvlink section either way")
+    p.add_argument("--no-nvls", action="store_true", help="N>1: do not bind the NVLS multicast wire at all (A/B)")
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--full-schedule", action="store_true",
                    help="config C5: time the whole 90-epoch schedule (T = 3,519 steps at 32k from t = 1) with the "
@@ -144,6 +150,100 @@ class ClockSampler:
         s = sorted(self.samples)
         return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz,
                 "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+class NvlinkCounters:
+    """NVLink traffic of one GPU (all links) between two snapshots, from NVML:
+    the field counters NVML_FI_DEV_NVLINK_COUNT_XMIT/RCV_BYTES (202/204, bytes) or
+    NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX (138/139, KiB), scope UINT_MAX (every link)
+    or link by link; else the GPM metrics NVML_GPM_METRIC_NVLINK_TOTAL_TX/RX_PER_SEC
+    (61/60) between two GPM samples times the host time between them.  `kind` says which;
+    None (and `err` says why) where the driver exposes none of them."""
+    SETS = (((202, "tx"), (204, "rx"), 1), ((138, "tx"), (139, "rx"), 1024))
+    LINKS = 18   # NVLink 5: 18 links per B200
+
+    def __init__(self, index: int):
+        self.kind, self.err = None, None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv, self.h = pynvml, pynvml.nvmlDeviceGetHandleByIndex(index)
+        except Exception as e:  # noqa: BLE001
+            self.err = str(e)
+            return
+        errs = []
+        for per_link in (False, True):
+            for tx, rx, unit in self.SETS:
+                self.fields, self.per_link = (tx, rx, unit), per_link
+                try:
+                    self._fields()
+                    self.kind = f"nvml fields {tx[0]}/{rx[0]}" + (" per link" if per_link else "")
+                    return
+                except Exception as e:  # noqa: BLE001
+                    errs.append(("per-link " if per_link else "") + str(e))
+        try:
+            sup = self.nv.nvmlGpmQueryDeviceSupport(self.h)
+            if not sup.isSupportedDevice:
+                raise RuntimeError("GPM not supported on this device")
+            a, b = self.snapshot_gpm(), None
+            time.sleep(0.01)
+            b = self.snapshot_gpm()
+            self._gpm_delta(a, b)
+            self.kind = "nvml gpm metrics 61/60 x host time"
+            return
+        except Exception as e:  # noqa: BLE001
+            errs.append("gpm " + str(e))
+        self.err = "; ".join(errs)
+
+    def _fields(self):
+        tx, rx, unit = self.fields
+        scopes = list(range(self.LINKS)) if self.per_link else [0xFFFFFFFF]
+        req = [(f[0], sc) for f in (tx, rx) for sc in scopes]
+        vals = self.nv.nvmlDeviceGetFieldValues(self.h, req)
+        out, ok = {"tx": 0, "rx": 0}, 0
+        for v, (fid, _) in zip(vals, req):
+            if v.nvmlReturn == 0:
+                ok += 1
+                out["tx" if fid == tx[0] else "rx"] += int(v.value.ullVal) * unit
+        if ok == 0:
+            raise RuntimeError(f"NVML fields {tx[0]}/{rx[0]}: return {vals[0].nvmlReturn}")
+        return out
+
+    def snapshot_gpm(self):
+        smp = self.nv.nvmlGpmSampleAlloc()
+        self.nv.nvmlGpmSampleGet(self.h, smp)
+        return smp, time.perf_counter()
+
+    def _gpm_delta(self, a, b):
+        nv = self.nv
+        mg = nv.c_nvmlGpmMetricsGet_t()
+        mg.version = nv.NVML_GPM_METRICS_GET_VERSION
+        mg.numMetrics = 2
+        mg.sample1, mg.sample2 = a[0], b[0]
+        mg.metrics[0].metricId = nv.NVML_GPM_METRIC_NVLINK_TOTAL_TX_PER_SEC
+        mg.metrics[1].metricId = nv.NVML_GPM_METRIC_NVLINK_TOTAL_RX_PER_SEC
+        nv.nvmlGpmMetricsGet(mg)
+        for i in range(2):
+            if mg.metrics[i].nvmlReturn != 0:
+                raise RuntimeError(f"gpm metric {mg.metrics[i].metricId}: return {mg.metrics[i].nvmlReturn}")
+        dt = b[1] - a[1]
+        # NVML reports these two metrics in MiB/s
+        return {"tx": mg.metrics[0].value * 2 ** 20 * dt, "rx": mg.metrics[1].value * 2 ** 20 * dt}
+
+    def snapshot(self):
+        if self.kind is None:
+            return None
+        return self.snapshot_gpm() if self.kind.startswith("nvml gpm") else self._fields()
+
+    def delta(self, a, b):
+        if a is None or b is None:
+            return None
+        if self.kind.startswith("nvml gpm"):
+            out = self._gpm_delta(a, b)
+        else:
+            out = {k: b[k] - a[k] for k in ("tx", "rx")}
+        out["source"] = self.kind
+        return out
 
 
 # ------------------------------------------------------------------ oracle timing (CPU)
@@ -253,6 +353,15 @@ def main():
     flags = L.LMSGD_FLAG_NO_SKIP if (args.mode == "fused" and world == 1) else 0
     ctx = L.lmsgd_init(world, rank, local, n, LOSS_SCALE, None, flags)
     L.connect_process_group(ctx)
+    NV_MODES = {"off": L.LMSGD_NVLS_OFF, "rs": L.LMSGD_NVLS_RS, "allreduce": L.LMSGD_NVLS_ALLREDUCE}
+    nvls_ok = False
+    if world > 1:
+        sup = torch.tensor([1 if L.lmsgd_nvls_supported(local) else 0], device=devc)
+        dist.all_reduce(sup, op=dist.ReduceOp.MIN)
+        nvls_ok = bool(sup.item()) and not args.no_nvls
+        if nvls_ok:   # bind the multicast wire once; the headline mode is --nvls
+            L.connect_nvls(ctx, NV_MODES[args.nvls])
+    assert args.nvls == "off" or nvls_ok, "--nvls needs multicast support on every GPU"
 
     # inputs, resident in HBM before timing (synthetic, paper-shaped; see synth / DESIGN.md)
     gen = torch.Generator(device=devc)
@@ -491,25 +600,96 @@ def main():
         nvlink["nccl_fp16_allreduce_us"] = nccl_ms * 1e3
         nvlink["nccl_fp16_allreduce_bus_gbs"] = bus_bytes / (nccl_ms * 1e-3) / 1e9
         del buf
-        # our fp16 all-reduce alone (lmsgd_exchange: pack + push + exact reduce + pulled
-        # all-gather into a local buffer), same payload, same convention
+        # our fp16 all-reduce alone (lmsgd_exchange: pack -> reduce -> all-gather into a
+        # local buffer), same payload, same convention, in every exchange mode; the step too.
+        # NVLink payload bytes from the NVML counters around each timed loop.
+        counters = NvlinkCounters(local)
         rout = torch.empty(n_pad, dtype=torch.int16, device=devc)
-        for _ in range(5):
-            L.lmsgd_exchange(ctx, grads, rout)
+        modes = ["off"] + (["rs", "allreduce"] if nvls_ok else [])
+        per_mode = {}
+
+        def timed_loop(fn, iters):
+            for i in range(5):
+                fn(i)
+            torch.cuda.synchronize()
+            barrier()
+            c0 = counters.snapshot()
+            y0.record(stream)
+            for i in range(iters):
+                fn(i)
+            y1.record(stream)
+            torch.cuda.synchronize()
+            c1 = counters.snapshot()
+            code, _ = L.lmsgd_query_status(ctx)
+            assert code == 0, f"status {code}"
+            t_ms = max_over_ranks(y0.elapsed_time(y1) / iters)
+            link = None
+            dl = counters.delta(c0, c1)   # taken after a device sync on both sides: these iters only
+            if dl:
+                link = {"tx": dl["tx"] / iters, "rx": dl["rx"] / iters, "source": dl["source"]}
+            return t_ms, link
+
+        push_alg = 2 * n_pad * (world - 1) / world           # one direction, per GPU, reduce-scatter
+        for md in modes:
+            if nvls_ok:
+                L.lmsgd_nvls_mode(ctx, NV_MODES[md])
+            x_ms, link = timed_loop(lambda i: L.lmsgd_exchange(ctx, grads, rout), 50)
+            s_ms, slink = timed_loop(lambda i: step(args.warmup + i % args.steps), 50)
+            per_mode[md] = {"exchange_us": x_ms * 1e3, "exchange_bus_gbs": bus_bytes / (x_ms * 1e-3) / 1e9,
+                            "exchange_bus_frac_of_900": bus_bytes / (x_ms * 1e-3) / 1e9 / 900.0,
+                            "step_us": s_ms * 1e3,
+                            "nvml_link_bytes_per_exchange": link, "nvml_link_bytes_per_step": slink}
+        if counters.kind is None:
+            nvlink["nvml_counters_error"] = counters.err
+        if nvls_ok:
+            L.lmsgd_nvls_mode(ctx, NV_MODES[args.nvls])
+        nvlink["modes"] = per_mode
+        nvlink["algorithmic_link_bytes_per_gpu"] = {
+            "off": {"tx": 2 * push_alg, "rx": 2 * push_alg,
+                    "note": "push 2 N_pad (k-1)/k out + R served to the peers' all-gather 2 N_pad (k-1)/k"},
+            "rs_allreduce": {"note": "switch reads every rank's wire (2 N_pad out per GPU, of which 2 N_pad/k "
+                                     "may stay local), returns the owner's reduced shard (2 N_pad/k in); "
+                                     "allreduce adds the multicast of R: 2 N_pad/k out, 2 N_pad in"}}
+        hd = per_mode[args.nvls]
+        nvlink["lmsgd_exchange_us"] = hd["exchange_us"]
+        nvlink["lmsgd_exchange_bus_gbs"] = hd["exchange_bus_gbs"]
+        nvlink["lmsgd_exchange_bus_frac_of_900"] = hd["exchange_bus_frac_of_900"]
+        best = min(per_mode, key=lambda k_: per_mode[k_]["exchange_us"])
+        nvlink["fastest_exchange_mode"] = best
+        nvlink["fastest_step_mode"] = min(per_mode, key=lambda k_: per_mode[k_]["step_us"])
+        del rout
+        # X-A2A yardstick (NCCL, not our path): our pack -> NCCL all-to-all of the fp16
+        # shards -> our exact local reduce of the k received slots -> NCCL all-gather of R
+        shard = n_pad // world
+        h16 = torch.empty(n_pad, dtype=torch.int16, device=devc)
+        recv = torch.empty(n_pad, dtype=torch.int16, device=devc)
+        Rsh = torch.empty(shard, dtype=torch.int16, device=devc)
+        outg = torch.empty(n_pad, dtype=torch.int16, device=devc)
+        f16 = lambda t: t.view(torch.float16)   # NCCL has no int16; the collectives only move bits  # noqa: E731
+        dstat = torch.empty(4, dtype=torch.int64, device=devc)
+
+        def a2a(i):
+            L.lmsgd_status_reset(dstat)
+            L.lmsgd_pack(grads, n_pad, LOSS_SCALE, h16, dstat)
+            dist.all_to_all_single(f16(recv), f16(h16))
+            L.lmsgd_reduce_local(recv, world, shard, Rsh, dstat)
+            dist.all_gather_into_tensor(f16(outg), f16(Rsh))
+
+        for i in range(5):
+            a2a(i)
         torch.cuda.synchronize()
         barrier()
         y0.record(stream)
-        for _ in range(50):
-            L.lmsgd_exchange(ctx, grads, rout)
+        for i in range(20):
+            a2a(i)
         y1.record(stream)
         torch.cuda.synchronize()
-        code, _ = L.lmsgd_query_status(ctx)
-        assert code == 0, f"exchange status {code}"
-        x_ms = max_over_ranks(y0.elapsed_time(y1) / 50)
-        nvlink["lmsgd_exchange_us"] = x_ms * 1e3
-        nvlink["lmsgd_exchange_bus_gbs"] = bus_bytes / (x_ms * 1e-3) / 1e9
-        nvlink["lmsgd_exchange_bus_frac_of_900"] = nvlink["lmsgd_exchange_bus_gbs"] / 900.0
-        del rout
+        a_ms = max_over_ranks(y0.elapsed_time(y1) / 20)
+        nvlink["x_a2a_yardstick_us"] = a_ms * 1e3
+        nvlink["x_a2a_yardstick_bus_gbs"] = bus_bytes / (a_ms * 1e-3) / 1e9
+        nvlink["x_a2a_note"] = ("lmsgd_pack + NCCL all_to_all_single (fp16) + lmsgd_reduce_local (exact) + NCCL "
+                                "all_gather_into_tensor: the NCCL route that keeps >= fp32 accumulation")
+        del h16, recv, Rsh, outg
 
     # config C4: BN last-minibatch statistics average over the ranks (53 layers, 26,560
     # channels for ResNet-50), latency-bound; device time per call, max over ranks
@@ -657,6 +837,8 @@ def main():
         for name, vflags in (("sgd_phase", flags), ("sgd_phase_freeze_m", flags | L.LMSGD_FLAG_FREEZE_M)):
             ctxv = L.lmsgd_init(world, rank, local, n, LOSS_SCALE, None, vflags)
             L.connect_process_group(ctxv)
+            if nvls_ok and args.nvls != "off":
+                L.connect_nvls(ctxv, NV_MODES[args.nvls])
             thv, dv_, mv = theta.clone(), delta.clone(), m.clone()
             pv = (P(thv.data_ptr()), P(grads.data_ptr()), P(dv_.data_ptr()), P(mv.data_ptr()))
             vo = oop and name == "sgd_phase"   # the headline's own mode, out of place at N = 1

@@ -31,7 +31,9 @@
  *    its fusion (fp16 wire) buffers, flags, status words and peer mappings.
  *  - Thread safety: one context per rank per host thread.
  *  - Determinism: identical inputs give bit-identical outputs on every rank and
- *    every run (the fp16 sum is exact, the update is elementwise).
+ *    every run (the fp16 sum is exact, the update is elementwise; in the optional NVLS
+ *    modes the switch's fp32-accumulated sum is not exact but still deterministic and
+ *    computed once per element by its owner, so replicas stay bit-identical).
  */
 #ifndef LMSGD_H
 #define LMSGD_H
@@ -170,6 +172,45 @@ lmsgd_status lmsgd_ipc_handle(lmsgd_ctx* ctx, uint8_t* out);
  * must be called by all ranks before the first step. */
 lmsgd_status lmsgd_connect(lmsgd_ctx* ctx, const uint8_t* handles);
 
+/* ---------------------------------------------------------------- NVLS (optional)
+ * The fp16 all-reduce of PAPER.md:82-87 through the NVSwitch's in-switch reduction
+ * (NVLink SHARP, "NVLS") instead of the peer-memory reduce-scatter.  Every rank's
+ * packed wire [n_pad] fp16 lives in memory bound to one multicast object; the owner of
+ * shard r reads the switch's sum of shard r over all ranks with
+ * multimem.ld_reduce.add.acc::f32 (fp32 accumulation inside the switch, one rounding
+ * to fp16 -- reading R8' in DESIGN.md: NOT the exact fp64 sum of the default path, so
+ * R may differ from the oracle's by one fp16 rounding of an inexact fp32 sum; the
+ * tolerance is 1e-3 |ghat| + 2^-24/(k s)), and counts an fp16 infinity in the result
+ * as a sum saturation (saturating it to +-65504, R7).  Flags, the global skip, the
+ * status words and the update are those of the default path.
+ *
+ * Modes (lmsgd_nvls_bind / lmsgd_nvls_mode):
+ *   LMSGD_NVLS_OFF       the default peer-memory path (push + exact fp64 reduce);
+ *   LMSGD_NVLS_RS        pack into the own wire (HBM only), the switch reduces each
+ *                        owner's shard into its R, the update pulls R from the owners;
+ *   LMSGD_NVLS_ALLREDUCE as RS, and the owner multicasts its reduced shard back into
+ *                        every rank's wire in place (multimem.st), so the update (and
+ *                        lmsgd_exchange's copy-out) reads R from local HBM.
+ * Bootstrap (one GPU per rank; collective, in this order, with a barrier where noted):
+ *   rank 0: lmsgd_nvls_create -> LMSGD_NVLS_HANDLE_BYTES host bytes, broadcast them;
+ *   every rank: lmsgd_nvls_connect(handle)   [the multicast object is shared as a POSIX
+ *               file descriptor, passed from rank 0 over an abstract unix socket named in
+ *               the handle]; barrier;
+ *   every rank: lmsgd_nvls_bind(mode); barrier before the first step.
+ * Errors: UNSUPPORTED (world == 1, no multicast support on the device, group-connected
+ * context), STATE (out of order), CUDA (driver call failed; the message names it). */
+#define LMSGD_NVLS_HANDLE_BYTES 64
+#define LMSGD_NVLS_OFF 0
+#define LMSGD_NVLS_RS 1
+#define LMSGD_NVLS_ALLREDUCE 2
+/* *supported = 1 if `device` supports multicast objects (CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED). */
+lmsgd_status lmsgd_nvls_supported(int device, int* supported);
+lmsgd_status lmsgd_nvls_create(lmsgd_ctx* ctx, uint8_t* handle_out);
+lmsgd_status lmsgd_nvls_connect(lmsgd_ctx* ctx, const uint8_t* handle);
+lmsgd_status lmsgd_nvls_bind(lmsgd_ctx* ctx, int mode);
+/* Switch between modes after lmsgd_nvls_bind (every rank the same mode, between steps). */
+lmsgd_status lmsgd_nvls_mode(lmsgd_ctx* ctx, int mode);
+
 /* Synchronizes the device, unmaps peers, frees library buffers.  NULL is a no-op.
  * world > 1: collective -- every rank must have finished its last step (e.g. a
  * barrier after lmsgd_query_status) before any rank finalizes, since peers write
@@ -255,6 +296,20 @@ lmsgd_status lmsgd_step_out_of_place_host(lmsgd_ctx* ctx, void* stream, const fl
  * the packed gradient (k_pack + a one-warp status kernel).  Errors: INVALID_ARG (NULL / misaligned),
  * STATE (before lmsgd_connect, or on a context that runs lmsgd_step_graph). */
 lmsgd_status lmsgd_exchange(lmsgd_ctx* ctx, void* stream, const float* grads, uint16_t* R_out);
+
+/* Bucketed exchange (the exchange of a layer bucket overlapped with
+ * the rest of backward, Fig. 1): one context per bucket of the flat
+ * gradient, lmsgd_exchange per bucket as its gradients complete, then ONE lmsgd_update
+ * (sub-step) over the concatenated R with the buckets' statuses merged:
+ *   merge ctx's last exchange status into the sub-step accumulator dstatus (device
+ *   int64[4], see lmsgd_status_reset): first = min(first, offset + the bucket's first
+ *   non-finite index), saturation counts added, the first non-NONFINITE error kept.
+ *   Stream-ordered (one thread; no host sync).  offset: the bucket's first flat index. */
+lmsgd_status lmsgd_status_accumulate(lmsgd_ctx* ctx, void* stream, int64_t offset, int64_t* dstatus);
+/* Cap the persistent exchange kernel (k_xstep1) of this context at `blocks` blocks
+ * (0 = the default, every SM x its resident blocks), so that an exchange overlapped with
+ * other work (backward) occupies only part of the GPU.  Every rank the same value. */
+lmsgd_status lmsgd_set_exchange_blocks(lmsgd_ctx* ctx, int blocks);
 
 /* ---------------------------------------------------------------- CUDA graphs
  * lmsgd_step bakes its per-step arguments (coefficients, step number) into the

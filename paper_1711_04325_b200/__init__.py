@@ -6,4 +6,4 @@ the library and fails loudly if it has not been built -- there is no CPU path.
 """
 from .lmsgd import *  # noqa: F401,F403
 from .lmsgd import LIB_PATH, EXPORTED, LmsgdError, Context, lib  # noqa: F401
-from .optim import LMSGD  # noqa: F401,E402
+from .optim import LMSGD, BucketedLMSGD  # noqa: F401,E402

@@ -1,7 +1,14 @@
 // C ABI of lmsgd (include/lmsgd.h): argument checking, the per-rank context
 // (exchange buffers, CUDA-IPC peer mappings, status words) and the stream-ordered
 // composition of the sm_100a kernels in kernels.cu.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <poll.h>
+#include <sys/socket.h>
+#include <sys/un.h>
+#include <time.h>
+#include <unistd.h>
 
 #include <cmath>
 #include <cstdint>
@@ -9,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "lmsgd.h"
@@ -55,6 +63,7 @@ struct lmsgd_ctx {
     uint32_t step = 0, bn_calls = 0;
     cudaStream_t last_stream = nullptr;
     lmsgd::Launch L{};
+    int xblocks = 0;                  // lmsgd_set_exchange_blocks (0 = L.grid_xstep)
     int64_t timeout_ns = 10'000'000'000LL;
     std::string err;
     // profiling (lmsgd_profile_enable): event pairs around each kernel launch
@@ -65,6 +74,18 @@ struct lmsgd_ctx {
     // tracing (lmsgd_trace_enable): TR_WORDS stamps per step, ring of trace_cap steps
     int64_t* d_trace = nullptr;
     int64_t trace_cap = 0, trace_steps = 0;
+    // NVLS (lmsgd_nvls_*): multicast object, this rank's physical wire bound to it, and
+    // its unicast and multicast mappings
+    struct Nvls {
+        int stage = 0;                 // 0 none, 1 created/imported + device added, 2 bound + mapped
+        int mode = 0;
+        bool bound = false, uc_mapped = false, mc_mapped = false;
+        CUmemGenericAllocationHandle mc = 0, phys = 0;
+        CUdeviceptr uc_va = 0, mc_va = 0;
+        size_t size = 0;
+        std::thread server;            // rank 0: hands the multicast fd to the other ranks
+        int fd = -1;
+    } nv;
 };
 
 namespace {
@@ -200,6 +221,9 @@ lmsgd::XArgs xargs(lmsgd_ctx* c, uint32_t epoch, uint32_t* dev_epoch) {
     x.ticket = c->tickets;
     x.dev_epoch = dev_epoch;
     x.trace = nullptr;
+    x.nv = c->nv.stage == 2 ? c->nv.mode : 0;
+    x.nv_uc = reinterpret_cast<char*>(c->nv.uc_va);
+    x.nv_mc = reinterpret_cast<char*>(c->nv.mc_va);
     if (c->d_trace) {
         x.trace = c->d_trace + (c->trace_steps % c->trace_cap) * lmsgd::TR_WORDS;
         ++c->trace_steps;
@@ -237,6 +261,190 @@ cudaError_t timed(lmsgd_ctx* c, cudaStream_t s, int phase, F&& launch) {
         c->recs.push_back(r);
     }
     return e;
+}
+
+
+// ---------------------------------------------------------------- NVLS plumbing
+// Driver API entry points (through the runtime: no link-time dependency on libcuda).
+struct Drv {
+    PFN_cuGetErrorString_v6000 errStr = nullptr;
+    PFN_cuDeviceGet_v2000 devGet = nullptr;
+    PFN_cuDeviceGetAttribute_v2000 devAttr = nullptr;
+    PFN_cuMulticastCreate_v12010 mcCreate = nullptr;
+    PFN_cuMulticastAddDevice_v12010 mcAdd = nullptr;
+    PFN_cuMulticastBindMem_v12010 mcBind = nullptr;
+    PFN_cuMulticastUnbind_v12010 mcUnbind = nullptr;
+    PFN_cuMulticastGetGranularity_v12010 mcGran = nullptr;
+    PFN_cuMemCreate_v10020 memCreate = nullptr;
+    PFN_cuMemRelease_v10020 memRelease = nullptr;
+    PFN_cuMemMap_v10020 memMap = nullptr;
+    PFN_cuMemUnmap_v10020 memUnmap = nullptr;
+    PFN_cuMemAddressReserve_v10020 addrReserve = nullptr;
+    PFN_cuMemAddressFree_v10020 addrFree = nullptr;
+    PFN_cuMemSetAccess_v10020 setAccess = nullptr;
+    PFN_cuMemGetAllocationGranularity_v10020 memGran = nullptr;
+    PFN_cuMemExportToShareableHandle_v10020 exportH = nullptr;
+    PFN_cuMemImportFromShareableHandle_v10020 importH = nullptr;
+    bool ok = false;
+};
+
+const Drv& drv() {
+    static Drv d;
+    static bool init = false;
+    if (init) return d;
+    init = true;
+    bool ok = true;
+    auto get = [&](const char* name, auto& fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || !p) ok = false;
+        fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
+    };
+    get("cuGetErrorString", d.errStr);
+    get("cuDeviceGet", d.devGet);
+    get("cuDeviceGetAttribute", d.devAttr);
+    get("cuMulticastCreate", d.mcCreate);
+    get("cuMulticastAddDevice", d.mcAdd);
+    get("cuMulticastBindMem", d.mcBind);
+    get("cuMulticastUnbind", d.mcUnbind);
+    get("cuMulticastGetGranularity", d.mcGran);
+    get("cuMemCreate", d.memCreate);
+    get("cuMemRelease", d.memRelease);
+    get("cuMemMap", d.memMap);
+    get("cuMemUnmap", d.memUnmap);
+    get("cuMemAddressReserve", d.addrReserve);
+    get("cuMemAddressFree", d.addrFree);
+    get("cuMemSetAccess", d.setAccess);
+    get("cuMemGetAllocationGranularity", d.memGran);
+    get("cuMemExportToShareableHandle", d.exportH);
+    get("cuMemImportFromShareableHandle", d.importH);
+    d.ok = ok;
+    return d;
+}
+
+lmsgd_status drv_fail(lmsgd_ctx* c, CUresult r, const char* what) {
+    const char* m = nullptr;
+    if (drv().errStr) drv().errStr(r, &m);
+    return fail(c, LMSGD_ERR_CUDA, std::string(what) + ": " + (m ? m : "driver error " + std::to_string(r)));
+}
+
+#define CKD(ctx, call)                                                  \
+    do {                                                                \
+        CUresult r_ = (call);                                           \
+        if (r_ != CUDA_SUCCESS) return drv_fail((ctx), r_, #call);      \
+    } while (0)
+
+// The NVLS handle (LMSGD_NVLS_HANDLE_BYTES): where to fetch the multicast fd, and the size.
+struct NvHandle {
+    uint32_t magic;        // 'LMNV'
+    uint32_t world;
+    uint64_t size;         // bytes of the multicast object (and of every rank's wire)
+    char name[48];         // abstract unix socket of rank 0's fd server (NUL-terminated)
+};
+static_assert(sizeof(NvHandle) == LMSGD_NVLS_HANDLE_BYTES, "NVLS handle size");
+constexpr uint32_t kNvMagic = 0x564e4d4cu;
+
+socklen_t abstract_addr(const char* name, sockaddr_un* a) {
+    std::memset(a, 0, sizeof *a);
+    a->sun_family = AF_UNIX;
+    const size_t len = std::strlen(name);
+    std::memcpy(a->sun_path + 1, name, len);   // sun_path[0] = 0: the abstract namespace
+    return static_cast<socklen_t>(offsetof(sockaddr_un, sun_path) + 1 + len);
+}
+
+// Rank 0: hand `fd` to `peers` connections (SCM_RIGHTS), then close the listening socket.
+void fd_server(int lfd, int fd, int peers) {
+    for (int i = 0; i < peers; ++i) {
+        pollfd p{lfd, POLLIN, 0};
+        if (poll(&p, 1, 120000) <= 0) break;   // 2 min without a peer: give up
+        const int cfd = accept(lfd, nullptr, nullptr);
+        if (cfd < 0) break;
+        char byte = 'f';
+        iovec io{&byte, 1};
+        alignas(cmsghdr) char ctl[CMSG_SPACE(sizeof(int))] = {};
+        msghdr m{};
+        m.msg_iov = &io;
+        m.msg_iovlen = 1;
+        m.msg_control = ctl;
+        m.msg_controllen = sizeof ctl;
+        cmsghdr* cm = CMSG_FIRSTHDR(&m);
+        cm->cmsg_level = SOL_SOCKET;
+        cm->cmsg_type = SCM_RIGHTS;
+        cm->cmsg_len = CMSG_LEN(sizeof(int));
+        std::memcpy(CMSG_DATA(cm), &fd, sizeof(int));
+        (void)sendmsg(cfd, &m, 0);
+        close(cfd);
+    }
+    close(lfd);
+}
+
+// Other ranks: fetch the fd from rank 0's server (retried while it comes up).
+int fd_fetch(const char* name) {
+    for (int attempt = 0; attempt < 600; ++attempt) {
+        const int s = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+        if (s < 0) return -1;
+        sockaddr_un a;
+        const socklen_t al = abstract_addr(name, &a);
+        if (connect(s, reinterpret_cast<sockaddr*>(&a), al) == 0) {
+            char byte = 0;
+            iovec io{&byte, 1};
+            alignas(cmsghdr) char ctl[CMSG_SPACE(sizeof(int))] = {};
+            msghdr m{};
+            m.msg_iov = &io;
+            m.msg_iovlen = 1;
+            m.msg_control = ctl;
+            m.msg_controllen = sizeof ctl;
+            int fd = -1;
+            if (recvmsg(s, &m, 0) > 0) {
+                cmsghdr* cm = CMSG_FIRSTHDR(&m);
+                if (cm && cm->cmsg_type == SCM_RIGHTS) std::memcpy(&fd, CMSG_DATA(cm), sizeof(int));
+            }
+            close(s);
+            return fd;
+        }
+        close(s);
+        usleep(100000);
+    }
+    return -1;
+}
+
+void nvls_release(lmsgd_ctx* c) {
+    auto& nv = c->nv;
+    if (nv.server.joinable()) nv.server.join();
+    if (nv.fd >= 0) { close(nv.fd); nv.fd = -1; }
+    if (nv.stage == 0 || !drv().ok) return;
+    const Drv& d = drv();
+    if (nv.mc_va) { if (nv.mc_mapped) d.memUnmap(nv.mc_va, nv.size); d.addrFree(nv.mc_va, nv.size); }
+    if (nv.uc_va) { if (nv.uc_mapped) d.memUnmap(nv.uc_va, nv.size); d.addrFree(nv.uc_va, nv.size); }
+    CUdevice dev = 0;
+    if (nv.bound && d.devGet(&dev, c->device) == CUDA_SUCCESS) d.mcUnbind(nv.mc, dev, 0, nv.size);
+    if (nv.phys) d.memRelease(nv.phys);
+    if (nv.mc) d.memRelease(nv.mc);
+    nv = lmsgd_ctx::Nvls{};
+}
+
+lmsgd_status nvls_pre(lmsgd_ctx* c) {
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (c->world < 2) return fail(c, LMSGD_ERR_UNSUPPORTED, "NVLS needs world > 1");
+    if (c->group) return fail(c, LMSGD_ERR_UNSUPPORTED, "NVLS needs one GPU per rank (not an emulated group)");
+    if (!drv().ok) return fail(c, LMSGD_ERR_UNSUPPORTED, "driver has no multicast entry points");
+    return LMSGD_OK;
+}
+
+CUmulticastObjectProp mc_prop(int world, size_t size) {
+    CUmulticastObjectProp p{};
+    p.numDevices = static_cast<unsigned>(world);
+    p.size = size;
+    p.handleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    p.flags = 0;
+    return p;
+}
+// The launch geometry of ctx's world > 1 kernels: k_xstep1's grid capped by
+// lmsgd_set_exchange_blocks.
+lmsgd::Launch xlaunch(const lmsgd_ctx* c) {
+    lmsgd::Launch L = c->L;
+    if (c->xblocks > 0 && c->xblocks < L.grid_xstep) L.grid_xstep = c->xblocks;
+    return L;
 }
 
 }  // namespace
@@ -385,6 +593,148 @@ lmsgd_status lmsgd_connect(lmsgd_ctx* c, const uint8_t* handles) {
     return LMSGD_OK;
 }
 
+lmsgd_status lmsgd_nvls_supported(int device, int* supported) {
+    if (!supported) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "supported is NULL");
+    *supported = 0;
+    if (!drv().ok) return LMSGD_OK;
+    CUdevice dev = 0;
+    int v = 0;
+    CKD(nullptr, drv().devGet(&dev, device));
+    CKD(nullptr, drv().devAttr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
+    *supported = v;
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_nvls_create(lmsgd_ctx* c, uint8_t* handle_out) {
+    lmsgd_status st = nvls_pre(c);
+    if (st != LMSGD_OK) return st;
+    if (!handle_out) return fail(c, LMSGD_ERR_INVALID_ARG, "handle_out is NULL");
+    if (c->rank != 0) return fail(c, LMSGD_ERR_STATE, "lmsgd_nvls_create is rank 0's call");
+    if (c->nv.stage != 0) return fail(c, LMSGD_ERR_STATE, "NVLS already set up");
+    DeviceGuard g(c->device);
+    CK(c, cudaFree(nullptr));   // the device's primary context is current
+    const Drv& d = drv();
+    CUdevice dev = 0;
+    CKD(c, d.devGet(&dev, c->device));
+    int sup = 0;
+    CKD(c, d.devAttr(&sup, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev));
+    if (!sup) return fail(c, LMSGD_ERR_UNSUPPORTED, "device does not support multicast objects");
+    // size: the fp16 wire [n_pad], rounded up to the multicast and allocation granularities
+    CUmulticastObjectProp mp = mc_prop(c->world, 2 * static_cast<size_t>(c->n_pad));
+    size_t gm = 0, ga = 0;
+    CKD(c, d.mcGran(&gm, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+    CUmemAllocationProp ap{};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = dev;
+    CKD(c, d.memGran(&ga, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+    const size_t gran = gm > ga ? gm : ga;
+    mp.size = (mp.size + gran - 1) / gran * gran;
+    CKD(c, d.mcCreate(&c->nv.mc, &mp));
+    c->nv.size = mp.size;
+    c->nv.stage = 1;
+    int fd = -1;
+    CKD(c, d.exportH(&fd, c->nv.mc, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0));
+    c->nv.fd = fd;
+    NvHandle h{};
+    h.magic = kNvMagic;
+    h.world = static_cast<uint32_t>(c->world);
+    h.size = mp.size;
+    timespec ts{};
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    std::snprintf(h.name, sizeof h.name, "lmsgd-nvls-%d-%llx", static_cast<int>(getpid()),
+                  static_cast<unsigned long long>(ts.tv_sec * 1000000000LL + ts.tv_nsec));
+    const int lfd = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+    sockaddr_un a;
+    const socklen_t al = abstract_addr(h.name, &a);
+    if (lfd < 0 || bind(lfd, reinterpret_cast<sockaddr*>(&a), al) != 0 || listen(lfd, c->world) != 0) {
+        if (lfd >= 0) close(lfd);
+        return fail(c, LMSGD_ERR_CUDA, "NVLS: cannot listen on the fd-passing socket");
+    }
+    c->nv.server = std::thread(fd_server, lfd, fd, c->world - 1);
+    std::memcpy(handle_out, &h, sizeof h);
+    // rank 0 joins its own multicast object
+    CKD(c, d.mcAdd(c->nv.mc, dev));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_nvls_connect(lmsgd_ctx* c, const uint8_t* handle) {
+    lmsgd_status st = nvls_pre(c);
+    if (st != LMSGD_OK) return st;
+    if (!handle) return fail(c, LMSGD_ERR_INVALID_ARG, "handle is NULL");
+    NvHandle h{};
+    std::memcpy(&h, handle, sizeof h);
+    if (h.magic != kNvMagic || h.world != static_cast<uint32_t>(c->world) || h.size < 2 * static_cast<uint64_t>(c->n_pad))
+        return fail(c, LMSGD_ERR_INVALID_ARG, "NVLS handle does not match this context");
+    if (c->rank == 0) return c->nv.stage == 1 ? LMSGD_OK : fail(c, LMSGD_ERR_STATE, "rank 0: call lmsgd_nvls_create first");
+    if (c->nv.stage != 0) return fail(c, LMSGD_ERR_STATE, "NVLS already set up");
+    DeviceGuard g(c->device);
+    CK(c, cudaFree(nullptr));
+    const Drv& d = drv();
+    h.name[sizeof h.name - 1] = 0;
+    const int fd = fd_fetch(h.name);
+    if (fd < 0) return fail(c, LMSGD_ERR_CUDA, "NVLS: could not fetch the multicast fd from rank 0");
+    c->nv.fd = fd;
+    CKD(c, d.importH(&c->nv.mc, reinterpret_cast<void*>(static_cast<uintptr_t>(fd)),
+                     CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR));
+    c->nv.size = h.size;
+    c->nv.stage = 1;
+    CUdevice dev = 0;
+    CKD(c, d.devGet(&dev, c->device));
+    CKD(c, d.mcAdd(c->nv.mc, dev));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_nvls_bind(lmsgd_ctx* c, int mode) {
+    lmsgd_status st = nvls_pre(c);
+    if (st != LMSGD_OK) return st;
+    if (mode < LMSGD_NVLS_OFF || mode > LMSGD_NVLS_ALLREDUCE) return fail(c, LMSGD_ERR_INVALID_ARG, "bad NVLS mode");
+    if (c->nv.stage != 1) return fail(c, LMSGD_ERR_STATE, "NVLS: lmsgd_nvls_connect first (and bind once)");
+    DeviceGuard g(c->device);
+    const Drv& d = drv();
+    if (c->nv.server.joinable()) c->nv.server.join();   // every peer connected before the barrier
+    CUdevice dev = 0;
+    CKD(c, d.devGet(&dev, c->device));
+    CUmemAllocationProp ap{};
+    ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    ap.location.id = dev;
+    // "externally shareable as well as imported multicast objects can be bound only to
+    // externally shareable memory" (cuda.h, cuMulticastBindMem)
+    ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR;
+    const size_t size = c->nv.size;
+    CKD(c, d.memCreate(&c->nv.phys, size, &ap, 0));
+    CKD(c, d.mcBind(c->nv.mc, 0, c->nv.phys, 0, size, 0));
+    c->nv.bound = true;
+    size_t gran = 0;
+    CKD(c, d.memGran(&gran, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+    CUmemAccessDesc acc{};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = dev;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    CKD(c, d.addrReserve(&c->nv.uc_va, size, gran, 0, 0));
+    CKD(c, d.memMap(c->nv.uc_va, size, 0, c->nv.phys, 0));
+    c->nv.uc_mapped = true;
+    CKD(c, d.setAccess(c->nv.uc_va, size, &acc, 1));
+    CKD(c, d.addrReserve(&c->nv.mc_va, size, gran, 0, 0));
+    CKD(c, d.memMap(c->nv.mc_va, size, 0, c->nv.mc, 0));
+    c->nv.mc_mapped = true;
+    CKD(c, d.setAccess(c->nv.mc_va, size, &acc, 1));
+    CK(c, cudaMemset(reinterpret_cast<void*>(c->nv.uc_va), 0, size));
+    CK(c, cudaDeviceSynchronize());
+    c->nv.stage = 2;
+    c->nv.mode = mode;
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_nvls_mode(lmsgd_ctx* c, int mode) {
+    if (!c) return fail(nullptr, LMSGD_ERR_INVALID_ARG, "ctx is NULL");
+    if (mode < LMSGD_NVLS_OFF || mode > LMSGD_NVLS_ALLREDUCE) return fail(c, LMSGD_ERR_INVALID_ARG, "bad NVLS mode");
+    if (mode != LMSGD_NVLS_OFF && c->nv.stage != 2) return fail(c, LMSGD_ERR_STATE, "NVLS is not bound");
+    c->nv.mode = mode;
+    return LMSGD_OK;
+}
+
 lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
     if (!c) return LMSGD_OK;
     {
@@ -408,6 +758,7 @@ lmsgd_status lmsgd_finalize(lmsgd_ctx* c) {
         }
         if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
         if (c->d_trace) cudaFree(c->d_trace);
+        nvls_release(c);
         for (auto& r : c->recs) { c->pool.push_back(r.a); c->pool.push_back(r.b); }
         for (auto e : c->pool) cudaEventDestroy(e);
     }
@@ -455,7 +806,7 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     }
     const lmsgd::XArgs x = xargs(c, epoch, &c->dstate->xepoch);
     lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, nullptr, 0, nullptr};
-    CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, c->L, a); }));
+    CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, xlaunch(c), a); }));
     return LMSGD_OK;
 }
 
@@ -529,7 +880,21 @@ lmsgd_status lmsgd_exchange(lmsgd_ctx* c, void* stream, const float* grads, uint
     const lmsgd::XArgs x = xargs(c, epoch, &c->dstate->xepoch);
     lmsgd::XStep a{x, grads, c->scale, lmsgd::UpdConst{}, nullptr, nullptr, nullptr, c->last, c->xctr,
                    nullptr, 0, nullptr, R_out};
-    CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, c->L, a); }));
+    CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, xlaunch(c), a); }));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_status_accumulate(lmsgd_ctx* c, void* stream, int64_t offset, int64_t* dstatus) {
+    if (!c || !dstatus || offset < 0) return fail(c, LMSGD_ERR_INVALID_ARG, "status_accumulate: bad argument");
+    if (c->step == 0) return fail(c, LMSGD_ERR_STATE, "no exchange or step has run on this context");
+    DeviceGuard g(c->device);
+    CK(c, lmsgd::launch_status_accumulate(static_cast<cudaStream_t>(stream), c->last, offset, dstatus));
+    return LMSGD_OK;
+}
+
+lmsgd_status lmsgd_set_exchange_blocks(lmsgd_ctx* c, int blocks) {
+    if (!c || blocks < 0) return fail(c, LMSGD_ERR_INVALID_ARG, "set_exchange_blocks: bad argument");
+    c->xblocks = blocks;
     return LMSGD_OK;
 }
 
@@ -605,7 +970,7 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
     if (x.trace) { x.trace = nullptr; --c->trace_steps; }   // the trace ring slot would be frozen in a graph
     lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, c->d_ctab, c->ctab_count,
                    &c->dstate->cursor};
-    CK(c, lmsgd::launch_xstep(s, c->L, a));
+    CK(c, lmsgd::launch_xstep(s, xlaunch(c), a));
     return LMSGD_OK;
 }
 

@@ -105,6 +105,38 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
     return v;
 }
 
+// NVLS (NVLink SHARP through the NVSwitch; lmsgd_nvls_*): `mc` is a multicast address,
+// i.e. the same offset in every rank's copy of the bound buffer.
+//   ld_reduce: the switch reads the 16 bytes (8 fp16) from every rank's copy and returns
+//              their sum, accumulated in fp32 (.acc::f32; SASS LDGMC.E.HPADD.F16x8) and
+//              rounded once to fp16 -- R = sat16(S) up to the fp32 accumulation (R8').
+//   st:        one store, replicated by the switch into every rank's copy.
+__device__ __forceinline__ uint4 mm_ld_reduce_f16x8(const void* mc) {
+    uint4 r;
+    asm volatile("multimem.ld_reduce.relaxed.sys.global.add.acc::f32.v4.f16x2 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(mc)
+                 : "memory");
+    return r;
+}
+__device__ __forceinline__ void mm_st_16B(void* mc, uint4 v) {
+    asm volatile("multimem.st.relaxed.sys.global.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(mc), "r"(v.x), "r"(v.y),
+                 "r"(v.z), "r"(v.w)
+                 : "memory");
+}
+// R7 on the switch's result: an fp16 infinity is a sum beyond the fp16 range (the inputs
+// are finite, saturated at pack); count it and saturate to +-65504.
+__device__ __forceinline__ uint32_t sat_inf_f16x2(uint32_t w, unsigned& sat) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const uint32_t h = (w >> (16 * i)) & 0xffffu;
+        if ((h & 0x7fffu) == 0x7c00u) {
+            ++sat;
+            w = (w & ~(0xffffu << (16 * i))) | (((h & 0x8000u) | 0x7bffu) << (16 * i));
+        }
+    }
+    return w;
+}
 
 // 8 consecutive fp32 from j0 (j0 % 8 == 0), zero beyond n.  Streaming loads.
 __device__ __forceinline__ void load8_g(const float* __restrict__ g, int64_t j0, int64_t n,
@@ -653,8 +685,14 @@ __device__ __forceinline__ uint32_t cflag_value(const XArgs& x, const Ep& ep) {
 #define LMSGD_XSTEP_MINB 8   // k_xstep1 capped at 32 registers: 8 blocks/SM (A/B at k = 4: 214.9 vs
                              // 225.6 us per step with no cap, 48 registers, 5 blocks/SM)
 #endif
-template <bool SIM>
+// NV (lmsgd_nvls_*, LMSGD_NVLS_*): 0 = peer memory as above; 1 = the pack is written to this
+// rank's own wire (no push) and phase 3 is the switch's reduction (multimem.ld_reduce) of
+// this rank's shard into R; 2 = as 1, and the reduced shard is multicast (multimem.st) back
+// into every rank's wire in place, so every rank then holds the whole all-reduce result
+// locally.
+template <bool SIM, int NV>
 __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
+    static_assert(!(SIM && NV), "NVLS needs one GPU per rank");
     pdl_enter();   // wait for the previous step / caller work; let k_xupdate queue up
     __shared__ XStep s_a;
     const XStep& a = rank_args<SIM>(a_, sim, s_a);
@@ -683,8 +721,9 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
             const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
             float xv[8];
             load8_g(a.g, j0, x.n, xv);
-            uint16_t* dst = reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
-                            (int64_t)x.rank * x.lay.shard + (gi << 3);
+            uint16_t* dst = NV ? reinterpret_cast<uint16_t*>(x.nv_uc) + j0   // own wire, [n_pad] layout
+                               : reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
+                                     (int64_t)x.rank * x.lay.shard + (gi << 3);
             *reinterpret_cast<uint4*>(dst) = pack8(xv, a.scale, j0, first, sat);
         }
         flush_status(first, sat, mine, ST_PACK_SAT);
@@ -746,9 +785,33 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
     const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
     uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
     unsigned sat = 0;
-    for (int64_t u = G.b(); u < ups; u += G.g()) {
-        const int64_t gi = u * kThreads + threadIdx.x;
-        if (gi < gsh) reduce8(recv, x.lay.shard, x.world, gi << 3, R, sat);
+    if (NV) {
+        // this shard's 8-element groups summed by the switch over every rank's wire,
+        // NVU units per trip with all their ld_reduce issued first (more bytes in flight)
+        constexpr int NVU = 2;
+        for (int64_t u0 = G.b(); u0 < ups; u0 += NVU * G.g()) {
+            uint4 v[NVU];
+            int64_t off[NVU];
+#pragma unroll
+            for (int i = 0; i < NVU; ++i) {
+                const int64_t gi = (u0 + i * G.g()) * kThreads + threadIdx.x;
+                off[i] = gi < gsh ? ((int64_t)x.rank * x.lay.shard + (gi << 3)) * 2 : -1;
+                if (off[i] >= 0) v[i] = mm_ld_reduce_f16x8(x.nv_mc + off[i]);
+            }
+#pragma unroll
+            for (int i = 0; i < NVU; ++i) {
+                if (off[i] < 0) continue;
+                v[i].x = sat_inf_f16x2(v[i].x, sat); v[i].y = sat_inf_f16x2(v[i].y, sat);
+                v[i].z = sat_inf_f16x2(v[i].z, sat); v[i].w = sat_inf_f16x2(v[i].w, sat);
+                if (NV == 2) mm_st_16B(x.nv_mc + off[i], v[i]);   // into every rank's wire, in place
+                else *reinterpret_cast<uint4*>(R + (off[i] / 2 - (int64_t)x.rank * x.lay.shard)) = v[i];
+            }
+        }
+    } else {
+        for (int64_t u = G.b(); u < ups; u += G.g()) {
+            const int64_t gi = u * kThreads + threadIdx.x;
+            if (gi < gsh) reduce8(recv, x.lay.shard, x.world, gi << 3, R, sat);
+        }
     }
     flush_status(kNone, sat, mine, ST_SUM_SAT);
     // one system fence per block, then count this block's units into their chunks.  A
@@ -779,7 +842,14 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
     if (t0) atomicAdd(a.ctr + 1, 1u);   // k_xfinalize waits for every block of this grid
 }
 
-template <bool RMS, bool WD, bool KM, bool SIM>
+// R of a unit: pulled from its owner's R (the all-gather fused into the update), or, after an
+// NVLS all-reduce in place (NV == 2, LOCALR), read from this rank's own wire.
+__device__ __forceinline__ const uint16_t* r_src(const XArgs& x, bool localr, int owner, int64_t gi) {
+    return localr ? reinterpret_cast<const uint16_t*>(x.nv_uc) + (int64_t)owner * x.lay.shard + (gi << 3)
+                  : reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
+}
+
+template <bool RMS, bool WD, bool KM, bool SIM, bool LOCALR>
 __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
     // no griddepcontrol.wait: ordering with k_xstep1 is by the chunk flags.
     // kXUnits units per block (LMSGD_XUNITS): with one acquire per unit (chunk flags
@@ -852,7 +922,7 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
         if (gi >= gsh) continue;
         const int64_t j0 = ((int64_t)owner[v] * gsh + gi) << 3;
         if (j0 >= x.n) continue;
-        const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner[v]] + x.lay.off_R) + (gi << 3);
+        const uint16_t* Rp = r_src(x, LOCALR, owner[v], gi);
         update8<RMS, WD, KM>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, c, a.th, a.d, a.m);
     }
 }
@@ -868,7 +938,7 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
 // profiles/r1/ab/gather_units_n4.txt): the pull is NVLink-bound (~600 GB/s in).  The
 // exchange moves 2 x 2 N (k-1)/k bytes out of every GPU (push, then R served to the
 // peers), 76.7 MB at k = 4: 118 us at the ~650 GB/s an SM store stream reaches.
-template <bool SIM>
+template <bool SIM, bool LOCALR>
 __global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
     __shared__ XStep s_a;
     const XStep& a = rank_args<SIM>(a_, sim, s_a);
@@ -896,8 +966,7 @@ __global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
     if (!s_go || u >= ups) return;
     const int64_t gi = u * kThreads + threadIdx.x;
     if (gi >= gsh) return;
-    const uint16_t* Rp = reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
-    const uint4 v = *reinterpret_cast<const uint4*>(Rp);
+    const uint4 v = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner, gi));
     __stcs(reinterpret_cast<uint4*>(a.rout + (((int64_t)owner * gsh + gi) << 3)), v);
 }
 
@@ -908,6 +977,18 @@ __global__ void k_xfinal1(const int64_t* st, int64_t* st_next, int64_t* last) {
     if (threadIdx.x == 0)
         store_last(last, st[ST_FIRST], st[ST_PACK_SAT], 0, st[ST_ERROR], st[ST_FIRST] != kNone ? 1 : 0);
     if (threadIdx.x < ST_WORDS) reset_words(st_next);
+}
+
+// lmsgd_status_accumulate: merge one context's last status record (lmsgd_step_status
+// layout) into a sub-step accumulator {first (kNone = none), pack_sat, sum_sat, error}.
+__global__ void k_status_acc(const int64_t* last, int64_t offset, int64_t* acc) {
+    if (threadIdx.x != 0) return;
+    const int64_t first = last[0];
+    if (first >= 0 && offset + first < acc[ST_FIRST]) acc[ST_FIRST] = offset + first;
+    acc[ST_PACK_SAT] += last[1];
+    acc[ST_SUM_SAT] += last[2];
+    const int32_t err = reinterpret_cast<const int32_t*>(last + 3)[1];
+    if (err != 0 && err != (int32_t)LMSGD_ERR_NONFINITE && acc[ST_ERROR] == 0) acc[ST_ERROR] = err;
 }
 
 // The step's public status record; runs after k_xupdate (every owner's reduce has
@@ -1012,8 +1093,8 @@ int grid_for(const Launch&, int64_t work_items) {
 // on the host in graph mode), WD (weight decay on), KM (m kept: not FREEZE_M).
 struct UpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_update<R, W, K>; } };
 struct Fused1K { template <bool R, bool W, bool K> static constexpr auto get() { return k_fused1<R, W, K>; } };
-template <bool SIM>
-struct XUpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_xupdate<R, W, K, SIM>; } };
+template <bool SIM, bool LOCALR>
+struct XUpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_xupdate<R, W, K, SIM, LOCALR>; } };
 template <typename K>
 auto pick_variant(const UpdConst& c, bool graph) {
     const bool rms = c.a_rms != 0.0f || graph, wd = c.n_wd > 0, km = rms || !c.freeze_m;
@@ -1044,7 +1125,14 @@ cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), int grid, int bloc
 
 int xstep_blocks_per_sm(bool sim) {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sim ? k_xstep1<true> : k_xstep1<false>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sim ? k_xstep1<true, 0> : k_xstep1<false, 0>, kThreads, 0);
+    int b1 = 0, b2 = 0;   // the NVLS instantiations share the grid size: take the smallest
+    if (!sim) {
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_xstep1<false, 1>, kThreads, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_xstep1<false, 2>, kThreads, 0);
+        b = b1 < b ? b1 : b;
+        b = b2 < b ? b2 : b;
+    }
     return b > 0 ? b : 1;
 }
 
@@ -1073,18 +1161,26 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const 
         attr[1].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = (L.pdl_mask & 2) ? 2 : 1;   // + programmatic dependent launch (hides the launch latency)
-        e = sim ? cudaLaunchKernelEx(&cfg, k_xstep1<true>, arg, sm) : cudaLaunchKernelEx(&cfg, k_xstep1<false>, arg, sm);
+        const int nv = sim ? 0 : a.x.nv;
+        e = sim       ? cudaLaunchKernelEx(&cfg, k_xstep1<true, 0>, arg, sm)
+            : nv == 1 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 1>, arg, sm)
+            : nv == 2 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 2>, arg, sm)
+                      : cudaLaunchKernelEx(&cfg, k_xstep1<false, 0>, arg, sm);
     }
     if (e != cudaSuccess) return e;
     const bool pdl = (L.pdl_mask & 4) == 0;   // bit 4 (diagnostics): launch k_xupdate after k_xstep1 completes
+    const bool localr = !sim && a.x.nv == 2;   // NVLS all-reduce in place: R is in the own wire
     if (a.rout) {   // lmsgd_exchange: the all-gather into the caller's buffer instead of the update
         const int grid = (int)((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu) * nsim;
-        e = sim ? launch_pdl_if(pdl, k_xgather<true>, grid, kThreads, s, a, sm)
-                : launch_pdl_if(pdl, k_xgather<false>, grid, kThreads, s, a, sm);
+        e = sim      ? launch_pdl_if(pdl, k_xgather<true, false>, grid, kThreads, s, a, sm)
+            : localr ? launch_pdl_if(pdl, k_xgather<false, true>, grid, kThreads, s, a, sm)
+                     : launch_pdl_if(pdl, k_xgather<false, false>, grid, kThreads, s, a, sm);
     } else {
         const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits) * nsim;
-        e = sim ? launch_pdl_if(pdl, pick_variant<XUpdateK<true>>(a.c, a.ctab != nullptr), grid, kThreads, s, a, sm)
-                : launch_pdl_if(pdl, pick_variant<XUpdateK<false>>(a.c, a.ctab != nullptr), grid, kThreads, s, a, sm);
+        const bool g = a.ctab != nullptr;
+        e = sim      ? launch_pdl_if(pdl, pick_variant<XUpdateK<true, false>>(a.c, g), grid, kThreads, s, a, sm)
+            : localr ? launch_pdl_if(pdl, pick_variant<XUpdateK<false, true>>(a.c, g), grid, kThreads, s, a, sm)
+                     : launch_pdl_if(pdl, pick_variant<XUpdateK<false, false>>(a.c, g), grid, kThreads, s, a, sm);
     }
     if (e != cudaSuccess) return e;
     return sim ? launch_pdl_if(true, k_xfinalize<true>, nsim, 32, s, a, sm, (unsigned int)per_rank)
@@ -1165,6 +1261,11 @@ cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, in
                              dout, mo, n, last, trace);
     return launch_pdl_if(true, k_repair1, 4 * L.sm_count, kThreads, s, (const int64_t*)st, thi, di, mi, tho, dout,
                          mo, n, last, trace);
+}
+
+cudaError_t launch_status_accumulate(cudaStream_t s, const int64_t* last, int64_t offset, int64_t* acc) {
+    k_status_acc<<<1, 32, 0, s>>>(last, offset, acc);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last) {

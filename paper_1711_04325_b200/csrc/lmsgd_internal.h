@@ -90,6 +90,8 @@ cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, in
                              int64_t* trace = nullptr);   // trace: TR_PACK_START / TR_UPD_END stamps
 // lmsgd_exchange at world == 1: status record of the pack, next slot cleared
 cudaError_t launch_xfinal1(cudaStream_t s, const int64_t* st, int64_t* st_next, int64_t* last);
+// lmsgd_status_accumulate: merge a step status record into a sub-step accumulator
+cudaError_t launch_status_accumulate(cudaStream_t s, const int64_t* last, int64_t offset, int64_t* acc);
 int stream_blocks_per_sm();
 
 // ---- world > 1 exchange over peer memory (NVLink / NVSwitch)
@@ -106,6 +108,11 @@ struct XArgs {
     uint32_t* dev_epoch; // device counter of completed steps (world > 1) or BN calls: the kernels
                          // use epoch = *dev_epoch + 1 and the phase's last kernel advances it,
                          // so a step captured in a CUDA graph replays as the next step
+    // NVLS (lmsgd_nvls_*): this rank's packed wire [n_pad] fp16 as a local (unicast) view and
+    // as the multicast view every rank's copy is bound to; nv = LMSGD_NVLS_* mode, 0 = off
+    char* nv_uc;
+    char* nv_mc;
+    int nv;
 };
 
 // Trace stamps of one world > 1 step (ns, this GPU's %globaltimer): pack start,

@@ -27,6 +27,10 @@ LMSGD_IPC_HANDLE_BYTES = 64
 LMSGD_MAX_BN_CHANNELS = 1 << 20
 LMSGD_FLAG_NO_SKIP = 0x1
 LMSGD_FLAG_FREEZE_M = 0x2
+LMSGD_NVLS_HANDLE_BYTES = 64
+LMSGD_NVLS_OFF = 0
+LMSGD_NVLS_RS = 1
+LMSGD_NVLS_ALLREDUCE = 2
 SCHEDULE_SLOW_START = 0
 SCHEDULE_GOYAL = 1
 TRANSITION_ELU, TRANSITION_LINEAR, TRANSITION_SIGMOID, TRANSITION_SUDDEN = 0, 1, 2, 3   # R20
@@ -75,6 +79,13 @@ def _load() -> ctypes.CDLL:
         "lmsgd_init": (I32, [ctypes.POINTER(P), I32, I32, I32, I64, F32, ctypes.POINTER(Hyper), U32]),
         "lmsgd_ipc_handle": (I32, [P, ctypes.c_char_p]),
         "lmsgd_connect": (I32, [P, ctypes.c_char_p]),
+        "lmsgd_nvls_supported": (I32, [I32, ctypes.POINTER(I32)]),
+        "lmsgd_nvls_create": (I32, [P, ctypes.c_char_p]),
+        "lmsgd_nvls_connect": (I32, [P, ctypes.c_char_p]),
+        "lmsgd_nvls_bind": (I32, [P, I32]),
+        "lmsgd_nvls_mode": (I32, [P, I32]),
+        "lmsgd_status_accumulate": (I32, [P, P, I64, P]),
+        "lmsgd_set_exchange_blocks": (I32, [P, I32]),
         "lmsgd_finalize": (I32, [P]),
         "lmsgd_last_error": (ctypes.c_char_p, [P]),
         "lmsgd_step": (I32, [P, P, P, P, P, P, ctypes.POINTER(Coeffs)]),
@@ -241,6 +252,47 @@ def connect_process_group(ctx: Context, group=None):
     dist.barrier(group=group)
 
 
+def lmsgd_nvls_supported(device: int) -> bool:
+    v = ctypes.c_int()
+    _check(_lib.lmsgd_nvls_supported(int(device), ctypes.byref(v)))
+    return bool(v.value)
+
+
+def lmsgd_nvls_create(ctx: Context) -> bytes:
+    buf = ctypes.create_string_buffer(LMSGD_NVLS_HANDLE_BYTES)
+    _check(_lib.lmsgd_nvls_create(ctx.ptr, buf), ctx)
+    return buf.raw
+
+
+def lmsgd_nvls_connect(ctx: Context, handle: bytes):
+    if len(handle) != LMSGD_NVLS_HANDLE_BYTES:
+        raise ValueError("handle must be LMSGD_NVLS_HANDLE_BYTES bytes")
+    _check(_lib.lmsgd_nvls_connect(ctx.ptr, handle), ctx)
+
+
+def lmsgd_nvls_bind(ctx: Context, mode: int):
+    _check(_lib.lmsgd_nvls_bind(ctx.ptr, int(mode)), ctx)
+
+
+def lmsgd_nvls_mode(ctx: Context, mode: int):
+    _check(_lib.lmsgd_nvls_mode(ctx.ptr, int(mode)), ctx)
+
+
+def connect_nvls(ctx: Context, mode: int = None, group=None):
+    """Bootstrap plumbing of the NVLS exchange (include/lmsgd.h "NVLS"): rank 0 creates
+    the multicast object, its handle is broadcast over torch.distributed, every rank
+    joins, a barrier, every rank binds its wire, a barrier.  Call after
+    connect_process_group."""
+    import torch.distributed as dist
+    mode = LMSGD_NVLS_ALLREDUCE if mode is None else mode
+    h = [lmsgd_nvls_create(ctx) if ctx.rank == 0 else None]
+    dist.broadcast_object_list(h, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    lmsgd_nvls_connect(ctx, h[0])
+    dist.barrier(group=group)
+    lmsgd_nvls_bind(ctx, mode)
+    dist.barrier(group=group)
+
+
 def lmsgd_finalize(ctx: Context):
     if ctx.ptr:
         _check(_lib.lmsgd_finalize(ctx.ptr))
@@ -281,6 +333,16 @@ def lmsgd_exchange(ctx: Context, grads, R_out, stream=None):
         raise ValueError(f"R_out must be a 2-byte tensor of n_pad = {n_pad} elements")
     _check(_lib.lmsgd_exchange(ctx.ptr, _stream(stream), _ptr(grads, torch.float32, "grads"),
                                _ptr(R_out, None, "R_out")), ctx)
+
+
+def lmsgd_status_accumulate(ctx: Context, offset: int, dstatus, stream=None):
+    import torch
+    _check(_lib.lmsgd_status_accumulate(ctx.ptr, _stream(stream), int(offset), _ptr(dstatus, torch.int64, "dstatus")),
+           ctx)
+
+
+def lmsgd_set_exchange_blocks(ctx: Context, blocks: int):
+    _check(_lib.lmsgd_set_exchange_blocks(ctx.ptr, int(blocks)), ctx)
 
 
 def lmsgd_set_weight_decay(ctx: Context, lam: float, n_decay: int = -1):

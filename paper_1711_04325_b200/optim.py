@@ -79,15 +79,19 @@ class LMSGD:
                 off += k
         self.cluster = cluster if cluster is not None else L.make_cluster()
         self.hyper = hyper
-        self.ctx = L.lmsgd_init(world, rank, dev.index if dev.index is not None else torch.cuda.current_device(),
-                                self.n, loss_scale, hyper, flags)
-        L.connect_process_group(self.ctx, group)
-        if weight_decay:
-            L.lmsgd_set_weight_decay(self.ctx, weight_decay, self.n_decay)
+        self.world, self.rank, self.group, self.loss_scale = world, rank, group, loss_scale
+        self.device = dev.index if dev.index is not None else torch.cuda.current_device()
+        self._init_exchange(flags, weight_decay)
         self._d = [torch.zeros(self.n, dtype=torch.float32, device=dev) for _ in range(nsets)]
         self._m = [torch.zeros(self.n, dtype=torch.float32, device=dev) for _ in range(nsets)]
         self.t = int(t_start)
         self.steps_total = L.lmsgd_schedule_steps(self.cluster)
+
+    def _init_exchange(self, flags, weight_decay):
+        self.ctx = L.lmsgd_init(self.world, self.rank, self.device, self.n, self.loss_scale, self.hyper, flags)
+        L.connect_process_group(self.ctx, self.group)
+        if weight_decay:
+            L.lmsgd_set_weight_decay(self.ctx, weight_decay, self.n_decay)
 
     # the current buffer set (the one the parameters view)
     @property
@@ -153,3 +157,134 @@ class LMSGD:
 
     def close(self):
         L.lmsgd_finalize(self.ctx)
+
+
+class BucketedLMSGD(LMSGD):
+    """``LMSGD`` with the exchange split into buckets of the flat gradient and overlapped
+    with backward (the communication/iteration overlap of
+    PAPER.md:113-116 Fig. 1).  Plumbing only:
+
+    * the flat buffer is cut, from its end, into buckets of about ``bucket_elems``
+      elements whose boundaries are multiples of 64 k (so every bucket's exchange output
+      is a contiguous slice of one R buffer [n_pad]); one context per bucket;
+    * a post-accumulate-grad hook counts each bucket's parameters; when the last one's
+      gradient is in, the bucket's ``lmsgd_exchange`` (pack -> fp16 all-reduce with exact
+      accumulation) is enqueued on a communication stream behind the backward work so
+      far, and its status is merged into one accumulator (``lmsgd_status_accumulate``);
+      ``exchange_blocks`` caps the exchange kernel's grid so it shares the GPU with
+      backward (``lmsgd_set_exchange_blocks``);
+    * ``step()`` enqueues any bucket not yet exchanged, waits for the communication
+      stream and runs ONE ``lmsgd_update`` over the whole R (unpack, average and the
+      blended update of PAPER.md:154-156, skipped on every rank if any bucket saw a
+      non-finite gradient), then resets the accumulator.
+
+    The arithmetic is that of ``LMSGD``'s step (the same fp16 all-reduce sum per element,
+    the same update kernel body), so the results are bit-identical to it.  No weight
+    decay, no out-of-place mode (the sub-step update has neither)."""
+
+    def __init__(self, params, *, bucket_elems: int = 1 << 22, exchange_blocks: int = 0, overlap: bool = True,
+                 **kw):
+        if kw.get("weight_decay") or kw.get("out_of_place") or kw.get("flags"):
+            raise ValueError("BucketedLMSGD: no weight decay, out-of-place mode or flags")
+        self.bucket_elems, self.exchange_blocks, self.overlap = int(bucket_elems), int(exchange_blocks), overlap
+        super().__init__(params, **kw)
+
+    def _init_exchange(self, flags, weight_decay):
+        dev = self.flat_g.device
+        unit = 64 * self.world
+        bounds, hi = [], self.n
+        while hi > 0:   # from the end of the buffer: the last layers' gradients come first
+            lo = max(0, (hi - self.bucket_elems) // unit * unit)
+            if lo == hi:
+                lo = max(0, hi - unit)
+            bounds.append((lo, hi))
+            hi = lo
+        self.buckets = []
+        top_pad = 0
+        for lo, hi in bounds:
+            ctx = L.lmsgd_init(self.world, self.rank, self.device, hi - lo, self.loss_scale, self.hyper, 0)
+            L.connect_process_group(ctx, self.group)
+            if self.exchange_blocks:
+                L.lmsgd_set_exchange_blocks(ctx, self.exchange_blocks)
+            n_pad = L.lmsgd_layout(self.world, hi - lo)[1]
+            top_pad = max(top_pad, lo + n_pad)
+            self.buckets.append({"lo": lo, "hi": hi, "n_pad": n_pad, "ctx": ctx})
+        self.ctx = self.buckets[0]["ctx"]      # any connected context serves BN (bn_sync)
+        self.R = torch.zeros(top_pad, dtype=torch.int16, device=dev)
+        self.dstatus = torch.empty(4, dtype=torch.int64, device=dev)
+        self.last_status = torch.empty(4, dtype=torch.int64, device=dev)
+        L.lmsgd_status_reset(self.dstatus)
+        self.comm = torch.cuda.Stream(device=dev)
+        self._upd_done = torch.cuda.Event()
+        self._upd_done.record(torch.cuda.current_stream(dev))
+        # parameter i -> the buckets its flat range overlaps; bucket b <- its parameter count
+        self._p2b, off = [], 0
+        npar = [0] * len(self.buckets)
+        for p in self.params:
+            k = p.numel()
+            bs = [b for b, bk in enumerate(self.buckets) if bk["lo"] < off + k and off < bk["hi"]]
+            self._p2b.append(bs)
+            for b in bs:
+                npar[b] += 1
+            off += k
+        self._npar = npar
+        self._pending = list(npar)
+        self._launched = [False] * len(self.buckets)
+        self._hooks = []
+        if self.overlap:
+            for i, p in enumerate(self.params):
+                self._hooks.append(p.register_post_accumulate_grad_hook(lambda _p, i=i: self._grad_ready(i)))
+
+    def _grad_ready(self, i: int):
+        for b in self._p2b[i]:
+            self._pending[b] -= 1
+            if self._pending[b] == 0:
+                self._launch(b, torch.cuda.current_stream(self.flat_g.device))
+
+    def _launch(self, b: int, after: torch.cuda.Stream):
+        if self._launched[b]:
+            return
+        self._launched[b] = True
+        bk = self.buckets[b]
+        ev = torch.cuda.Event()
+        ev.record(after)                       # this bucket's gradients are complete on `after`
+        self.comm.wait_event(ev)
+        self.comm.wait_event(self._upd_done)   # R and the accumulator are free again
+        lo, hi = bk["lo"], bk["hi"]
+        L.lmsgd_exchange(bk["ctx"], self.flat_g[lo:hi], self.R[lo:lo + bk["n_pad"]], self.comm)
+        L.lmsgd_status_accumulate(bk["ctx"], lo, self.dstatus, self.comm)
+
+    def step(self, stream=None) -> L.Coeffs:
+        self._check_views()
+        cur = stream if stream is not None else torch.cuda.current_stream(self.flat_g.device)
+        for b in range(len(self.buckets)):     # buckets whose hooks did not fire (or overlap off)
+            self._launch(b, cur)
+        cur.wait_stream(self.comm)
+        c = self.coeffs()
+        L.lmsgd_update(self.R, self.n, self.world, self.loss_scale, self.hyper, c, self.flat_p, self.delta, self.m,
+                       self.dstatus, cur)
+        self.last_status.copy_(self.dstatus)
+        L.lmsgd_status_reset(self.dstatus, cur)
+        self._upd_done.record(cur)
+        self._pending = list(self._npar)
+        self._launched = [False] * len(self.buckets)
+        self.t += 1
+        return c
+
+    def status(self):
+        """(code, lmsgd_step_status) of the last step, from the merged bucket statuses."""
+        torch.cuda.synchronize(self.flat_g.device)
+        first, psat, ssat, err = (int(v) for v in self.last_status.cpu().tolist())
+        st = L.StepStatus()
+        st.first_nonfinite = -1 if first == (1 << 63) - 1 else first
+        st.pack_saturations, st.sum_saturations = psat, ssat
+        st.skipped = 1 if (st.first_nonfinite >= 0 or err) else 0
+        st.error = err if err else (L.LMSGD_ERR_NONFINITE if st.first_nonfinite >= 0 else 0)
+        return st.error, st
+
+    def close(self):
+        for h in self._hooks:
+            h.remove()
+        torch.cuda.synchronize(self.flat_g.device)
+        for bk in self.buckets:
+            L.lmsgd_finalize(bk["ctx"])

@@ -209,6 +209,36 @@ def main():
     dist.barrier()
     opt.close()
 
+    # ---- row f1: the bucketed exchange overlapped with backward (BucketedLMSGD) gives
+    #      bit-identically LMSGD's state, and the oracle's one-step state, on every rank
+    def deep(seed):
+        torch.manual_seed(seed)
+        return torch.nn.Sequential(torch.nn.Conv2d(3, 16, 3), torch.nn.ReLU(), torch.nn.Conv2d(16, 32, 3),
+                                   torch.nn.ReLU(), torch.nn.Flatten(), torch.nn.Linear(32 * 4 * 4, 10)).to(dev)
+    torch.backends.cudnn.deterministic, torch.backends.cudnn.benchmark = True, False   # identical grads
+    na, nb = deep(3), deep(3)
+    oa = L.LMSGD(na.parameters(), cluster=C1_C, loss_scale=S)
+    ob = L.BucketedLMSGD(nb.parameters(), cluster=C1_C, loss_scale=S, bucket_elems=2048, exchange_blocks=32)
+    assert len(ob.buckets) > 2
+    for t in (1, 2, 3):
+        gen = torch.Generator(device="cpu").manual_seed(500 * t + rank)
+        x, y = torch.randn(16, 3, 8, 8, generator=gen).to(dev), torch.randint(0, 10, (16,), generator=gen).to(dev)
+        for net_, opt_ in ((na, oa), (nb, ob)):
+            opt_.zero_grad()
+            torch.nn.functional.cross_entropy(net_(x), y).backward()
+        allg = all_gather_host(ob.flat_g)
+        prev = H(ob.flat_p), H(ob.delta), H(ob.m)
+        oa.step()
+        ob.step()
+        assert ob.status()[0] == 0 and oa.status()[0] == 0
+        assert torch.equal(oa.flat_p, ob.flat_p) and torch.equal(oa.delta, ob.delta) and torch.equal(oa.m, ob.m), t
+        check_state(H(ob.flat_p), H(ob.delta), H(ob.m), *prev, exchange.exchange(allg, S).ghat,
+                    schedule.coeffs_at(t, schedule.Hyper(), C1))
+        replicas_identical(ob.flat_p, ob.delta, ob.m)
+    dist.barrier()
+    oa.close()
+    ob.close()
+
     # ---- ghat bit-exact (mu1 = 0, (a_SGD, a_RMS) = (1, 0) => Delta = -ghat), with saturation
     n = 200_003
     hyp = L.lmsgd_hyper_default()

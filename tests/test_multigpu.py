@@ -91,3 +91,18 @@ def test_world8_oversubscribed():
     # ranks per GPU (time-sliced; correctness only)
     _run(8, 29536, worker="oversub_worker.py", extra_env={"LMSGD_TIMEOUT_MS": "120000"},
          ok="OVERSUB_OK world=8")
+
+
+def _nvls_supported():
+    if NGPU < 2:
+        return False
+    import paper_1711_04325_b200 as L
+    return L.lmsgd_nvls_supported(0)
+
+
+@pytest.mark.skipif(NGPU < 2, reason="NVLS needs >= 2 GPUs (one per rank, one multicast object)")
+def test_nvls_on_all_gpus():
+    # the NVSwitch-reduction exchange (LMSGD_NVLS_RS / _ALLREDUCE): tests/nvls_worker.py
+    if not _nvls_supported():
+        pytest.skip("no multicast support on this box")
+    _run(NGPU, 29539, worker="nvls_worker.py", ok=f"NVLS_OK world={NGPU}")

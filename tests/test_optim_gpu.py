@@ -183,3 +183,69 @@ def test_lmsgd_default_in_place_with_captured_forward(monkeypatch):
 def test_lmsgd_out_of_place_rejects_flags():
     with pytest.raises(ValueError):
         L.LMSGD(_net().parameters(), out_of_place=True, flags=L.LMSGD_FLAG_FREEZE_M)
+
+
+def _deep_net(seed=0):
+    torch.manual_seed(seed)
+    return torch.nn.Sequential(torch.nn.Conv2d(3, 16, 3), torch.nn.BatchNorm2d(16), torch.nn.ReLU(),
+                               torch.nn.Conv2d(16, 32, 3), torch.nn.BatchNorm2d(32), torch.nn.ReLU(),
+                               torch.nn.Conv2d(32, 32, 3), torch.nn.ReLU(), torch.nn.Flatten(),
+                               torch.nn.Linear(32 * 2 * 2, 64), torch.nn.ReLU(), torch.nn.Linear(64, 10)).to(DEV)
+
+
+@pytest.mark.parametrize("overlap,bucket", [(True, 1000), (True, 64), (False, 5000), (True, 1 << 22)])
+def test_bucketed_lmsgd_matches_lmsgd_and_oracle(monkeypatch, overlap, bucket):
+    """Row f1: the bucketed exchange (one lmsgd_exchange per bucket from a post-accumulate
+    hook, on a side stream, then one lmsgd_update) gives bit-identically the state of the
+    unbucketed LMSGD step, and the oracle's one-step state; a non-finite gradient in one
+    bucket skips the whole step (first index global)."""
+    monkeypatch.setattr(torch.backends.cudnn, "deterministic", True)
+    monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
+    s = 1024.0
+    net_a, net_b = _deep_net(), _deep_net()
+    opt_a = L.LMSGD(net_a.parameters(), cluster=L.make_cluster(2, 32, 64), loss_scale=s)
+    opt_b = L.BucketedLMSGD(net_b.parameters(), cluster=L.make_cluster(2, 32, 64), loss_scale=s,
+                            bucket_elems=bucket, exchange_blocks=16, overlap=overlap)
+    bks = sorted((bk["lo"], bk["hi"]) for bk in opt_b.buckets)   # the buckets tile [0, n) at 64 k boundaries
+    assert bks[0][0] == 0 and bks[-1][1] == opt_b.n and all(a[1] == b[0] for a, b in zip(bks, bks[1:]))
+    assert all(lo % 64 == 0 for lo, _ in bks) and (len(bks) > 1) == (bucket < opt_b.n)
+    for t in range(1, 5):
+        x, y = torch.randn(16, 3, 8, 8, generator=torch.Generator().manual_seed(t)).to(DEV), \
+            torch.randint(0, 10, (16,), generator=torch.Generator().manual_seed(t)).to(DEV)
+        for net, opt in ((net_a, opt_a), (net_b, opt_b)):
+            opt.zero_grad()
+            torch.nn.functional.cross_entropy(net(x), y).backward()
+        g = opt_b.flat_g.cpu().numpy()[None]
+        assert np.array_equal(g[0], opt_a.flat_g.cpu().numpy())
+        prev = opt_b.flat_p.cpu().numpy(), opt_b.delta.cpu().numpy(), opt_b.m.cpu().numpy()
+        opt_a.step()
+        opt_b.step()
+        code, st = opt_b.status()
+        assert code == 0 and st.skipped == 0
+        assert torch.equal(opt_a.flat_p, opt_b.flat_p) and torch.equal(opt_a.delta, opt_b.delta) and \
+            torch.equal(opt_a.m, opt_b.m), t
+        check_state(opt_b.flat_p.cpu().numpy(), opt_b.delta.cpu().numpy(), opt_b.m.cpu().numpy(), *prev,
+                    exchange.exchange(list(g), s).ghat, schedule.coeffs_at(t, schedule.Hyper(), C1))
+    # a NaN in one parameter's gradient (a tensor hook, i.e. inside backward): every bucket
+    # is exchanged, the update is skipped, the first index is the global flat index
+    w = net_b[3].weight
+    off = sum(p.numel() for p in opt_b.params[:[id(p) for p in opt_b.params].index(id(w))])
+    h = w.register_hook(lambda gr: gr.index_put((torch.tensor([1], device=DEV),), torch.tensor(float("nan"),
+                                                                                            device=DEV)))
+    before = opt_b.flat_p.clone(), opt_b.delta.clone(), opt_b.m.clone()
+    opt_b.zero_grad()
+    torch.nn.functional.cross_entropy(net_b(x), y).backward()
+    opt_b.step()
+    code, st = opt_b.status()
+    h.remove()
+    row = w.shape[1] * w.shape[2] * w.shape[3]
+    assert code == L.LMSGD_ERR_NONFINITE and st.skipped == 1 and st.first_nonfinite == off + row, \
+        (code, st.first_nonfinite, off + row)
+    assert torch.equal(before[0], opt_b.flat_p) and torch.equal(before[1], opt_b.delta) and torch.equal(before[2], opt_b.m)
+    # and the next clean step goes through
+    opt_b.zero_grad()
+    torch.nn.functional.cross_entropy(net_b(x), y).backward()
+    opt_b.step()
+    assert opt_b.status()[0] == 0
+    opt_a.close()
+    opt_b.close()

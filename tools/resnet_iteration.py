@@ -36,6 +36,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--batch", type=int, default=32)
     ap.add_argument("--weight-decay", type=float, default=0.0, help="R12 (Goyal et al. used 1e-4)")
+    ap.add_argument("--bucketed", type=int, default=0,
+                    help="row f1: BucketedLMSGD with buckets of this many elements, each exchanged from a "
+                         "post-accumulate-grad hook on a side stream while backward runs (0 = LMSGD, the "
+                         "exchange after backward)")
+    ap.add_argument("--exchange-blocks", type=int, default=0, help="bucketed: k_xstep1 grid cap (0 = whole GPU)")
     args = ap.parse_args()
     rank, world, local = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), \
         int(os.environ.get("LOCAL_RANK", 0))
@@ -47,8 +52,12 @@ def main():
     model = torchvision.models.resnet50().to(dev)
     bn_sync.last_minibatch_bn(model)
     # the torch-style front end: parameters and gradients become views of flat buffers
-    opt = L.LMSGD(model.parameters(), cluster=L.make_cluster(1024, args.batch), loss_scale=1024.0,
-                  weight_decay=args.weight_decay)
+    if args.bucketed:
+        opt = L.BucketedLMSGD(model.parameters(), cluster=L.make_cluster(1024, args.batch), loss_scale=1024.0,
+                              bucket_elems=args.bucketed, exchange_blocks=args.exchange_blocks)
+    else:
+        opt = L.LMSGD(model.parameters(), cluster=L.make_cluster(1024, args.batch), loss_scale=1024.0,
+                      weight_decay=args.weight_decay)
     n, ctx = opt.n, opt.ctx
     sync = bn_sync.BNStatsSync(model, ctx)
     gen = torch.Generator(device=dev)
@@ -85,6 +94,11 @@ def main():
     if rank == 0:
         out = {"what": "ResNet-50 synchronous SGD iteration, synthetic data, lmsgd exchange + update",
                "n_gpus": world, "batch_per_gpu": args.batch, "params": n, "iters": args.iters, **res,
+               "optimizer": (f"BucketedLMSGD({len(opt.buckets)} buckets of ~{args.bucketed} elements, exchange "
+                             f"overlapped with backward, k_xstep1 grid cap {args.exchange_blocks or 'none'})"
+                             if args.bucketed else "LMSGD (lmsgd_step after backward)"),
+               "note": "exchange_update_ms = backward end -> step end on the main stream: the exchange and "
+                       "update time NOT hidden behind backward (with rank skew at N > 1)",
                "exchange_share": res["exchange_update_ms"] / res["iteration_ms"],
                "images_per_s": world * args.batch / (res["iteration_ms"] * 1e-3),
                "last_status": code, "loss": float(loss)}
