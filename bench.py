@@ -56,7 +56,9 @@ def parse():
                         "push + exact fp64 owner reduce (default); rs = NVSwitch reduction (fp32 accumulation) "
                         "into the owner's R; allreduce = rs + multicast of R back into every rank's wire. "
                         "Every available mode is timed in the nvlink section either way")
-    p.add_argument("--no-nvls", action="store_true", help="N>1: do not bind the NVLS multicast wire at all (A/B)")
+    p.add_argument("--nvls-ab", action="store_true",
+                   help="N>1: also bind the NVLS multicast wire and time every exchange mode (nvlink.modes); "
+                        "implied by --nvls rs|allreduce")
     p.add_argument("--e2e-steps", type=int, default=50)
     p.add_argument("--full-schedule", action="store_true",
                    help="config C5: time the whole 90-epoch schedule (T = 3,519 steps at 32k from t = 1) with the "
@@ -358,7 +360,7 @@ def main():
     if world > 1:
         sup = torch.tensor([1 if L.lmsgd_nvls_supported(local) else 0], device=devc)
         dist.all_reduce(sup, op=dist.ReduceOp.MIN)
-        nvls_ok = bool(sup.item()) and not args.no_nvls
+        nvls_ok = bool(sup.item()) and (args.nvls_ab or args.nvls != "off")
         if nvls_ok:   # bind the multicast wire once; the headline mode is --nvls
             L.connect_nvls(ctx, NV_MODES[args.nvls])
     assert args.nvls == "off" or nvls_ok, "--nvls needs multicast support on every GPU"

@@ -7,12 +7,13 @@
 
 namespace lmsgd {
 namespace {
-#include "../paper_1711_04325_b200/csrc/stream_tma.cuh"
+#include "stream_tma.cuh"   // tools/: the TMA-staged development variant
 }  // namespace
 }  // namespace lmsgd
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <functional>
 #include <vector>
 
@@ -233,6 +234,26 @@ __global__ void __launch_bounds__(256) k_ag_push(const uint16_t* __restrict__ Rm
     __threadfence_system();
 }
 
+// f4 (sharded update): every rank updates only its own shard (above, with
+// launch_update on the shard), then pulls the other owners' updated fp32 theta shards
+// (4 B/elem over NVLink, interleaved units like k_upd_pull).
+struct ThPtrs { const float* th[8]; };
+__global__ void __launch_bounds__(256) k_th_gather(ThPtrs P, int world, int rank, int64_t shard, int64_t n,
+                                                   float* __restrict__ th) {
+    const int64_t gsh = shard >> 2;                      // float4 groups per shard
+    const int64_t u = blockIdx.x;                        // unit: 256 float4 of one remote owner
+    const int q = (int)(u % (world - 1));
+    const int owner = (rank + 1 + q) % world;
+    const int64_t gi = (u / (world - 1)) * 256 + threadIdx.x;
+    if (gi >= gsh) return;
+    const int64_t j0 = (int64_t)owner * shard + (gi << 2);
+    if (j0 + 4 <= n) {
+        __stcs(reinterpret_cast<float4*>(th + j0), *reinterpret_cast<const float4*>(P.th[owner] + j0));
+    } else {
+        for (int64_t j = j0; j < n; ++j) th[j] = P.th[owner][j];
+    }
+}
+
 }  // namespace xb
 
 int main(int argc, char** argv) {
@@ -265,10 +286,14 @@ int main(int argc, char** argv) {
     UpdConst c{0.9f, 0.99f, (float)(1.0 - 0.99), 1e-8f, 6.4f, 0.0091578f, 4.64e-05f, 1.0f / 4096};
     xb::Ptrs P{};
     for (int i = 0; i < W; ++i) P.R[i] = R[i];
+    // argv[1]: run only the benchmarks whose name contains it; XB_ITERS: timed iterations
+    // (a short run under ncu: every launch is profiled)
+    const char* only = argc > 1 ? argv[1] : nullptr;
+    const int iters = std::getenv("XB_ITERS") ? std::atoi(std::getenv("XB_ITERS")) : 30;
     auto run = [&](const char* name, double bytes, const std::function<void(int)>& f) {
+        if (only && !std::strstr(name, only)) return;
         for (int it = 0; it < 3; ++it) for (int i = 0; i < W; ++i) { cudaSetDevice(i); f(i); }
         for (int i = 0; i < W; ++i) { cudaSetDevice(i); CKE(cudaDeviceSynchronize()); }
-        const int iters = 30;
         for (int i = 0; i < W; ++i) { cudaSetDevice(i); cudaEventRecord(e0[i], st[i]); }
         for (int it = 0; it < iters; ++it) for (int i = 0; i < W; ++i) { cudaSetDevice(i); f(i); }
         float worst = 0;
@@ -315,6 +340,19 @@ int main(int argc, char** argv) {
             xb::k_push_fenced<<<sms * 2, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1);
             xb::k_upd_pull<<<W * ups, 256, 0, st2[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]);
             cudaEventRecord(ev, st2[i]); cudaStreamWaitEvent(st[i], ev, 0); cudaEventDestroy(ev); });
+    }
+    {   // f4: sharded update + fp32 theta all-gather, against the replicated update above
+        xb::ThPtrs TP{};
+        for (int i = 0; i < W; ++i) TP.th[i] = th[i];
+        auto nsh = [&](int i) { const int64_t lo = (int64_t)i * shard; return lo >= n ? (int64_t)0 : (n - lo < shard ? n - lo : shard); };
+        const int gunits = (int)((W - 1) * (((shard >> 2) + 255) / 256));
+        run("f4 sharded update (own shard, local R)", 26.0 * n / W, [&](int i) {
+            if (nsh(i)) launch_update(st[i], L, R[i], nsh(i), c, th[i] + (int64_t)i * shard, d[i], m[i], nullptr, nullptr, nullptr); });
+        run("f4 theta all-gather pull (fp32)", 4.0 * n * (W - 1) / W, [&](int i) {
+            xb::k_th_gather<<<gunits, 256, 0, st[i]>>>(TP, W, i, shard, n, th[i]); });
+        run("f4 sharded update + theta all-gather", 26.0 * n, [&](int i) {
+            if (nsh(i)) launch_update(st[i], L, R[i], nsh(i), c, th[i] + (int64_t)i * shard, d[i], m[i], nullptr, nullptr, nullptr);
+            xb::k_th_gather<<<gunits, 256, 0, st[i]>>>(TP, W, i, shard, n, th[i]); });
     }
     run("AG push R shard to all (persistent 148x8)", 2.0 * shard * (W - 1), [&](int i) { xb::k_ag_push<<<sms * 8, 256, 0, st[i]>>>(R[i], fullp[i], W, i, shard); });
     run("AG push + local update", 26.0 * n, [&](int i) { xb::k_ag_push<<<sms * 8, 256, 0, st[i]>>>(R[i], fullp[i], W, i, shard);
