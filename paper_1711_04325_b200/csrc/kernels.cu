@@ -728,8 +728,10 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
         }
         flush_status(first, sat, mine, ST_PACK_SAT);
     }
-    __threadfence_system();
+    // this block's pushes and status atomics, then its ticket: bar.sync + one thread's
+    // system fence (cumulativity; the grid-sync pattern)
     __syncthreads();
+    if (t0) __threadfence_system();
     if (t0 && atomicAdd(a.ctr + 0, 1u) + 1u == G.g()) {
         a.ctr[0] = 0;
         stamp(x, TR_PACK_END);
@@ -785,6 +787,35 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
     const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
     uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
     unsigned sat = 0;
+    __shared__ uint32_t s_fv;   // this step's chunk-flag value (thread 0; 0 = not read yet)
+    if (t0) s_fv = 0;
+    // thread 0, after a bar.sync and a system fence that order this block's R writes of
+    // unit u (cumulativity): count the unit into its chunk; the block completing a chunk
+    // releases it to every rank (cflag[c][rank] = 2 epoch + skip)
+    auto count_unit = [&](int64_t u) {
+        const int c = (int)(u / x.lay.cu);
+        const int64_t rem = ups - (int64_t)c * x.lay.cu;
+        const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
+        if (atomicAdd(a.ctr + 4 + c, 1u) + 1u == cnt) {
+            a.ctr[4 + c] = 0;
+            // the other blocks fenced their R writes before their tickets; this fence
+            // orders the observed tickets (hence those writes) before the flag stores
+            // peers acquire (cumulativity), as publish() does after its ticket
+            __threadfence_system();
+            if (!s_fv) s_fv = cflag_value(x, ep);
+            for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, c, x.rank), s_fv);
+        }
+    };
+    // LMSGD_RED_PER_ROUND (A/B knob, off): release after every round of units (bar.sync,
+    // then ONE thread's system fence -- the grid-sync pattern), so the update starts on the
+    // first chunks while later rounds are reduced.  Measured at k = 4 (round 2,
+    // profiles/r2/ab/reduce_release_n4.txt): the update blocks then start 16 us earlier
+    // but compete with the reduce for HBM (block 0's reduce 12 -> 60 us, update 92 ->
+    // 111 us) -- step 206.3 vs 204.5 us; the 32-register cap also spills the fp64
+    // accumulators.  Default: one fence per block after all its units.
+#ifndef LMSGD_RED_PER_ROUND
+#define LMSGD_RED_PER_ROUND 0
+#endif
     if (NV) {
         // this shard's 8-element groups summed by the switch over every rank's wire,
         // NVU units per trip with all their ld_reduce issued first (more bytes in flight)
@@ -806,36 +837,36 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
                 if (NV == 2) mm_st_16B(x.nv_mc + off[i], v[i]);   // into every rank's wire, in place
                 else *reinterpret_cast<uint4*>(R + (off[i] / 2 - (int64_t)x.rank * x.lay.shard)) = v[i];
             }
+            if (LMSGD_RED_PER_ROUND) {
+                if (u0 + NVU * G.g() >= ups) flush_status(kNone, sat, mine, ST_SUM_SAT);   // before the last release
+                __syncthreads();
+                if (t0) {
+                    __threadfence_system();
+                    for (int i = 0; i < NVU; ++i)
+                        if (u0 + i * G.g() < ups) count_unit(u0 + i * G.g());
+                }
+            }
         }
     } else {
         for (int64_t u = G.b(); u < ups; u += G.g()) {
             const int64_t gi = u * kThreads + threadIdx.x;
             if (gi < gsh) reduce8(recv, x.lay.shard, x.world, gi << 3, R, sat);
-        }
-    }
-    flush_status(kNone, sat, mine, ST_SUM_SAT);
-    // one system fence per block, then count this block's units into their chunks.  A
-    // fence + release after every round (so early chunks go out while later rounds run)
-    // measured slower: reduce 12 -> 34 us, step 204 -> 215 us at k = 4
-    // (profiles/r1/ab/reduce_fence_per_round_n4.txt).
-    __threadfence_system();
-    __syncthreads();
-    if (t0) {
-        uint32_t fv = 0;
-        for (int64_t u = G.b(); u < ups; u += G.g()) {
-            const int c = (int)(u / x.lay.cu);
-            const int64_t rem = ups - (int64_t)c * x.lay.cu;
-            const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
-            if (atomicAdd(a.ctr + 4 + c, 1u) + 1u == cnt) {
-                a.ctr[4 + c] = 0;
-                // the other blocks fenced their R writes before their tickets; this fence
-                // orders the observed tickets (hence those writes) before the flag stores
-                // peers acquire (cumulativity), as publish() does after its ticket
-                __threadfence_system();
-                if (!fv) fv = cflag_value(x, ep);
-                for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, c, x.rank), fv);
+            if (LMSGD_RED_PER_ROUND) {
+                if (u + G.g() >= ups) flush_status(kNone, sat, mine, ST_SUM_SAT);   // before the last release
+                __syncthreads();
+                if (t0) {
+                    __threadfence_system();
+                    count_unit(u);
+                }
             }
         }
+    }
+    if (!LMSGD_RED_PER_ROUND) {
+        flush_status(kNone, sat, mine, ST_SUM_SAT);
+        __threadfence_system();
+        __syncthreads();
+        if (t0)
+            for (int64_t u = G.b(); u < ups; u += G.g()) count_unit(u);
     }
     if (G.b() == 0 && t0) stamp(x, TR_RED_END);
 
@@ -916,14 +947,25 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
     if (!go || s_range) return;
     const UpdConst c = s_c;
 #pragma unroll
+    // every unit's R (a peer load for remote owners) issued before the first update
+    // (LMSGD_XUPD_PREFETCH; 0 = load each unit's R right before its update)
+#ifndef LMSGD_XUPD_PREFETCH
+#define LMSGD_XUPD_PREFETCH 1
+#endif
+    uint4 rv[kXUnits];
+    int64_t j0v[kXUnits];
+#pragma unroll
     for (int v = 0; v < kXUnits; ++v) {
-        if (us[v] >= ups) continue;
         const int64_t gi = us[v] * kThreads + threadIdx.x;
-        if (gi >= gsh) continue;
-        const int64_t j0 = ((int64_t)owner[v] * gsh + gi) << 3;
-        if (j0 >= x.n) continue;
-        const uint16_t* Rp = r_src(x, LOCALR, owner[v], gi);
-        update8<RMS, WD, KM>(*reinterpret_cast<const uint4*>(Rp), j0, x.n, c, a.th, a.d, a.m);
+        j0v[v] = (us[v] < ups && gi < gsh) ? ((int64_t)owner[v] * gsh + gi) << 3 : x.n;
+        if (LMSGD_XUPD_PREFETCH && j0v[v] < x.n) rv[v] = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner[v], gi));
+    }
+#pragma unroll
+    for (int v = 0; v < kXUnits; ++v) {
+        if (j0v[v] >= x.n) continue;
+        if (!LMSGD_XUPD_PREFETCH)
+            rv[v] = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner[v], us[v] * kThreads + threadIdx.x));
+        update8<RMS, WD, KM>(rv[v], j0v[v], x.n, c, a.th, a.d, a.m);
     }
 }
 
