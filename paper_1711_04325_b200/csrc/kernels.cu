@@ -690,7 +690,10 @@ __device__ __forceinline__ uint32_t cflag_value(const XArgs& x, const Ep& ep) {
 // this rank's shard into R; 2 = as 1, and the reduced shard is multicast (multimem.st) back
 // into every rank's wire in place, so every rank then holds the whole all-reduce result
 // locally.
-template <bool SIM, int NV>
+// XCH (lmsgd_exchange: a.rout != NULL): the reduce releases its chunks after every round
+// (its consumer, k_xgather's pull, is NVLink-bound and does not compete with the reduce
+// for HBM); the step releases once per block (see LMSGD_RED_PER_ROUND).
+template <bool SIM, int NV, bool XCH>
 __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
     static_assert(!(SIM && NV), "NVLS needs one GPU per rank");
     pdl_enter();   // wait for the previous step / caller work; let k_xupdate queue up
@@ -816,6 +819,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
 #ifndef LMSGD_RED_PER_ROUND
 #define LMSGD_RED_PER_ROUND 0
 #endif
+    constexpr bool per_round = LMSGD_RED_PER_ROUND || XCH;
     if (NV) {
         // this shard's 8-element groups summed by the switch over every rank's wire,
         // NVU units per trip with all their ld_reduce issued first (more bytes in flight)
@@ -837,7 +841,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
                 if (NV == 2) mm_st_16B(x.nv_mc + off[i], v[i]);   // into every rank's wire, in place
                 else *reinterpret_cast<uint4*>(R + (off[i] / 2 - (int64_t)x.rank * x.lay.shard)) = v[i];
             }
-            if (LMSGD_RED_PER_ROUND) {
+            if constexpr (per_round) {
                 if (u0 + NVU * G.g() >= ups) flush_status(kNone, sat, mine, ST_SUM_SAT);   // before the last release
                 __syncthreads();
                 if (t0) {
@@ -851,7 +855,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
         for (int64_t u = G.b(); u < ups; u += G.g()) {
             const int64_t gi = u * kThreads + threadIdx.x;
             if (gi < gsh) reduce8(recv, x.lay.shard, x.world, gi << 3, R, sat);
-            if (LMSGD_RED_PER_ROUND) {
+            if constexpr (per_round) {
                 if (u + G.g() >= ups) flush_status(kNone, sat, mine, ST_SUM_SAT);   // before the last release
                 __syncthreads();
                 if (t0) {
@@ -861,7 +865,7 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
             }
         }
     }
-    if (!LMSGD_RED_PER_ROUND) {
+    if constexpr (!per_round) {
         flush_status(kNone, sat, mine, ST_SUM_SAT);
         __threadfence_system();
         __syncthreads();
@@ -1167,13 +1171,22 @@ cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), int grid, int bloc
 
 int xstep_blocks_per_sm(bool sim) {
     int b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, sim ? k_xstep1<true, 0> : k_xstep1<false, 0>, kThreads, 0);
-    int b1 = 0, b2 = 0;   // the NVLS instantiations share the grid size: take the smallest
-    if (!sim) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b1, k_xstep1<false, 1>, kThreads, 0);
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b2, k_xstep1<false, 2>, kThreads, 0);
-        b = b1 < b ? b1 : b;
-        b = b2 < b ? b2 : b;
+    // every instantiation shares the grid size: take the smallest occupancy
+    auto occ = [&](auto k) {
+        int v = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, kThreads, 0);
+        b = (b == 0 || v < b) ? v : b;
+    };
+    if (sim) {
+        occ(k_xstep1<true, 0, false>);
+        occ(k_xstep1<true, 0, true>);
+    } else {
+        occ(k_xstep1<false, 0, false>);
+        occ(k_xstep1<false, 0, true>);
+        occ(k_xstep1<false, 1, false>);
+        occ(k_xstep1<false, 1, true>);
+        occ(k_xstep1<false, 2, false>);
+        occ(k_xstep1<false, 2, true>);
     }
     return b > 0 ? b : 1;
 }
@@ -1204,10 +1217,16 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const 
         cfg.attrs = attr;
         cfg.numAttrs = (L.pdl_mask & 2) ? 2 : 1;   // + programmatic dependent launch (hides the launch latency)
         const int nv = sim ? 0 : a.x.nv;
-        e = sim       ? cudaLaunchKernelEx(&cfg, k_xstep1<true, 0>, arg, sm)
-            : nv == 1 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 1>, arg, sm)
-            : nv == 2 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 2>, arg, sm)
-                      : cudaLaunchKernelEx(&cfg, k_xstep1<false, 0>, arg, sm);
+        if (a.rout)   // lmsgd_exchange
+            e = sim       ? cudaLaunchKernelEx(&cfg, k_xstep1<true, 0, true>, arg, sm)
+                : nv == 1 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 1, true>, arg, sm)
+                : nv == 2 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 2, true>, arg, sm)
+                          : cudaLaunchKernelEx(&cfg, k_xstep1<false, 0, true>, arg, sm);
+        else
+            e = sim       ? cudaLaunchKernelEx(&cfg, k_xstep1<true, 0, false>, arg, sm)
+                : nv == 1 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 1, false>, arg, sm)
+                : nv == 2 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 2, false>, arg, sm)
+                          : cudaLaunchKernelEx(&cfg, k_xstep1<false, 0, false>, arg, sm);
     }
     if (e != cudaSuccess) return e;
     const bool pdl = (L.pdl_mask & 4) == 0;   // bit 4 (diagnostics): launch k_xupdate after k_xstep1 completes

@@ -180,7 +180,11 @@ class BucketedLMSGD(LMSGD):
 
     The arithmetic is that of ``LMSGD``'s step (the same fp16 all-reduce sum per element,
     the same update kernel body), so the results are bit-identical to it.  No weight
-    decay, no out-of-place mode (the sub-step update has neither)."""
+    decay, no out-of-place mode (the sub-step update has neither).
+
+    One backward per step: a bucket is exchanged as soon as its gradients are in, so a
+    second backward before ``step()`` (gradient accumulation) must run inside
+    ``no_sync()`` -- the hooks then do nothing and ``step()`` exchanges every bucket."""
 
     def __init__(self, params, *, bucket_elems: int = 1 << 22, exchange_blocks: int = 0, overlap: bool = True,
                  **kw):
@@ -235,9 +239,27 @@ class BucketedLMSGD(LMSGD):
             for i, p in enumerate(self.params):
                 self._hooks.append(p.register_post_accumulate_grad_hook(lambda _p, i=i: self._grad_ready(i)))
 
+    def no_sync(self):
+        """Context manager: backward passes inside it only accumulate (no bucket exchange)."""
+        import contextlib
+
+        @contextlib.contextmanager
+        def _ctx():
+            self._paused = True
+            try:
+                yield
+            finally:
+                self._paused = False
+        return _ctx()
+
     def _grad_ready(self, i: int):
+        if getattr(self, "_paused", False):
+            return
         for b in self._p2b[i]:
             self._pending[b] -= 1
+            if self._pending[b] < 0:
+                raise RuntimeError("BucketedLMSGD: a second backward before step() -- its bucket was already "
+                                   "exchanged; accumulate gradients inside opt.no_sync()")
             if self._pending[b] == 0:
                 self._launch(b, torch.cuda.current_stream(self.flat_g.device))
 

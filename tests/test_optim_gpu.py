@@ -249,3 +249,34 @@ def test_bucketed_lmsgd_matches_lmsgd_and_oracle(monkeypatch, overlap, bucket):
     assert opt_b.status()[0] == 0
     opt_a.close()
     opt_b.close()
+
+
+def test_bucketed_lmsgd_accumulation_needs_no_sync(monkeypatch):
+    """Two backward passes before one step: inside no_sync() the first only accumulates and
+    the step equals LMSGD's on the summed gradient; without it the second backward is
+    refused (its buckets were already exchanged)."""
+    monkeypatch.setattr(torch.backends.cudnn, "deterministic", True)
+    monkeypatch.setattr(torch.backends.cudnn, "benchmark", False)
+    s = 1024.0
+    net_a, net_b = _deep_net(), _deep_net()
+    opt_a = L.LMSGD(net_a.parameters(), cluster=L.make_cluster(2, 32, 64), loss_scale=s)
+    opt_b = L.BucketedLMSGD(net_b.parameters(), cluster=L.make_cluster(2, 32, 64), loss_scale=s, bucket_elems=2048)
+    xs = [torch.randn(8, 3, 8, 8, generator=torch.Generator().manual_seed(i)).to(DEV) for i in range(2)]
+    y = torch.zeros(8, dtype=torch.long, device=DEV)
+    for net, opt in ((net_a, opt_a), (net_b, opt_b)):
+        opt.zero_grad()
+        if opt is opt_b:
+            with opt_b.no_sync():
+                torch.nn.functional.cross_entropy(net(xs[0]), y).backward()
+        else:
+            torch.nn.functional.cross_entropy(net(xs[0]), y).backward()
+        torch.nn.functional.cross_entropy(net(xs[1]), y).backward()
+        opt.step()
+    assert opt_b.status()[0] == 0
+    assert torch.equal(opt_a.flat_p, opt_b.flat_p) and torch.equal(opt_a.delta, opt_b.delta)
+    opt_b.zero_grad()
+    torch.nn.functional.cross_entropy(net_b(xs[0]), y).backward()
+    with pytest.raises(RuntimeError, match="no_sync"):
+        torch.nn.functional.cross_entropy(net_b(xs[1]), y).backward()
+    opt_a.close()
+    opt_b.close()
