@@ -229,6 +229,8 @@ class NvlinkCounters:
             if mg.metrics[i].nvmlReturn != 0:
                 raise RuntimeError(f"gpm metric {mg.metrics[i].metricId}: return {mg.metrics[i].nvmlReturn}")
         dt = b[1] - a[1]
+        for smp in (a[0], b[0]):
+            nv.nvmlGpmSampleFree(smp)
         # NVML reports these two metrics in MiB/s
         return {"tx": mg.metrics[0].value * 2 ** 20 * dt, "rx": mg.metrics[1].value * 2 ** 20 * dt}
 

@@ -288,11 +288,8 @@ struct Drv {
     bool ok = false;
 };
 
-const Drv& drv() {
-    static Drv d;
-    static bool init = false;
-    if (init) return d;
-    init = true;
+Drv load_drv() {
+    Drv d;
     bool ok = true;
     auto get = [&](const char* name, auto& fn) {
         void* p = nullptr;
@@ -319,6 +316,11 @@ const Drv& drv() {
     get("cuMemExportToShareableHandle", d.exportH);
     get("cuMemImportFromShareableHandle", d.importH);
     d.ok = ok;
+    return d;
+}
+
+const Drv& drv() {
+    static const Drv d = load_drv();   // thread-safe one-time initialisation
     return d;
 }
 
@@ -356,7 +358,7 @@ socklen_t abstract_addr(const char* name, sockaddr_un* a) {
 void fd_server(int lfd, int fd, int peers) {
     for (int i = 0; i < peers; ++i) {
         pollfd p{lfd, POLLIN, 0};
-        if (poll(&p, 1, 120000) <= 0) break;   // 2 min without a peer: give up
+        if (poll(&p, 1, 60000) <= 0) break;   // a minute without a peer: give up
         const int cfd = accept(lfd, nullptr, nullptr);
         if (cfd < 0) break;
         char byte = 'f';

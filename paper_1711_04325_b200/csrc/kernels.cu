@@ -690,10 +690,7 @@ __device__ __forceinline__ uint32_t cflag_value(const XArgs& x, const Ep& ep) {
 // this rank's shard into R; 2 = as 1, and the reduced shard is multicast (multimem.st) back
 // into every rank's wire in place, so every rank then holds the whole all-reduce result
 // locally.
-// XCH (lmsgd_exchange: a.rout != NULL): the reduce releases its chunks after every round
-// (its consumer, k_xgather's pull, is NVLink-bound and does not compete with the reduce
-// for HBM); the step releases once per block (see LMSGD_RED_PER_ROUND).
-template <bool SIM, int NV, bool XCH>
+template <bool SIM, int NV>
 __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
     static_assert(!(SIM && NV), "NVLS needs one GPU per rank");
     pdl_enter();   // wait for the previous step / caller work; let k_xupdate queue up
@@ -819,7 +816,10 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
 #ifndef LMSGD_RED_PER_ROUND
 #define LMSGD_RED_PER_ROUND 0
 #endif
-    constexpr bool per_round = LMSGD_RED_PER_ROUND || XCH;
+    // (the same per-round release for lmsgd_exchange, whose consumer is k_xgather's pull,
+    // measured slower too: k = 4 187 vs 180 us, k = 2 174 vs 148 us per exchange,
+    // profiles/r2/ab/exchange_release.txt)
+    constexpr bool per_round = LMSGD_RED_PER_ROUND;
     if (NV) {
         // this shard's 8-element groups summed by the switch over every rank's wire,
         // NVU units per trip with all their ld_reduce issued first (more bytes in flight)
@@ -1178,15 +1178,11 @@ int xstep_blocks_per_sm(bool sim) {
         b = (b == 0 || v < b) ? v : b;
     };
     if (sim) {
-        occ(k_xstep1<true, 0, false>);
-        occ(k_xstep1<true, 0, true>);
+        occ(k_xstep1<true, 0>);
     } else {
-        occ(k_xstep1<false, 0, false>);
-        occ(k_xstep1<false, 0, true>);
-        occ(k_xstep1<false, 1, false>);
-        occ(k_xstep1<false, 1, true>);
-        occ(k_xstep1<false, 2, false>);
-        occ(k_xstep1<false, 2, true>);
+        occ(k_xstep1<false, 0>);
+        occ(k_xstep1<false, 1>);
+        occ(k_xstep1<false, 2>);
     }
     return b > 0 ? b : 1;
 }
@@ -1217,16 +1213,10 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const 
         cfg.attrs = attr;
         cfg.numAttrs = (L.pdl_mask & 2) ? 2 : 1;   // + programmatic dependent launch (hides the launch latency)
         const int nv = sim ? 0 : a.x.nv;
-        if (a.rout)   // lmsgd_exchange
-            e = sim       ? cudaLaunchKernelEx(&cfg, k_xstep1<true, 0, true>, arg, sm)
-                : nv == 1 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 1, true>, arg, sm)
-                : nv == 2 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 2, true>, arg, sm)
-                          : cudaLaunchKernelEx(&cfg, k_xstep1<false, 0, true>, arg, sm);
-        else
-            e = sim       ? cudaLaunchKernelEx(&cfg, k_xstep1<true, 0, false>, arg, sm)
-                : nv == 1 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 1, false>, arg, sm)
-                : nv == 2 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 2, false>, arg, sm)
-                          : cudaLaunchKernelEx(&cfg, k_xstep1<false, 0, false>, arg, sm);
+        e = sim       ? cudaLaunchKernelEx(&cfg, k_xstep1<true, 0>, arg, sm)
+            : nv == 1 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 1>, arg, sm)
+            : nv == 2 ? cudaLaunchKernelEx(&cfg, k_xstep1<false, 2>, arg, sm)
+                      : cudaLaunchKernelEx(&cfg, k_xstep1<false, 0>, arg, sm);
     }
     if (e != cudaSuccess) return e;
     const bool pdl = (L.pdl_mask & 4) == 0;   // bit 4 (diagnostics): launch k_xupdate after k_xstep1 completes
