@@ -832,6 +832,32 @@ def main():
         L.lmsgd_finalize(ctxo)
         del vs
 
+    # N = 1 out of place: a skipped step (a non-finite gradient) = the fused pass + the
+    # repair copy in -> out by k_repair1 (24 B/elem more)
+    if oop and not args.no_profile:
+        bad = grads.clone()
+        bad[n // 2] = float("nan")
+        pb = P(bad.data_ptr())
+        kk = 20
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(kk):
+            a_, b_ = sets[i & 1], sets[(i & 1) ^ 1]
+            lib.lmsgd_step_out_of_place(ctx.ptr, sp, a_[0], b_[0], pb, a_[2], b_[2], a_[3], b_[3],
+                                        ctypes.byref(coeffs[i]))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        sk_ms = e0.elapsed_time(e1) / kk
+        codes, sts = L.lmsgd_query_status(ctx)
+        assert codes == L.LMSGD_ERR_NONFINITE and sts.skipped == 1
+        variants = variants or {}
+        variants["out_of_place_skipped_step"] = {
+            "ms_per_step": sk_ms, "steps": kk,
+            "hbm_gbs_algorithmic": (FUSED_BYTES_PER_ELEM + 24) * n / (sk_ms * 1e-3) / 1e9,
+            "note": "every step has a non-finite gradient: k_fused1_oop (28 B/elem) + k_repair1's copy in -> out "
+                    "(24 B/elem, one block per SM)"}
+        del bad
+
     # SGD phase (alpha_RMSprop = 0, t >= 490 at 32k: 86% of the 3,519 steps), with and
     # without LMSGD_FLAG_FREEZE_M (m not touched: 18 instead of 26 B/elem in the update)
     if not args.no_profile and not args.full_schedule:

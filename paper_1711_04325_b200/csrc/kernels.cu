@@ -19,6 +19,7 @@
 #include <utility>
 
 #include "lmsgd_internal.h"
+#include "device_common.cuh"
 
 namespace lmsgd {
 namespace {
@@ -82,21 +83,6 @@ __device__ __forceinline__ unsigned short sat16_f64(double a, unsigned& sat) {
     if (fabs(a) > 65504.0) ++sat;
     a = fmin(fmax(a, -65504.0), 65504.0);
     return __half_as_ushort(__double2half(a));
-}
-
-// Programmatic dependent launch (sm_90+): every product kernel lets the next kernel
-// in the stream be scheduled immediately and waits for its own predecessors to
-// complete (and their memory to be visible) before touching any data.  This hides
-// the launch latency between the step's kernels without changing their ordering.
-__device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
-__device__ __forceinline__ uint64_t globaltimer() {
-    uint64_t t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
 }
 
 __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
@@ -257,17 +243,6 @@ __device__ __forceinline__ void reset_status(int64_t* st) {
     if (st && blockIdx.x == 0 && threadIdx.x < ST_WORDS) reset_words(st);
 }
 
-// `last` record in the public lmsgd_step_status layout:
-// {int64 first (-1 none), int64 pack_sat, int64 sum_sat, int32 skipped, int32 error}
-__device__ __forceinline__ void store_last(int64_t* last, int64_t first, int64_t psat, int64_t ssat,
-                                           int64_t err, int64_t skipped) {
-    last[0] = first == kNone ? -1 : first;
-    last[1] = psat;
-    last[2] = ssat;
-    int32_t* tail = reinterpret_cast<int32_t*>(last + 3);
-    tail[0] = (int32_t)skipped;
-    tail[1] = (int32_t)(err ? err : (first != kNone ? (int64_t)LMSGD_ERR_NONFINITE : 0));
-}
 __device__ __forceinline__ void write_last(int64_t* last, int64_t first, int64_t psat, int64_t ssat,
                                            int64_t err, int64_t skipped) {
     if (last && blockIdx.x == 0 && threadIdx.x == 0) store_last(last, first, psat, ssat, err, skipped);
@@ -429,13 +404,20 @@ __device__ __forceinline__ void update8_oop(uint4 r, int64_t j0, int64_t n, cons
 // like k_fused1) -- the new state goes to separate buffers, so a non-finite gradient,
 // found only at the end, costs nothing but a repair copy (k_repair1).
 template <bool RMS>
+#ifndef LMSGD_OOP_LATE_TRIGGER
+#define LMSGD_OOP_LATE_TRIGGER 0
+#endif
 __global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1_oop(const float* __restrict__ g, int64_t n, float s,
                                                          UpdConst c, const float* __restrict__ thi,
                                                          const float* __restrict__ di, const float* __restrict__ mi,
                                                          float* __restrict__ tho, float* __restrict__ dout,
                                                          float* __restrict__ mo, int64_t* st, int64_t* st_reset,
                                                          int64_t* trace) {
-    pdl_enter();
+    // wait for the previous step and let k_repair1 launch (LMSGD_OOP_LATE_TRIGGER = 1: only
+    // once every block has finished its elements -- measured neutral with one repair block,
+    // +0.7 us per clean step with 148, profiles/r2/ab/repair_n1.txt)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (!LMSGD_OOP_LATE_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     // lmsgd_trace_enable: block 0's start (it runs in the first wave) ...
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR_PACK_START] = (int64_t)globaltimer();
     reset_status(st_reset);
@@ -449,17 +431,23 @@ __global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1_oop(const float* __restrict_
         update8_oop<RMS>(pack8(x, s, j0, first, sat), j0, n, c, thi, di, mi, tho, dout, mo);
     }
     flush_status(first, sat, st, ST_PACK_SAT);
+    if (LMSGD_OOP_LATE_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// After k_fused1_oop: if a gradient was non-finite the step is skipped -- the output
-// buffers receive the unchanged input state (rare path: a grid-stride copy); block 0
-// publishes the status record.  On a clean step every block returns at once.
-__global__ void k_repair1(const int64_t* st, const float* __restrict__ thi, const float* __restrict__ di,
-                          const float* __restrict__ mi, float* __restrict__ tho, float* __restrict__ dout,
-                          float* __restrict__ mo, int64_t n, int64_t* last, int64_t* trace) {
+// After k_fused1_oop: block 0 publishes the status record; if a gradient was non-finite
+// the step is skipped and the output set receives the unchanged input set (theta, Delta,
+// m; a grid-stride copy by every block, 24 B/elem).  On a clean step every block returns
+// at once.  LMSGD_REPAIR_BLOCKS blocks of 512 threads (0 = one per SM), launched with
+// programmatic dependent launch.  Measured (N = 1, R50, 3 runs each, repair_n1.txt): one
+// block (round 1) 105.3 us per clean step but 18.7 ms per skipped step; 32 blocks 105.4 us
+// and 0.78 ms; 148 blocks behind an end-of-block trigger 106.0 us and 0.29 ms.
+__global__ void __launch_bounds__(512) k_repair1(const int64_t* st, const float* __restrict__ thi,
+                                                 const float* __restrict__ di, const float* __restrict__ mi,
+                                                 float* __restrict__ tho, float* __restrict__ dout,
+                                                 float* __restrict__ mo, int64_t n, int64_t* last, int64_t* trace) {
     pdl_enter();
-    // ... and the end of k_fused1_oop: this kernel passes griddepcontrol.wait once every
-    // k_fused1_oop block has completed and its memory is visible
+    // ... and the end of k_fused1_oop: griddepcontrol.wait returns once every k_fused1_oop
+    // block has completed and its memory is visible (lmsgd_trace_enable)
     if (trace && blockIdx.x == 0 && threadIdx.x == 0) trace[TR_UPD_END] = (int64_t)globaltimer();
     const int64_t first = *reinterpret_cast<volatile const int64_t*>(st + ST_FIRST);
     if (blockIdx.x == 0 && threadIdx.x == 0)
@@ -467,9 +455,9 @@ __global__ void k_repair1(const int64_t* st, const float* __restrict__ thi, cons
     if (first == kNone) return;
     const int64_t nv = n >> 2;
     for (int64_t v = gtid(); v < nv; v += gstride()) {
-        reinterpret_cast<float4*>(tho)[v] = reinterpret_cast<const float4*>(thi)[v];
-        reinterpret_cast<float4*>(dout)[v] = reinterpret_cast<const float4*>(di)[v];
-        reinterpret_cast<float4*>(mo)[v] = reinterpret_cast<const float4*>(mi)[v];
+        __stcs(reinterpret_cast<float4*>(tho) + v, __ldcs(reinterpret_cast<const float4*>(thi) + v));
+        __stcs(reinterpret_cast<float4*>(dout) + v, __ldcs(reinterpret_cast<const float4*>(di) + v));
+        __stcs(reinterpret_cast<float4*>(mo) + v, __ldcs(reinterpret_cast<const float4*>(mi) + v));
     }
     for (int64_t j = (nv << 2) + gtid(); j < n; j += gstride()) {
         tho[j] = thi[j]; dout[j] = di[j]; mo[j] = mi[j];
@@ -1302,16 +1290,10 @@ cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, in
                                scale, c, thi, di, mi, tho, dout, mo, st, st_reset, trace);
     if (e != cudaSuccess) return e;
 #ifndef LMSGD_REPAIR_BLOCKS
-// k_repair1 grid: n blocks of 512 threads, or 0 = 4 x SMs.  One block: 105.1 vs 106.4 us
-// per clean step (profiles/r1/ab/repair_grid_n1.txt); the price is a slow copy (a few ms
-// for ResNet-50) on the rare skipped step.
-#define LMSGD_REPAIR_BLOCKS 1
+#define LMSGD_REPAIR_BLOCKS 32   // 0: one block per SM
 #endif
-    if (LMSGD_REPAIR_BLOCKS > 0)
-        return launch_pdl_if(true, k_repair1, LMSGD_REPAIR_BLOCKS, 512, s, (const int64_t*)st, thi, di, mi, tho,
-                             dout, mo, n, last, trace);
-    return launch_pdl_if(true, k_repair1, 4 * L.sm_count, kThreads, s, (const int64_t*)st, thi, di, mi, tho, dout,
-                         mo, n, last, trace);
+    const int rb = LMSGD_REPAIR_BLOCKS > 0 ? LMSGD_REPAIR_BLOCKS : L.sm_count;
+    return launch_pdl_if(true, k_repair1, rb, 512, s, (const int64_t*)st, thi, di, mi, tho, dout, mo, n, last, trace);
 }
 
 cudaError_t launch_status_accumulate(cudaStream_t s, const int64_t* last, int64_t offset, int64_t* acc) {

@@ -83,7 +83,7 @@ cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64
 // graph mode, k = 1: publish the fused step's status (fused) and advance the counters
 cudaError_t launch_advance1(cudaStream_t s, const Dev1& dv, int64_t* last, bool fused);
 cudaError_t launch_finalize_fused(cudaStream_t s, const int64_t* st, int64_t* last);
-// lmsgd_step_out_of_place, k = 1: one pass in -> out, then the repair/status kernel
+// lmsgd_step_out_of_place, k = 1: one pass in -> out, then the status / repair kernel
 cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, int64_t n, float scale,
                              const UpdConst& c, const float* thi, const float* di, const float* mi, float* tho,
                              float* dout, float* mo, int64_t* st, int64_t* st_reset, int64_t* last,

@@ -746,3 +746,46 @@ def test_freeze_m_sgd_phase(flags):
             assert torch.equal(a[2], b[2]), t
     L.lmsgd_finalize(ref)
     L.lmsgd_finalize(frz)
+
+
+def test_out_of_place_skip_is_repaired_in_stream_order_and_fast():
+    """A skipped out-of-place step repairs its output set (k_repair1's copy, 32 blocks): the
+    next step, enqueued with no host synchronisation in between, must read the repaired set
+    (bit-identical to the in-place reference), and the skipped step must cost well under a
+    millisecond, not round 1's 18.7 ms single-block copy."""
+    n = synth.resnet_n_params(50)
+    s = 1024.0
+    th0 = synth.theta0(n, 50)
+    r = np.random.default_rng(5)
+    d0 = (r.standard_normal(n) * 1e-3).astype(np.float32)
+    m0 = (r.random(n) * 1e-6).astype(np.float32)
+    oop, ref = L.lmsgd_init(1, 0, 0, n, s), L.lmsgd_init(1, 0, 0, n, s)
+    sets = [[dev(th0), dev(d0), dev(m0)], [torch.zeros(n, device=DEV) for _ in range(3)]]
+    inplace = [dev(th0), dev(d0), dev(m0)]
+    a = synth.grad_scale(n)
+    gs = [dev(synth.grads(1, t, n, a)[0]) for t in (1, 2, 3, 4)]
+    bad = gs[1].clone()
+    bad[n // 2] = float("nan")
+    seq = [gs[0], bad, gs[2], bad, bad, gs[3]]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(seq) + 1)]
+    torch.cuda.synchronize()
+    cur = 0
+    ev[0].record()
+    for i, g in enumerate(seq):          # no host synchronisation between the steps
+        co = L.lmsgd_schedule_at(None, K32_C, i + 1)
+        src, dst = sets[cur], sets[cur ^ 1]
+        L.lmsgd_step_out_of_place(oop, src[0], dst[0], g, src[1], dst[1], src[2], dst[2], co)
+        ev[i + 1].record()
+        cur ^= 1
+    torch.cuda.synchronize()
+    for i, g in enumerate(seq):
+        L.lmsgd_step(ref, inplace[0], g, inplace[1], inplace[2], L.lmsgd_schedule_at(None, K32_C, i + 1))
+    torch.cuda.synchronize()
+    assert all(torch.equal(x, y) for x, y in zip(sets[cur], inplace))
+    us = [ev[i].elapsed_time(ev[i + 1]) * 1e3 for i in range(len(seq))]
+    clean, skipped = us[5], max(us[3], us[4])    # steps after warm-up
+    # a skipped step = the fused pass + the repair copy by 32 blocks: ~0.8 ms at R50 (round
+    # 1's one-block copy took 18.7 ms)
+    assert skipped < 12.0 * clean and skipped < 2000.0, (us, clean, skipped)
+    L.lmsgd_finalize(oop)
+    L.lmsgd_finalize(ref)
