@@ -470,6 +470,16 @@ lmsgd_status group_check(lmsgd_ctx* const* ctxs, int count, bool need_group) {
     return LMSGD_OK;
 }
 
+// An emulated group's update may use 256-bit accesses only if every rank's state is
+// 32-byte aligned (one kernel instantiation serves all ranks).
+void set_group_v8(std::vector<lmsgd::XStep>& v) {
+    bool all = true;
+    for (const auto& a : v)
+        for (const void* p : {static_cast<const void*>(a.th), static_cast<const void*>(a.d), static_cast<const void*>(a.m)})
+            all = all && (reinterpret_cast<uintptr_t>(p) & 31u) == 0;
+    for (auto& a : v) a.v8 = all ? 1 : 0;
+}
+
 // Upload the per-rank arguments (pageable -> device, stream-ordered) into *dbuf.
 template <typename T>
 lmsgd_status group_upload(lmsgd_ctx* lead, cudaStream_t s, T** dbuf, const std::vector<T>& v) {
@@ -708,8 +718,13 @@ lmsgd_status lmsgd_nvls_bind(lmsgd_ctx* c, int mode) {
     CKD(c, d.memCreate(&c->nv.phys, size, &ap, 0));
     CKD(c, d.mcBind(c->nv.mc, 0, c->nv.phys, 0, size, 0));
     c->nv.bound = true;
-    size_t gran = 0;
+    // VA alignment: the larger of the allocation and multicast granularities (the size
+    // is a multiple of both, lmsgd_nvls_create)
+    size_t gran = 0, gm = 0;
     CKD(c, d.memGran(&gran, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED));
+    const CUmulticastObjectProp mp = mc_prop(c->world, size);
+    CKD(c, d.mcGran(&gm, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED));
+    gran = gm > gran ? gm : gran;
     CUmemAccessDesc acc{};
     acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
     acc.location.id = dev;
@@ -808,6 +823,7 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     }
     const lmsgd::XArgs x = xargs(c, epoch, &c->dstate->xepoch);
     lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, nullptr, 0, nullptr};
+    a.v8 = 1;   // 256-bit accesses if params / delta / m are 32-byte aligned (launch_xstep checks)
     CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, xlaunch(c), a); }));
     return LMSGD_OK;
 }
@@ -972,6 +988,7 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
     if (x.trace) { x.trace = nullptr; --c->trace_steps; }   // the trace ring slot would be frozen in a graph
     lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, c->d_ctab, c->ctab_count,
                    &c->dstate->cursor};
+    a.v8 = 1;
     CK(c, lmsgd::launch_xstep(s, xlaunch(c), a));
     return LMSGD_OK;
 }
@@ -1181,6 +1198,7 @@ lmsgd_status lmsgd_step_group(lmsgd_ctx* const* ctxs, int count, void* stream, f
         v[i] = lmsgd::XStep{xargs(c, epoch, &c->dstate->xepoch), grads[i], c->scale, u, params[i], delta[i], m[i],
                             c->last, c->xctr, nullptr, 0, nullptr, nullptr};
     }
+    set_group_v8(v);
     if ((st = group_upload(lead, s, &lead->d_group, v)) != LMSGD_OK) return st;
     CK(lead, lmsgd::launch_xstep(s, lead->L, v[0], lead->d_group, count));
     return LMSGD_OK;
@@ -1243,6 +1261,7 @@ lmsgd_status lmsgd_step_graph_group(lmsgd_ctx* const* ctxs, int count, void* str
         v[i] = lmsgd::XStep{x, grads[i], c->scale, u, params[i], delta[i], m[i], c->last, c->xctr, c->d_ctab,
                             c->ctab_count, &c->dstate->cursor, nullptr};
     }
+    set_group_v8(v);
     // the arguments do not change between graph-mode calls (everything per-step is read
     // from the device): upload once, outside any capture; a capture then records launches only
     const bool same = lead->group_graph_cache.size() == v.size() &&

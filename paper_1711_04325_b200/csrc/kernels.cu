@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <initializer_list>
 #include <utility>
 
 #include "lmsgd_internal.h"
@@ -124,14 +125,44 @@ __device__ __forceinline__ uint32_t sat_inf_f16x2(uint32_t w, unsigned& sat) {
     return w;
 }
 
+
+// 8 consecutive fp32 at p with the evict-first streaming hint: one 256-bit access
+// (V8: LDG/STG.E.EF.ENL2.256, sm_100; p 32-byte aligned) or two 128-bit ones (p 16-byte
+// aligned).  The host picks V8 when every state / gradient pointer of the launch is
+// 32-byte aligned (a torch allocation is).  Measured (N = 1, R50, profiles/r2/ab/v8_n1.txt):
+// the in-place single pass 114.8 -> 106.0 us, the guarded in-place step 131.9 -> 123.7 us,
+// the SGD-phase step with m frozen 101.7 -> 93.6 us; the out-of-place step unchanged.
+template <bool V8>
+__device__ __forceinline__ void ld8cs(const float* p, float v[8]) {
+    if constexpr (V8) {
+    asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                 : "l"(p));
+    } else {
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
+}
+template <bool V8>
+__device__ __forceinline__ void st8cs(float* p, const float v[8]) {
+    if constexpr (V8) {
+    asm volatile("st.global.cs.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(p), "f"(v[0]), "f"(v[1]),
+                 "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7])
+                 : "memory");
+    } else {
+    __stcs(reinterpret_cast<float4*>(p), make_float4(v[0], v[1], v[2], v[3]));
+    __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(v[4], v[5], v[6], v[7]));
+    }
+}
+
 // 8 consecutive fp32 from j0 (j0 % 8 == 0), zero beyond n.  Streaming loads.
+template <bool V8 = false>
 __device__ __forceinline__ void load8_g(const float* __restrict__ g, int64_t j0, int64_t n,
                                         float x[8]) {
     if (j0 + 8 <= n) {
-        const float4 a = __ldcs(reinterpret_cast<const float4*>(g + j0));
-        const float4 b = __ldcs(reinterpret_cast<const float4*>(g + j0) + 1);
-        x[0] = a.x; x[1] = a.y; x[2] = a.z; x[3] = a.w;
-        x[4] = b.x; x[5] = b.y; x[6] = b.z; x[7] = b.w;
+        ld8cs<V8>(g + j0, x);
     } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) x[i] = (j0 + i < n) ? g[j0 + i] : 0.0f;
@@ -193,37 +224,26 @@ __device__ __forceinline__ void upd1(float gh, float& th, float& d, float& m, co
 // instantiation so the default path carries no per-element test.
 // KM == false (LMSGD_FLAG_FREEZE_M, only with alpha_RMSprop == 0, RMS == false): m
 // is neither read nor written -- it does not enter Delta or theta then.
-template <bool RMS, bool WD, bool KM = true>
+template <bool RMS, bool WD, bool KM = true, bool V8 = false>
 __device__ __forceinline__ void update8(uint4 r, int64_t j0, int64_t n, const UpdConst& c,
                                         float* __restrict__ th, float* __restrict__ d,
                                         float* __restrict__ m) {
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
     if (j0 + 8 <= n) {
-        float4* th4 = reinterpret_cast<float4*>(th + j0);
-        float4* d4 = reinterpret_cast<float4*>(d + j0);
-        float4* m4 = reinterpret_cast<float4*>(m + j0);
-        float4 t0 = __ldcs(th4), t1 = __ldcs(th4 + 1);
-        float4 d0 = __ldcs(d4), d1 = __ldcs(d4 + 1);
         static_assert(KM || !RMS, "m is only frozen when alpha_RMSprop == 0");
-        float4 m0 = make_float4(0.f, 0.f, 0.f, 0.f), m1 = m0;
-        if (KM) { m0 = __ldcs(m4); m1 = __ldcs(m4 + 1); }
-        float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-        float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-        float mv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+        float tv[8], dv[8], mv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        ld8cs<V8>(th + j0, tv);
+        ld8cs<V8>(d + j0, dv);
+        if (KM) ld8cs<V8>(m + j0, mv);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
             float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
             if (WD && j0 + i < c.n_wd) gh = fmaf(c.wd, tv[i], gh);
             upd1<RMS>(gh, tv[i], dv[i], mv[i], c);
         }
-        __stcs(th4, make_float4(tv[0], tv[1], tv[2], tv[3]));
-        __stcs(th4 + 1, make_float4(tv[4], tv[5], tv[6], tv[7]));
-        __stcs(d4, make_float4(dv[0], dv[1], dv[2], dv[3]));
-        __stcs(d4 + 1, make_float4(dv[4], dv[5], dv[6], dv[7]));
-        if (KM) {
-            __stcs(m4, make_float4(mv[0], mv[1], mv[2], mv[3]));
-            __stcs(m4 + 1, make_float4(mv[4], mv[5], mv[6], mv[7]));
-        }
+        st8cs<V8>(th + j0, tv);
+        st8cs<V8>(d + j0, dv);
+        if (KM) st8cs<V8>(m + j0, mv);
     } else {
         for (int i = 0; i < 8 && j0 + i < n; ++i) {
             float gh = h2f(w[i >> 1], i & 1) * c.inv_ks;
@@ -280,6 +300,7 @@ __device__ __forceinline__ int dev_parity(const Dev1& dv) {
     return (int)((*reinterpret_cast<volatile const uint32_t*>(dv.epoch) + 1u) & 1u);
 }
 
+template <bool V8>
 __global__ void __launch_bounds__(kThreads) k_pack(const float* __restrict__ g, int64_t n,
                                                    int64_t n_pad, float s, uint16_t* __restrict__ h,
                                                    int64_t* st, Dev1 dv) {
@@ -291,7 +312,7 @@ __global__ void __launch_bounds__(kThreads) k_pack(const float* __restrict__ g, 
     for (int64_t v = gtid(); v < nv; v += gstride()) {
         const int64_t j0 = v << 3;
         float x[8];
-        load8_g(g, j0, n, x);
+        load8_g<V8>(g, j0, n, x);
         *reinterpret_cast<uint4*>(h + j0) = pack8(x, s, j0, first, sat);
     }
     flush_status(first, sat, st, ST_PACK_SAT);
@@ -307,7 +328,7 @@ __global__ void __launch_bounds__(kThreads) k_reduce_local(const uint16_t* __res
     if (st) flush_status(kNone, sat, st, ST_SUM_SAT);
 }
 
-template <bool RMS, bool WD, bool KM>
+template <bool RMS, bool WD, bool KM, bool V8>
 __global__ void LMSGD_LB(LMSGD_UPD_MINB) k_update(const uint16_t* __restrict__ R, int64_t n, UpdConst c,
                                                      float* __restrict__ th, float* __restrict__ d,
                                                      float* __restrict__ m, const int64_t* st,
@@ -334,13 +355,13 @@ __global__ void LMSGD_LB(LMSGD_UPD_MINB) k_update(const uint16_t* __restrict__ R
     for (int64_t v = gtid(); v < nv; v += gstride()) {
         const int64_t j0 = v << 3;
         const uint4 r = *reinterpret_cast<const uint4*>(R + j0);
-        update8<RMS, WD, KM>(r, j0, n, c, th, d, m);
+        update8<RMS, WD, KM, V8>(r, j0, n, c, th, d, m);
     }
 }
 
 // k = 1 single pass (LMSGD_FLAG_NO_SKIP): h = sat16(s g) kept in registers,
 // ghat = fp32(h) / s, update.  28 B/elem of HBM traffic.
-template <bool RMS, bool WD, bool KM>
+template <bool RMS, bool WD, bool KM, bool V8>
 __global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1(const float* __restrict__ g, int64_t n, float s,
                                                      UpdConst c, float* __restrict__ th,
                                                      float* __restrict__ d, float* __restrict__ m,
@@ -361,36 +382,31 @@ __global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1(const float* __restrict__ g,
     for (int64_t v = gtid(); v < nv; v += gstride()) {
         const int64_t j0 = v << 3;
         float x[8];
-        load8_g(g, j0, n, x);
+        load8_g<V8>(g, j0, n, x);
         const uint4 r = pack8(x, s, j0, first, sat);
-        update8<RMS, WD, KM>(r, j0, n, c, th, d, m);
+        update8<RMS, WD, KM, V8>(r, j0, n, c, th, d, m);
     }
     flush_status(first, sat, st, ST_PACK_SAT);
 }
 
 // Out-of-place variant of update8 (lmsgd_step_out_of_place): reads theta, Delta, m
 // from the *_in buffers and writes the new values to the *_out buffers.
-template <bool RMS>
+template <bool RMS, bool V8>
 __device__ __forceinline__ void update8_oop(uint4 r, int64_t j0, int64_t n, const UpdConst& c,
                                             const float* __restrict__ thi, const float* __restrict__ di,
                                             const float* __restrict__ mi, float* __restrict__ tho,
                                             float* __restrict__ dout, float* __restrict__ mo) {
     const uint32_t w[4] = {r.x, r.y, r.z, r.w};
     if (j0 + 8 <= n) {
-        const float4 t0 = __ldcs(reinterpret_cast<const float4*>(thi + j0)), t1 = __ldcs(reinterpret_cast<const float4*>(thi + j0) + 1);
-        const float4 d0 = __ldcs(reinterpret_cast<const float4*>(di + j0)), d1 = __ldcs(reinterpret_cast<const float4*>(di + j0) + 1);
-        const float4 m0 = __ldcs(reinterpret_cast<const float4*>(mi + j0)), m1 = __ldcs(reinterpret_cast<const float4*>(mi + j0) + 1);
-        float tv[8] = {t0.x, t0.y, t0.z, t0.w, t1.x, t1.y, t1.z, t1.w};
-        float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
-        float mv[8] = {m0.x, m0.y, m0.z, m0.w, m1.x, m1.y, m1.z, m1.w};
+        float tv[8], dv[8], mv[8];
+        ld8cs<V8>(thi + j0, tv);
+        ld8cs<V8>(di + j0, dv);
+        ld8cs<V8>(mi + j0, mv);
 #pragma unroll
         for (int i = 0; i < 8; ++i) upd1<RMS>(h2f(w[i >> 1], i & 1) * c.inv_ks, tv[i], dv[i], mv[i], c);
-        __stcs(reinterpret_cast<float4*>(tho + j0), make_float4(tv[0], tv[1], tv[2], tv[3]));
-        __stcs(reinterpret_cast<float4*>(tho + j0) + 1, make_float4(tv[4], tv[5], tv[6], tv[7]));
-        __stcs(reinterpret_cast<float4*>(dout + j0), make_float4(dv[0], dv[1], dv[2], dv[3]));
-        __stcs(reinterpret_cast<float4*>(dout + j0) + 1, make_float4(dv[4], dv[5], dv[6], dv[7]));
-        __stcs(reinterpret_cast<float4*>(mo + j0), make_float4(mv[0], mv[1], mv[2], mv[3]));
-        __stcs(reinterpret_cast<float4*>(mo + j0) + 1, make_float4(mv[4], mv[5], mv[6], mv[7]));
+        st8cs<V8>(tho + j0, tv);
+        st8cs<V8>(dout + j0, dv);
+        st8cs<V8>(mo + j0, mv);
     } else {
         for (int i = 0; i < 8 && j0 + i < n; ++i) {
             float t = thi[j0 + i], dd = di[j0 + i], mm = mi[j0 + i];
@@ -403,10 +419,10 @@ __device__ __forceinline__ void update8_oop(uint4 r, int64_t j0, int64_t n, cons
 // lmsgd_step_out_of_place, k = 1: the guarded step in ONE pass over the state (28 B/elem,
 // like k_fused1) -- the new state goes to separate buffers, so a non-finite gradient,
 // found only at the end, costs nothing but a repair copy (k_repair1).
-template <bool RMS>
 #ifndef LMSGD_OOP_LATE_TRIGGER
 #define LMSGD_OOP_LATE_TRIGGER 0
 #endif
+template <bool RMS, bool V8>
 __global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1_oop(const float* __restrict__ g, int64_t n, float s,
                                                          UpdConst c, const float* __restrict__ thi,
                                                          const float* __restrict__ di, const float* __restrict__ mi,
@@ -427,8 +443,8 @@ __global__ void LMSGD_LB(LMSGD_FUSED_MINB) k_fused1_oop(const float* __restrict_
     for (int64_t v = gtid(); v < nv; v += gstride()) {
         const int64_t j0 = v << 3;
         float x[8];
-        load8_g(g, j0, n, x);
-        update8_oop<RMS>(pack8(x, s, j0, first, sat), j0, n, c, thi, di, mi, tho, dout, mo);
+        load8_g<V8>(g, j0, n, x);
+        update8_oop<RMS, V8>(pack8(x, s, j0, first, sat), j0, n, c, thi, di, mi, tho, dout, mo);
     }
     flush_status(first, sat, st, ST_PACK_SAT);
     if (LMSGD_OOP_LATE_TRIGGER) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
@@ -872,7 +888,7 @@ __device__ __forceinline__ const uint16_t* r_src(const XArgs& x, bool localr, in
                   : reinterpret_cast<const uint16_t*>(x.peers.base[owner] + x.lay.off_R) + (gi << 3);
 }
 
-template <bool RMS, bool WD, bool KM, bool SIM, bool LOCALR>
+template <bool RMS, bool WD, bool KM, bool SIM, bool LOCALR, bool V8>
 __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
     // no griddepcontrol.wait: ordering with k_xstep1 is by the chunk flags.
     // kXUnits units per block (LMSGD_XUNITS): with one acquire per unit (chunk flags
@@ -957,7 +973,7 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
         if (j0v[v] >= x.n) continue;
         if (!LMSGD_XUPD_PREFETCH)
             rv[v] = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner[v], us[v] * kThreads + threadIdx.x));
-        update8<RMS, WD, KM>(rv[v], j0v[v], x.n, c, a.th, a.d, a.m);
+        update8<RMS, WD, KM, V8>(rv[v], j0v[v], x.n, c, a.th, a.d, a.m);
     }
 }
 
@@ -1125,16 +1141,30 @@ int grid_for(const Launch&, int64_t work_items) {
 
 // The update's kernel instantiation for a step: RMS (alpha_RMSprop != 0, or unknown
 // on the host in graph mode), WD (weight decay on), KM (m kept: not FREEZE_M).
-struct UpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_update<R, W, K>; } };
-struct Fused1K { template <bool R, bool W, bool K> static constexpr auto get() { return k_fused1<R, W, K>; } };
+struct UpdateK { template <bool R, bool W, bool K, bool V> static constexpr auto get() { return k_update<R, W, K, V>; } };
+struct Fused1K { template <bool R, bool W, bool K, bool V> static constexpr auto get() { return k_fused1<R, W, K, V>; } };
 template <bool SIM, bool LOCALR>
-struct XUpdateK { template <bool R, bool W, bool K> static constexpr auto get() { return k_xupdate<R, W, K, SIM, LOCALR>; } };
+struct XUpdateK {
+    template <bool R, bool W, bool K, bool V> static constexpr auto get() { return k_xupdate<R, W, K, SIM, LOCALR, V>; }
+};
 template <typename K>
-auto pick_variant(const UpdConst& c, bool graph) {
+auto pick_variant(const UpdConst& c, bool graph, bool v8) {
     const bool rms = c.a_rms != 0.0f || graph, wd = c.n_wd > 0, km = rms || !c.freeze_m;
-    if (rms) return wd ? K::template get<true, true, true>() : K::template get<true, false, true>();
-    if (km) return wd ? K::template get<false, true, true>() : K::template get<false, false, true>();
-    return wd ? K::template get<false, true, false>() : K::template get<false, false, false>();
+    if (v8) {
+        if (rms) return wd ? K::template get<true, true, true, true>() : K::template get<true, false, true, true>();
+        if (km) return wd ? K::template get<false, true, true, true>() : K::template get<false, false, true, true>();
+        return wd ? K::template get<false, true, false, true>() : K::template get<false, false, false, true>();
+    }
+    if (rms) return wd ? K::template get<true, true, true, false>() : K::template get<true, false, true, false>();
+    if (km) return wd ? K::template get<false, true, true, false>() : K::template get<false, false, true, false>();
+    return wd ? K::template get<false, true, false, false>() : K::template get<false, false, false, false>();
+}
+
+// 256-bit accesses need 32-byte aligned rows: every pointer of the launch (NULLs ignored)
+__host__ inline bool aligned32(std::initializer_list<const void*> ps) {
+    for (const void* p : ps)
+        if (p && (reinterpret_cast<uintptr_t>(p) & 31u)) return false;
+    return true;
 }
 
 // Launch with the programmatic-stream-serialization attribute (see pdl_enter).
@@ -1217,9 +1247,12 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const 
     } else {
         const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits) * nsim;
         const bool g = a.ctab != nullptr;
-        e = sim      ? launch_pdl_if(pdl, pick_variant<XUpdateK<true, false>>(a.c, g), grid, kThreads, s, a, sm)
-            : localr ? launch_pdl_if(pdl, pick_variant<XUpdateK<false, true>>(a.c, g), grid, kThreads, s, a, sm)
-                     : launch_pdl_if(pdl, pick_variant<XUpdateK<false, false>>(a.c, g), grid, kThreads, s, a, sm);
+        // the 256-bit variant needs every rank's state 32-byte aligned (a.v8: set by the caller
+        // over all ranks of an emulated group)
+        const bool v8 = a.v8 && aligned32({a.th, a.d, a.m});
+        e = sim      ? launch_pdl_if(pdl, pick_variant<XUpdateK<true, false>>(a.c, g, v8), grid, kThreads, s, a, sm)
+            : localr ? launch_pdl_if(pdl, pick_variant<XUpdateK<false, true>>(a.c, g, v8), grid, kThreads, s, a, sm)
+                     : launch_pdl_if(pdl, pick_variant<XUpdateK<false, false>>(a.c, g, v8), grid, kThreads, s, a, sm);
     }
     if (e != cudaSuccess) return e;
     return sim ? launch_pdl_if(true, k_xfinalize<true>, nsim, 32, s, a, sm, (unsigned int)per_rank)
@@ -1229,9 +1262,9 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const 
 
 int stream_blocks_per_sm() {
     int worst = 1 << 30, b = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update<true, false, true>, kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_update<true, false, true, false>, kThreads, 0);
     worst = b < worst ? b : worst;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true, false, true>, kThreads, 0);  // NOLINT
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k_fused1<true, false, true, false>, kThreads, 0);  // NOLINT
     worst = b < worst ? b : worst;
     return worst > 0 ? worst : 1;
 }
@@ -1243,7 +1276,8 @@ cudaError_t launch_status_reset(cudaStream_t s, int64_t* st) {
 
 cudaError_t launch_pack(cudaStream_t s, const Launch& L, const float* g, int64_t n, int64_t n_pad,
                         float scale, uint16_t* h, int64_t* st, const Dev1& dv) {
-    return launch_pdl(k_pack, grid_for(L, n_pad >> 3), kThreads, s, g, n, n_pad, scale, h, st, dv);
+    return launch_pdl(aligned32({g}) ? k_pack<true> : k_pack<false>, grid_for(L, n_pad >> 3), kThreads, s, g, n,
+                      n_pad, scale, h, st, dv);
 }
 
 cudaError_t launch_reduce_local(cudaStream_t s, const Launch& L, const uint16_t* h, int k,
@@ -1256,7 +1290,8 @@ cudaError_t launch_update(cudaStream_t s, const Launch& L, const uint16_t* R, in
                           int64_t* st_reset, int64_t* last, const Dev1& dv) {
     const int grid = grid_for(L, (n + 7) >> 3);
     // graph mode: alpha_RMSprop is only known on the device
-    return launch_pdl(pick_variant<UpdateK>(c, dv.epoch != nullptr), grid, kThreads, s, R, n, c, th, d, m, st,
+    return launch_pdl(pick_variant<UpdateK>(c, dv.epoch != nullptr, aligned32({th, d, m})), grid, kThreads, s, R, n,
+                      c, th, d, m, st,
                       st_reset, last, dv);
 }
 
@@ -1264,7 +1299,8 @@ cudaError_t launch_fused1(cudaStream_t s, const Launch& L, const float* g, int64
                           const UpdConst& c, float* th, float* d, float* m, int64_t* st,
                           int64_t* st_reset, int64_t* /*last: see launch_finalize_fused*/, const Dev1& dv) {
     const int grid = grid_for(L, (n + 7) >> 3);
-    return launch_pdl(pick_variant<Fused1K>(c, dv.epoch != nullptr), grid, kThreads, s, g, n, scale, c, th, d, m,
+    return launch_pdl(pick_variant<Fused1K>(c, dv.epoch != nullptr, aligned32({g, th, d, m})), grid, kThreads, s, g,
+                      n, scale, c, th, d, m,
                       st, st_reset, dv);
 }
 
@@ -1286,7 +1322,10 @@ cudaError_t launch_step_oop1(cudaStream_t s, const Launch& L, const float* g, in
                              float* dout, float* mo, int64_t* st, int64_t* st_reset, int64_t* last,
                              int64_t* trace) {
     const int grid = grid_for(L, (n + 7) >> 3);
-    cudaError_t e = launch_pdl(c.a_rms != 0.0f ? k_fused1_oop<true> : k_fused1_oop<false>, grid, kThreads, s, g, n,
+    const bool v8 = aligned32({g, thi, di, mi, tho, dout, mo});
+    cudaError_t e = launch_pdl(c.a_rms != 0.0f ? (v8 ? k_fused1_oop<true, true> : k_fused1_oop<true, false>)
+                                               : (v8 ? k_fused1_oop<false, true> : k_fused1_oop<false, false>),
+                               grid, kThreads, s, g, n,
                                scale, c, thi, di, mi, tho, dout, mo, st, st_reset, trace);
     if (e != cudaSuccess) return e;
 #ifndef LMSGD_REPAIR_BLOCKS

@@ -136,6 +136,8 @@ struct XStep {
     int64_t* cursor;         // graph mode: device index of the next step's coefficients
     uint16_t* rout;          // lmsgd_exchange: the caller's [n_pad] all-reduce output (k_xgather
                              // replaces k_xupdate); NULL for a step
+    int32_t v8;              // 1: the update may use 256-bit accesses if th/d/m are 32-byte aligned
+                             // (an emulated group sets it only if every rank's are)
 };
 // d_group / nsim: emulated-group mode (lmsgd_*_group): device array of the nsim ranks'
 // XStep, every rank's blocks in one launch per kernel; NULL for a real (one-rank) launch

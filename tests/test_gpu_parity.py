@@ -789,3 +789,56 @@ def test_out_of_place_skip_is_repaired_in_stream_order_and_fast():
     assert skipped < 12.0 * clean and skipped < 2000.0, (us, clean, skipped)
     L.lmsgd_finalize(oop)
     L.lmsgd_finalize(ref)
+
+
+@pytest.mark.parametrize("n", [1000, 100_003])
+def test_16_byte_aligned_buffers_match_32_byte_aligned(n):
+    """The streaming kernels use 256-bit accesses (LDG/STG.E.EF.ENL2.256) when every pointer
+    of a launch is 32-byte aligned and 128-bit ones otherwise (the ABI only requires 16-byte
+    alignment).  Both paths give bit-identical results: in-place guarded (k_pack + k_update),
+    in-place fused (k_fused1), out of place (k_fused1_oop), emulated world 2 (k_xupdate)."""
+    s = 1024.0
+    th0 = synth.theta0(n, None)
+    r = np.random.default_rng(n)
+    d0 = (r.standard_normal(n) * 1e-3).astype(np.float32)
+    m0 = (r.random(n) * 1e-6).astype(np.float32)
+    g = synth.grads(2, 3, n)
+    co = L.lmsgd_schedule_at(None, C1_C, 3)
+
+    def bufs(off):   # theta, Delta, m, g0, g1 at a float offset into fresh allocations
+        out = []
+        for x in (th0, d0, m0, g[0], g[1]):
+            b = torch.zeros(n + 8, device=DEV)
+            b[off:off + n] = dev(x)
+            out.append(b[off:off + n])
+        return out
+
+    results = []
+    for off in (0, 4):   # 0: 32-byte aligned (torch allocations are), 4: 16-byte only
+        a = bufs(off)
+        assert (a[0].data_ptr() % 32 == 0) == (off == 0)
+        out = {}
+        ctx = L.lmsgd_init(1, 0, 0, n, s)
+        th, d, m = (x.clone() for x in a[:3])
+        L.lmsgd_step(ctx, th, a[3], d, m, co)
+        out["guarded"] = (th, d, m)
+        ctxf = L.lmsgd_init(1, 0, 0, n, s, None, L.LMSGD_FLAG_NO_SKIP)
+        th, d, m = (x.clone() for x in a[:3])
+        L.lmsgd_step(ctxf, th, a[3], d, m, co)
+        out["fused"] = (th, d, m)
+        b = bufs(off)
+        ctxo = L.lmsgd_init(1, 0, 0, n, s)
+        L.lmsgd_step_out_of_place(ctxo, a[0], b[0], a[3], a[1], b[1], a[2], b[2], co)
+        out["oop"] = tuple(b[:3])
+        ctxs = [L.lmsgd_init(2, r_, 0, n, s) for r_ in range(2)]
+        L.lmsgd_connect_group(ctxs)
+        st2 = [[x.clone() for x in bufs(off)[:3]] for _ in range(2)]
+        L.lmsgd_step_group(ctxs, [x[0] for x in st2], [a[3], a[4]], [x[1] for x in st2], [x[2] for x in st2], co)
+        out["group"] = tuple(st2[0])
+        torch.cuda.synchronize()
+        for c_ in [ctx, ctxf, ctxo] + ctxs:
+            assert L.lmsgd_query_status(c_)[0] == 0
+            L.lmsgd_finalize(c_)
+        results.append({k: tuple(x.cpu() for x in v) for k, v in out.items()})
+    for k in results[0]:
+        assert all(torch.equal(x, y) for x, y in zip(results[0][k], results[1][k])), k
