@@ -1248,8 +1248,10 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const 
         const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kXUnits - 1) / kXUnits) * nsim;
         const bool g = a.ctab != nullptr;
         // the 256-bit variant needs every rank's state 32-byte aligned (a.v8: set by the caller
-        // over all ranks of an emulated group)
-        const bool v8 = a.v8 && aligned32({a.th, a.d, a.m});
+        // over all ranks of an emulated group); not with m frozen, where it measured slower
+        // at k > 1 (172.6 vs 169.7 us at k = 4, profiles/r2/ab/v8_xupdate.txt)
+        const bool frozen = a.c.freeze_m && a.c.a_rms == 0.0f && !g;
+        const bool v8 = a.v8 && aligned32({a.th, a.d, a.m}) && !frozen;
         e = sim      ? launch_pdl_if(pdl, pick_variant<XUpdateK<true, false>>(a.c, g, v8), grid, kThreads, s, a, sm)
             : localr ? launch_pdl_if(pdl, pick_variant<XUpdateK<false, true>>(a.c, g, v8), grid, kThreads, s, a, sm)
                      : launch_pdl_if(pdl, pick_variant<XUpdateK<false, false>>(a.c, g, v8), grid, kThreads, s, a, sm);
