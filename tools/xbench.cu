@@ -137,6 +137,38 @@ __global__ void __launch_bounds__(256) k_push_fenced(const float* __restrict__ g
     __threadfence_system();
 }
 
+// P with 16 elements per thread and ONE 32-byte remote store (st.global.v8.b32, sm_100) per
+// owner per thread, the g loads as two 256-bit loads; persistent, one fence per block
+__global__ void __launch_bounds__(256) k_push32(const float* __restrict__ g, uint16_t* const* recv, int world,
+                                                int rank, int64_t shard, int64_t n) {
+    const int64_t gsh = shard >> 4;                     // 16-element groups per shard
+    const int64_t ups = (gsh + 255) / 256;
+    for (int64_t us = blockIdx.x; us < ups * world; us += gridDim.x) {
+        const int owner = (int)((us % world + rank) % world);
+        const int64_t gi = (us / world) * 256 + threadIdx.x;
+        if (gi >= gsh) continue;
+        const int64_t j0 = ((int64_t)owner * shard) + (gi << 4);
+        float xa[8], xb[8];
+        if (j0 + 16 <= n) {
+            asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=f"(xa[0]), "=f"(xa[1]), "=f"(xa[2]), "=f"(xa[3]), "=f"(xa[4]), "=f"(xa[5]), "=f"(xa[6]),
+                           "=f"(xa[7]) : "l"(g + j0));
+            asm volatile("ld.global.cs.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                         : "=f"(xb[0]), "=f"(xb[1]), "=f"(xb[2]), "=f"(xb[3]), "=f"(xb[4]), "=f"(xb[5]), "=f"(xb[6]),
+                           "=f"(xb[7]) : "l"(g + j0 + 8));
+        } else {
+            load8_g(g, j0, n, xa);
+            load8_g(g, j0 + 8, n, xb);
+        }
+        int64_t first = kNone; unsigned sat = 0;
+        const uint4 pa = pack8(xa, 1024.f, j0, first, sat), pb = pack8(xb, 1024.f, j0 + 8, first, sat);
+        uint16_t* dst = recv[owner] + (int64_t)rank * shard + (gi << 4);
+        asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(pa.x), "r"(pa.y),
+                     "r"(pa.z), "r"(pa.w), "r"(pb.x), "r"(pb.y), "r"(pb.z), "r"(pb.w) : "memory");
+    }
+    __threadfence_system();
+}
+
 // P with 16 elements per thread (two 16-B stores per owner per thread)
 __global__ void __launch_bounds__(256) k_push16(const float* __restrict__ g, uint16_t* const* recv, int world,
                                                 int rank, int64_t shard, int64_t n) {
@@ -324,6 +356,8 @@ int main(int argc, char** argv) {
         const double pb = 2.0 * n_pad * (W - 1) / W;
         run("P persistent 148x6, one fence/block", pb, [&](int i) { xb::k_push_fenced<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
         run("P persistent 148x6, 16 elem/thread", pb, [&](int i) { xb::k_push16<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n); });
+        run("P persistent 148x8, 32-B remote stores", pb, [&](int i) { xb::k_push32<<<sms * 8, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n); });
+        run("P persistent 148x4, 32-B remote stores", pb, [&](int i) { xb::k_push32<<<sms * 4, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n); });
         run("P persistent 148x8, one fence/block", pb, [&](int i) { xb::k_push_fenced<<<sms * 8, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
         run("P persistent 148x4, one fence/block", pb, [&](int i) { xb::k_push_fenced<<<sms * 4, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
         run("update pull, R by one bulk copy per block", 26.0 * n, [&](int i) { xb::k_upd_pull_bulk<<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
