@@ -134,13 +134,16 @@ lmsgd::Launch launch_for_current_device() {
     lmsgd::Launch L{};
     cudaDeviceGetAttribute(&L.sm_count, cudaDevAttrMultiProcessorCount, dev);
     L.grid_cap_stream = L.sm_count * lmsgd::stream_blocks_per_sm();
-    L.grid_xstep = L.sm_count * lmsgd::xstep_blocks_per_sm();
+    {
+        const int occ = lmsgd::xstep_blocks_per_sm(), bps = lmsgd::xstep_default_bps();
+        L.grid_xstep = L.sm_count * (bps < occ ? bps : occ);
+    }
     // diagnostics: fewer k_xstep1 blocks per SM, leaving slots for k_xupdate blocks to be
     // resident early -- measured slower (k = 4: 205.0 / 207.8 us at 6 / 4 vs 203.9 us at 8,
     // profiles/r1/ab/xstep_grid_n4.txt)
     if (const char* b = std::getenv("LMSGD_XSTEP_BPS")) {
         const int bps = std::atoi(b);
-        if (bps > 0 && bps < lmsgd::xstep_blocks_per_sm()) L.grid_xstep = L.sm_count * bps;
+        if (bps > 0 && bps <= lmsgd::xstep_blocks_per_sm()) L.grid_xstep = L.sm_count * bps;
     }
     // PDL on the k = 1 pair: 128.7 vs 132.3 us (the world > 1 step uses it internally).
     L.pdl_mask = 0x1;

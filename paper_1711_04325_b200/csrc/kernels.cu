@@ -30,7 +30,7 @@ constexpr int kThreads = 256;   // LMSGD_LB below spells the same block size
 #define LMSGD_XUNITS 2   // A/B at k = 4 (profiles/r1/ab/xunits_n4.txt): 201.9 vs 206.8 us per step with 1
 #endif
 constexpr int kXUnits = LMSGD_XUNITS;   // k_xupdate: 2048-element units per block
-enum { FLAG_A = 0, FLAG_C = 2, FLAG_D = 3 };  // A: a rank's pack+push is done; C: BN staged;
+enum { FLAG_A = 0, FLAG_B = 1, FLAG_C = 2, FLAG_D = 3 };  // A / B: a rank's phase 0 / 1 push is done; C: BN staged;
                                              // D (local): this step's skip decision is stored
 
 // Minimum resident blocks per SM asked of ptxas (register caps), A/B knobs set with
@@ -648,11 +648,18 @@ __device__ __forceinline__ bool spin_flag(const XArgs& x, const Ep& ep, const ui
 // consumer then needs one acquire load (no separate wait for flag D and no status
 // reads before its update).  The value is exactly 2 e or 2 e + 1 once ready: the next
 // step's reduce cannot publish before every rank has finished this step's update.
+// Polling backs off exponentially from 32 ns to LMSGD_CFLAG_BACKOFF ns, so that update
+// blocks resident long before their chunk (the phased k_xstep1) do not flood L2 with polls.
+#ifndef LMSGD_CFLAG_BACKOFF
+#define LMSGD_CFLAG_BACKOFF 32
+#endif
 __device__ __forceinline__ bool spin_cflag(const XArgs& x, const Ep& ep, const uint32_t* f, uint32_t& v) {
     const uint64_t t0 = globaltimer();
     const uint32_t want = ep.e << 1;
+    unsigned ns = 32;
     while ((int32_t)((v = ld_acquire_sys(f)) - want) < 0) {
-        __nanosleep(32);
+        __nanosleep(ns);
+        ns = ns < LMSGD_CFLAG_BACKOFF ? 2 * ns : ns;
         if ((int64_t)(globaltimer() - t0) > x.timeout_ns) return false;
     }
     return true;
@@ -694,6 +701,24 @@ __device__ __forceinline__ uint32_t cflag_value(const XArgs& x, const Ep& ep) {
 // this rank's shard into R; 2 = as 1, and the reduced shard is multicast (multimem.st) back
 // into every rank's wire in place, so every rank then holds the whole all-reduce result
 // locally.
+// LMSGD_XPHASES (A/B knob, 1): the shard's units split at chunk boundaries into this many
+// phases, each pushed, barriered and reduced in turn, so that k_xupdate (launched behind
+// this kernel with programmatic dependent launch, on the SMs left free: LMSGD_XSTEP_BPS
+// blocks per SM) updates phase 0's chunks while phase 1 is pushed.  The update is in
+// place, so the global skip decision must precede it: phase 0 then also scans the later
+// phases' gradient for non-finite values.  tools/xbench.cu suggested the overlap (push ||
+// update 134 us against 70 + 99 us serial at k = 4), but in the step two phases measured
+// 242-294 us against 203 us (k = 4, 2-6 blocks per SM, with or without backed-off flag
+// polling; profiles/r2/ab/phases_n4.txt): the second barrier, the scan and the push with
+// fewer blocks beside a busy update cost more than the overlap saves.  Parity-tested at 2.
+#ifndef LMSGD_XPHASES
+#define LMSGD_XPHASES 1
+#endif
+static_assert(LMSGD_XPHASES == 1 || LMSGD_XPHASES == 2, "phase flags: A (phase 0) and B (phase 1)");
+// k_xstep1 blocks per SM (the rest of each SM is left to k_xupdate when the phases overlap)
+#ifndef LMSGD_XSTEP_BPS_DEFAULT
+#define LMSGD_XSTEP_BPS_DEFAULT (LMSGD_XPHASES > 1 ? 2 : 8)
+#endif
 template <bool SIM, int NV>
 __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
     static_assert(!(SIM && NV), "NVLS needs one GPU per rank");
@@ -704,95 +729,28 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
     const XArgs& x = a.x;
     const Ep ep = get_ep(x);
     __shared__ int s_ok;
+    __shared__ uint32_t s_fv;   // this step's chunk-flag value (thread 0; 0 = not read yet)
     const bool t0 = threadIdx.x == 0;
+    if (t0) s_fv = 0;
     if (G.b() == 0 && t0) stamp(x, TR_PACK_START);
     const int64_t gsh = x.lay.shard >> 3;
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
     int64_t* mine = status_of(x, ep, x.rank);
-
-    // ---- 1. pack + push (16-byte SM stores to the owners; pushing each packed unit as
-    //         one 4 KB cp.async.bulk from shared memory instead measured the same, 66.2
-    //         vs 65.4 us at k = 4: the all-to-all is NVLink-bound at ~575 GB/s per
-    //         direction, profiles/r1/ab/push_bulk_n4.txt)
-    {
-        int64_t first = kNone;
-        unsigned sat = 0;
-        const int64_t units = (int64_t)x.world * ups;
-        for (int64_t u = G.b(); u < units; u += G.g()) {
-            int owner;
-            int64_t gi;
-            if (!map_unit(x, u, owner, gi)) continue;
-            const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
-            float xv[8];
-            load8_g(a.g, j0, x.n, xv);
-            uint16_t* dst = NV ? reinterpret_cast<uint16_t*>(x.nv_uc) + j0   // own wire, [n_pad] layout
-                               : reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
-                                     (int64_t)x.rank * x.lay.shard + (gi << 3);
-            *reinterpret_cast<uint4*>(dst) = pack8(xv, a.scale, j0, first, sat);
-        }
-        flush_status(first, sat, mine, ST_PACK_SAT);
-    }
-    // this block's pushes and status atomics, then its ticket: bar.sync + one thread's
-    // system fence (cumulativity; the grid-sync pattern)
-    __syncthreads();
-    if (t0) __threadfence_system();
-    if (t0 && atomicAdd(a.ctr + 0, 1u) + 1u == G.g()) {
-        a.ctr[0] = 0;
-        stamp(x, TR_PACK_END);
-        publish(x, ep, FLAG_A);
-        stamp(x, TR_PUB_END);
-    }
-
-    // ---- 2. all ranks packed; block 0 makes the global skip decision (identical on
-    //         every rank) and releases the local flag D.  The reduce does not need it.
-    if (threadIdx.x < 32) {
-        const bool ok = warp_wait_all(x, ep, FLAG_A, G.b() == 0);
-        if (t0) s_ok = ok ? 1 : 0;
-    }
-    __syncthreads();
-    if (G.b() == 0) {
-        __shared__ int64_t s_st[3 * LMSGD_MAX_WORLD];
-        if (threadIdx.x < x.world) {   // every rank's final pack words, read in parallel
-            const volatile int64_t* sp = status_of(x, ep, threadIdx.x);
-            s_st[3 * threadIdx.x] = sp[ST_FIRST];
-            s_st[3 * threadIdx.x + 1] = sp[ST_PACK_SAT];
-            s_st[3 * threadIdx.x + 2] = sp[ST_ERROR];
-        }
-        __syncthreads();
-        if (t0) {
-            int64_t gfirst = kNone, psat = 0, err = s_ok ? 0 : (int64_t)LMSGD_ERR_TIMEOUT;
-            for (int p = 0; p < x.world; ++p) {
-                gfirst = s_st[3 * p] < gfirst ? s_st[3 * p] : gfirst;
-                psat += s_st[3 * p + 1];
-                err = err ? err : s_st[3 * p + 2];
-            }
-            mine[ST_G_FIRST] = gfirst;
-            mine[ST_G_PACK_SAT] = psat;
-            mine[ST_G_ERROR] = err;
-            int64_t* nxt = reinterpret_cast<int64_t*>(x.peers.base[x.rank] + x.lay.off_status) +
-                           (ep.par ^ 1) * ST_WORDS;   // next step's slot: every rank has read it
-            for (int w = 0; w < ST_WORDS; ++w) nxt[w] = (w == ST_FIRST || w == ST_G_FIRST) ? kNone : 0;
-            __threadfence();
-            asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag_slot(x, x.rank, FLAG_D)), "r"(ep.e)
-                         : "memory");
-            stamp(x, TR_RED_START);
-        }
-    }
-    if (!s_ok) {
-        if (t0) atomicAdd(a.ctr + 1, 1u);
-        return;
-    }
-
-    // ---- 3. exact reduce of this rank's shard, chunk-major over blocks (unit u on
-    //         block u % grid); a chunk is released when the last block holding one of
-    //         its units has finished all its units.
-    //         Runs even for a step that will be skipped (its R is then never read).
-    if (G.b() == 0 && t0) stamp(x, TR_RED_GO);
     const uint16_t* recv = reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv);
     uint16_t* R = reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R);
-    unsigned sat = 0;
-    __shared__ uint32_t s_fv;   // this step's chunk-flag value (thread 0; 0 = not read yet)
-    if (t0) s_fv = 0;
+    // phase p covers the shard units [ulo(p), ulo(p + 1)), chunk-aligned (identical on every rank)
+    const int nph = x.lay.nchunks >= LMSGD_XPHASES ? LMSGD_XPHASES : 1;
+    auto ulo = [&](int p) -> int64_t {
+        const int64_t u = ((int64_t)x.lay.nchunks * p / nph) * x.lay.cu;
+        return u < ups ? u : ups;
+    };
+    // unit u of a phase's all-owner sweep: owner-interleaved (unit u -> owner (u + rank) % world)
+    // so that every rank's blocks in flight touch all owners evenly; -1 past the shard
+    auto sweep = [&](int64_t lo, int64_t u, int& owner) -> int64_t {
+        owner = (int)((u % x.world + x.rank) % x.world);
+        const int64_t gi = (lo + u / x.world) * kThreads + threadIdx.x;
+        return gi < gsh ? gi : -1;
+    };
     // thread 0, after a bar.sync and a system fence that order this block's R writes of
     // unit u (cumulativity): count the unit into its chunk; the block completing a chunk
     // releases it to every rank (cflag[c][rank] = 2 epoch + skip)
@@ -810,71 +768,140 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
             for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, c, x.rank), s_fv);
         }
     };
-    // LMSGD_RED_PER_ROUND (A/B knob, off): release after every round of units (bar.sync,
-    // then ONE thread's system fence -- the grid-sync pattern), so the update starts on the
-    // first chunks while later rounds are reduced.  Measured at k = 4 (round 2,
-    // profiles/r2/ab/reduce_release_n4.txt): the update blocks then start 16 us earlier
-    // but compete with the reduce for HBM (block 0's reduce 12 -> 60 us, update 92 ->
-    // 111 us) -- step 206.3 vs 204.5 us; the 32-register cap also spills the fp64
-    // accumulators.  Default: one fence per block after all its units.
-#ifndef LMSGD_RED_PER_ROUND
-#define LMSGD_RED_PER_ROUND 0
-#endif
-    // (the same per-round release for lmsgd_exchange, whose consumer is k_xgather's pull,
-    // measured slower too: k = 4 187 vs 180 us, k = 2 174 vs 148 us per exchange,
-    // profiles/r2/ab/exchange_release.txt)
-    constexpr bool per_round = LMSGD_RED_PER_ROUND;
-    if (NV) {
-        // this shard's 8-element groups summed by the switch over every rank's wire,
-        // NVU units per trip with all their ld_reduce issued first (more bytes in flight)
-        constexpr int NVU = 2;
-        for (int64_t u0 = G.b(); u0 < ups; u0 += NVU * G.g()) {
-            uint4 v[NVU];
-            int64_t off[NVU];
-#pragma unroll
-            for (int i = 0; i < NVU; ++i) {
-                const int64_t gi = (u0 + i * G.g()) * kThreads + threadIdx.x;
-                off[i] = gi < gsh ? ((int64_t)x.rank * x.lay.shard + (gi << 3)) * 2 : -1;
-                if (off[i] >= 0) v[i] = mm_ld_reduce_f16x8(x.nv_mc + off[i]);
+
+    for (int ph = 0; ph < nph; ++ph) {
+        const int64_t lo = ulo(ph), hi = ulo(ph + 1);
+        // ---- 1. pack + push of this phase's units (16-byte SM stores to the owners;
+        //         pushing each packed unit as one 4 KB cp.async.bulk, or 32-byte stores,
+        //         measured the same: the all-to-all is NVLink-bound)
+        {
+            int64_t first = kNone;
+            unsigned sat = 0;
+            const int64_t units = (int64_t)x.world * (hi - lo);
+            for (int64_t u = G.b(); u < units; u += G.g()) {
+                int owner;
+                const int64_t gi = sweep(lo, u, owner);
+                if (gi < 0) continue;
+                const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+                float xv[8];
+                load8_g(a.g, j0, x.n, xv);
+                uint16_t* dst = NV ? reinterpret_cast<uint16_t*>(x.nv_uc) + j0   // own wire, [n_pad] layout
+                                   : reinterpret_cast<uint16_t*>(x.peers.base[owner] + x.lay.off_recv) +
+                                         (int64_t)x.rank * x.lay.shard + (gi << 3);
+                *reinterpret_cast<uint4*>(dst) = pack8(xv, a.scale, j0, first, sat);
             }
+            if (ph == 0 && nph > 1) {   // the later phases' gradient: finiteness only
+                const int64_t units2 = (int64_t)x.world * (ups - hi);
+                for (int64_t u = G.b(); u < units2; u += G.g()) {
+                    int owner;
+                    const int64_t gi = sweep(hi, u, owner);
+                    if (gi < 0) continue;
+                    const int64_t j0 = ((int64_t)owner * gsh + gi) << 3;
+                    float xv[8];
+                    load8_g(a.g, j0, x.n, xv);
 #pragma unroll
-            for (int i = 0; i < NVU; ++i) {
-                if (off[i] < 0) continue;
-                v[i].x = sat_inf_f16x2(v[i].x, sat); v[i].y = sat_inf_f16x2(v[i].y, sat);
-                v[i].z = sat_inf_f16x2(v[i].z, sat); v[i].w = sat_inf_f16x2(v[i].w, sat);
-                if (NV == 2) mm_st_16B(x.nv_mc + off[i], v[i]);   // into every rank's wire, in place
-                else *reinterpret_cast<uint4*>(R + (off[i] / 2 - (int64_t)x.rank * x.lay.shard)) = v[i];
-            }
-            if constexpr (per_round) {
-                if (u0 + NVU * G.g() >= ups) flush_status(kNone, sat, mine, ST_SUM_SAT);   // before the last release
-                __syncthreads();
-                if (t0) {
-                    __threadfence_system();
-                    for (int i = 0; i < NVU; ++i)
-                        if (u0 + i * G.g() < ups) count_unit(u0 + i * G.g());
+                    for (int i = 0; i < 8; ++i)
+                        if (nonfinite(xv[i]) && j0 + i < first) first = j0 + i;
                 }
             }
+            flush_status(first, sat, mine, ST_PACK_SAT);
         }
-    } else {
-        for (int64_t u = G.b(); u < ups; u += G.g()) {
-            const int64_t gi = u * kThreads + threadIdx.x;
-            if (gi < gsh) reduce8(recv, x.lay.shard, x.world, gi << 3, R, sat);
-            if constexpr (per_round) {
-                if (u + G.g() >= ups) flush_status(kNone, sat, mine, ST_SUM_SAT);   // before the last release
-                __syncthreads();
-                if (t0) {
-                    __threadfence_system();
-                    count_unit(u);
-                }
-            }
-        }
-    }
-    if constexpr (!per_round) {
-        flush_status(kNone, sat, mine, ST_SUM_SAT);
-        __threadfence_system();
+        // this block's pushes and status atomics, then its ticket: bar.sync + one thread's
+        // system fence (cumulativity; the grid-sync pattern); flag A (phase 0) or B
+        const int which = ph == 0 ? FLAG_A : FLAG_B;
+        unsigned int* tk = a.ctr + (ph == 0 ? 0 : 2);
         __syncthreads();
-        if (t0)
-            for (int64_t u = G.b(); u < ups; u += G.g()) count_unit(u);
+        if (t0) __threadfence_system();
+        if (t0 && atomicAdd(tk, 1u) + 1u == G.g()) {
+            *tk = 0;
+            if (ph == 0) stamp(x, TR_PACK_END);
+            publish(x, ep, which);
+            if (ph == 0) stamp(x, TR_PUB_END);
+        }
+
+        // ---- 2. all ranks pushed this phase; after phase 0 block 0 makes the global skip
+        //         decision (every rank's first non-finite index is final: phase 0 scanned
+        //         the rest) and releases the local flag D.  The reduce does not need it.
+        if (threadIdx.x < 32) {
+            const bool ok = warp_wait_all(x, ep, which, G.b() == 0 && ph == 0);
+            if (t0) s_ok = ok ? 1 : 0;
+        }
+        __syncthreads();
+        if (ph == 0 && G.b() == 0) {
+            __shared__ int64_t s_st[2 * LMSGD_MAX_WORLD];
+            if (threadIdx.x < x.world) {   // every rank's first index and error, read in parallel
+                const volatile int64_t* sp = status_of(x, ep, threadIdx.x);
+                s_st[2 * threadIdx.x] = sp[ST_FIRST];
+                s_st[2 * threadIdx.x + 1] = sp[ST_ERROR];
+            }
+            __syncthreads();
+            if (t0) {
+                int64_t gfirst = kNone, err = s_ok ? 0 : (int64_t)LMSGD_ERR_TIMEOUT;
+                for (int p = 0; p < x.world; ++p) {
+                    gfirst = s_st[2 * p] < gfirst ? s_st[2 * p] : gfirst;
+                    err = err ? err : s_st[2 * p + 1];
+                }
+                mine[ST_G_FIRST] = gfirst;
+                mine[ST_G_ERROR] = err;
+                int64_t* nxt = reinterpret_cast<int64_t*>(x.peers.base[x.rank] + x.lay.off_status) +
+                               (ep.par ^ 1) * ST_WORDS;   // next step's slot: every rank has read it
+                for (int w = 0; w < ST_WORDS; ++w) nxt[w] = (w == ST_FIRST || w == ST_G_FIRST) ? kNone : 0;
+                __threadfence();
+                asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag_slot(x, x.rank, FLAG_D)), "r"(ep.e)
+                             : "memory");
+                stamp(x, TR_RED_START);
+            }
+        }
+        if (!s_ok) {
+            if (t0) atomicAdd(a.ctr + 1, 1u);
+            return;
+        }
+
+        // ---- 3. exact reduce of this phase's units of the own shard (unit u on block
+        //         u % grid); a chunk is released when the last block holding one of its
+        //         units has finished all its units of the phase.  Runs even for a step
+        //         that will be skipped (its R is then never read).
+        if (ph == 0 && G.b() == 0 && t0) stamp(x, TR_RED_GO);
+        unsigned sat = 0;
+        if (NV) {
+            // this shard's 8-element groups summed by the switch over every rank's wire,
+            // NVU units per trip with all their ld_reduce issued first (more bytes in flight)
+            constexpr int NVU = 2;
+            for (int64_t u0 = lo + G.b(); u0 < hi; u0 += NVU * G.g()) {
+                uint4 v[NVU];
+                int64_t off[NVU];
+#pragma unroll
+                for (int i = 0; i < NVU; ++i) {
+                    const int64_t su = u0 + i * G.g();
+                    const int64_t gi = su * kThreads + threadIdx.x;
+                    off[i] = (su < hi && gi < gsh) ? ((int64_t)x.rank * x.lay.shard + (gi << 3)) * 2 : -1;
+                    if (off[i] >= 0) v[i] = mm_ld_reduce_f16x8(x.nv_mc + off[i]);
+                }
+#pragma unroll
+                for (int i = 0; i < NVU; ++i) {
+                    if (off[i] < 0) continue;
+                    v[i].x = sat_inf_f16x2(v[i].x, sat); v[i].y = sat_inf_f16x2(v[i].y, sat);
+                    v[i].z = sat_inf_f16x2(v[i].z, sat); v[i].w = sat_inf_f16x2(v[i].w, sat);
+                    if (NV == 2) mm_st_16B(x.nv_mc + off[i], v[i]);   // into every rank's wire, in place
+                    else *reinterpret_cast<uint4*>(R + (off[i] / 2 - (int64_t)x.rank * x.lay.shard)) = v[i];
+                }
+            }
+        } else {
+            for (int64_t su = lo + G.b(); su < hi; su += G.g()) {
+                const int64_t gi = su * kThreads + threadIdx.x;
+                if (gi < gsh) reduce8(recv, x.lay.shard, x.world, gi << 3, R, sat);
+            }
+        }
+        flush_status(kNone, sat, mine, ST_SUM_SAT);
+        // one system fence per block (one thread, after bar.sync), then count this block's
+        // units of the phase into their chunks.  (Releasing after every round of units
+        // measured slower: the early update blocks compete with the reduce for HBM,
+        // profiles/r2/ab/reduce_release_n4.txt.)
+        __syncthreads();
+        if (t0) {
+            __threadfence_system();
+            for (int64_t su = lo + G.b(); su < hi; su += G.g()) count_unit(su);
+        }
     }
     if (G.b() == 0 && t0) stamp(x, TR_RED_END);
 
@@ -1060,10 +1087,15 @@ __global__ void k_xfinalize(XStep a_, Sim sim, unsigned int xstep1_blocks) {
     int64_t err = mine[ST_G_ERROR];
     if (!err && a.ctab && *a.cursor >= a.ctab_count) err = (int64_t)LMSGD_ERR_RANGE;   // table exhausted
     const bool skip = gfirst != kNone || err != 0;
-    int64_t ssat = 0;
-    if (!skip)
-        for (int p = 0; p < x.world; ++p) ssat += static_cast<const volatile int64_t*>(status_of(x, ep, p))[ST_SUM_SAT];
-    store_last(a.last, gfirst, mine[ST_G_PACK_SAT], ssat, err, skip);
+    // every rank's phases have been pushed and reduced by now: its pack and sum saturation
+    // counts are final (a skipped step reports no sum saturations)
+    int64_t ssat = 0, psat = 0;
+    for (int p = 0; p < x.world; ++p) {
+        const volatile int64_t* sp = status_of(x, ep, p);
+        psat += sp[ST_PACK_SAT];
+        if (!skip) ssat += sp[ST_SUM_SAT];
+    }
+    store_last(a.last, gfirst, psat, ssat, err, skip);
     stamp(x, TR_UPD_END);
     // the step is complete on this GPU: advance the device step counter (and cursor)
     if (a.cursor) *a.cursor += 1;
@@ -1187,6 +1219,8 @@ cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), int grid, int bloc
 
 
 
+int xstep_default_bps() { return LMSGD_XSTEP_BPS_DEFAULT; }
+
 int xstep_blocks_per_sm(bool sim) {
     int b = 0;
     // every instantiation shares the grid size: take the smallest occupancy
@@ -1215,7 +1249,9 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const 
     if (!sim) nsim = 1;
     const Sim sm{d_group, nsim};
     // per-rank k_xstep1 grid: all nsim grids co-resident
-    const int per_rank = sim ? (L.sm_count * xstep_blocks_per_sm(true)) / nsim : L.grid_xstep;
+    const int bps_sim = xstep_blocks_per_sm(true) < LMSGD_XSTEP_BPS_DEFAULT ? xstep_blocks_per_sm(true)
+                                                                          : LMSGD_XSTEP_BPS_DEFAULT;
+    const int per_rank = sim ? (L.sm_count * bps_sim) / nsim : L.grid_xstep;
     XStep arg = a;
     cudaError_t e;
     {

@@ -143,7 +143,8 @@ struct XStep {
 // XStep, every rank's blocks in one launch per kernel; NULL for a real (one-rank) launch
 cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const XStep* d_group = nullptr,
                          int nsim = 1);
-int xstep_blocks_per_sm(bool sim = false);
+int xstep_blocks_per_sm(bool sim = false);   // occupancy of k_xstep1 (all co-resident)
+int xstep_default_bps();                      // blocks per SM it is launched with by default
 
 struct BnArgs {
     XArgs x;
