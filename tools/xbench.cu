@@ -364,6 +364,16 @@ int main(int argc, char** argv) {
     run("update pull, R via ld.global.nc", 26.0 * n, [&](int i) { xb::k_upd_pull_nc<<<W * ups, 256, 0, st[i]>>>(P, W, i, shard, n, c, th[i], d[i], m[i]); });
         run("P persistent 148x6, fence/unit", pb, [&](int i) { xb::k_push_fenced<<<sms * 6, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1); });
         run("P persistent 148x2, fence/unit", pb, [&](int i) { xb::k_push_fenced<<<sms * 2, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1); });
+        for (int pb_ = 1; pb_ <= 4; pb_ *= 2)   // pipelining potential: the push (one fence per block) || the update
+            run(pb_ == 1 ? "P 148x1 one fence || local update (2 streams)" : pb_ == 2 ? "P 148x2 one fence || local update (2 streams)"
+                                                                       : "P 148x4 one fence || local update (2 streams)",
+                26.0 * n, [&](int i) {
+                    cudaEvent_t ev; cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+                    xb::k_push_fenced<<<sms * pb_, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0);
+                    launch_update(st2[i], L, full[i], n, c, th[i], d[i], m[i], nullptr, nullptr, nullptr);
+                    cudaEventRecord(ev, st2[i]); cudaStreamWaitEvent(st[i], ev, 0); cudaEventDestroy(ev); });
+        run("P 148x1 one fence alone", pb, [&](int i) { xb::k_push_fenced<<<sms * 1, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
+        run("P 148x2 one fence alone", pb, [&](int i) { xb::k_push_fenced<<<sms * 2, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 0); });
         run("P 148x2 fence/unit || local update (2 streams)", 26.0 * n, [&](int i) {
             cudaEvent_t ev; cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
             xb::k_push_fenced<<<sms * 2, 256, 0, st[i]>>>(g[i], recvp[i], W, i, shard, n, 1);
