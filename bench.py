@@ -647,6 +647,22 @@ def main():
             nvlink["nvml_counters_error"] = counters.err
         if nvls_ok:
             L.lmsgd_nvls_mode(ctx, NV_MODES[args.nvls])
+        # phases of the exchange alone (in-kernel stamps, medians, max over ranks):
+        # pack+push, the wait for every rank's push, the reduce, and the all-gather pull
+        # (k_xgather) up to the status record
+        import statistics
+        L.lmsgd_trace_enable(ctx, 50)
+        for _ in range(50):
+            L.lmsgd_exchange(ctx, grads, rout)
+        tr = L.lmsgd_trace_read(ctx, 50)
+        L.lmsgd_trace_enable(ctx, 0)
+        xsegs = {"pack_push": ("pack_start", "pack_end"), "wait_all_pushes": ("pack_end", "reduce_start"),
+                 "reduce": ("reduce_go", "reduce_end"), "gather_after_reduce": ("reduce_end", "update_end"),
+                 "exchange": ("pack_start", "update_end")}
+        mine_x = {k_: statistics.median((t[b] - t[a]) / 1e3 for t in tr[10:]) for k_, (a, b) in xsegs.items()}
+        allx = [None] * world
+        dist.all_gather_object(allx, mine_x)
+        nvlink["exchange_trace_us"] = {k_: max(r[k_] for r in allx) for k_ in xsegs}
         nvlink["modes"] = per_mode
         nvlink["algorithmic_link_bytes_per_gpu"] = {
             "off": {"tx": 2 * push_alg, "rx": 2 * push_alg,
