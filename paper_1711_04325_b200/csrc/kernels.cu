@@ -1015,6 +1015,10 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
 // profiles/r1/ab/gather_units_n4.txt): the pull is NVLink-bound (~600 GB/s in).  The
 // exchange moves 2 x 2 N (k-1)/k bytes out of every GPU (push, then R served to the
 // peers), 76.7 MB at k = 4: 118 us at the ~650 GB/s an SM store stream reaches.
+#ifndef LMSGD_XGATHER_UNITS
+#define LMSGD_XGATHER_UNITS 1   // units per k_xgather block (A/B knob)
+#endif
+constexpr int kGUnits = LMSGD_XGATHER_UNITS;
 template <bool SIM, bool LOCALR>
 __global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
     __shared__ XStep s_a;
@@ -1024,27 +1028,48 @@ __global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
     const int64_t gsh = x.lay.shard >> 3;
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
     const int64_t kcu = (int64_t)x.world * x.lay.cu;
-    const int64_t i = Grid<SIM>{sim}.b();
-    const int c = (int)(i / kcu);
-    const int64_t r = i - (int64_t)c * kcu;
-    const int owner = (int)((r % x.world + x.rank) % x.world);
-    const int64_t u = c < x.lay.nchunks ? (int64_t)c * x.lay.cu + r / x.world : ups;
+    // kGUnits consecutive units of the chunk-major, owner-interleaved order per block; lane
+    // v of warp 0 waits for unit v's chunk flag (the waits overlap), then every thread
+    // issues its units' peer loads before the local stores
+    auto unit_of = [&](int v, int& owner, int64_t& u, int& c) {
+        const int64_t i = Grid<SIM>{sim}.b() * kGUnits + v;
+        c = (int)(i / kcu);
+        const int64_t r = i - (int64_t)c * kcu;
+        owner = (int)((r % x.world + x.rank) % x.world);
+        u = c < x.lay.nchunks ? (int64_t)c * x.lay.cu + r / x.world : ups;
+    };
     __shared__ int s_go;
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < 32) {
         int go = 1;
-        uint32_t fv;
-        if (u < ups && !spin_cflag(x, ep, cflag(x, x.rank, c, owner), fv)) {
-            go = 0;
-            status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+        if ((int)threadIdx.x < kGUnits) {
+            int owner, c;
+            int64_t u;
+            unit_of(threadIdx.x, owner, u, c);
+            uint32_t fv;
+            if (u < ups && !spin_cflag(x, ep, cflag(x, x.rank, c, owner), fv)) {
+                go = 0;
+                status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+            }
         }
-        s_go = go;
+        go = __all_sync(0xffffffffu, go);
+        if (threadIdx.x == 0) s_go = go;
     }
     __syncthreads();
-    if (!s_go || u >= ups) return;
-    const int64_t gi = u * kThreads + threadIdx.x;
-    if (gi >= gsh) return;
-    const uint4 v = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner, gi));
-    __stcs(reinterpret_cast<uint4*>(a.rout + (((int64_t)owner * gsh + gi) << 3)), v);
+    if (!s_go) return;
+    uint4 v[kGUnits];
+    int64_t dst[kGUnits];
+#pragma unroll
+    for (int q = 0; q < kGUnits; ++q) {
+        int owner, c;
+        int64_t u;
+        unit_of(q, owner, u, c);
+        const int64_t gi = u * kThreads + threadIdx.x;
+        dst[q] = (u < ups && gi < gsh) ? (((int64_t)owner * gsh + gi) << 3) : -1;
+        if (dst[q] >= 0) v[q] = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner, gi));
+    }
+#pragma unroll
+    for (int q = 0; q < kGUnits; ++q)
+        if (dst[q] >= 0) __stcs(reinterpret_cast<uint4*>(a.rout + dst[q]), v[q]);
 }
 
 // lmsgd_exchange, world == 1: the step's public status record (R = h, no second
@@ -1276,7 +1301,7 @@ cudaError_t launch_xstep(cudaStream_t s, const Launch& L, const XStep& a, const 
     const bool pdl = (L.pdl_mask & 4) == 0;   // bit 4 (diagnostics): launch k_xupdate after k_xstep1 completes
     const bool localr = !sim && a.x.nv == 2;   // NVLS all-reduce in place: R is in the own wire
     if (a.rout) {   // lmsgd_exchange: the all-gather into the caller's buffer instead of the update
-        const int grid = (int)((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu) * nsim;
+        const int grid = (int)(((int64_t)a.x.lay.nchunks * a.x.world * a.x.lay.cu + kGUnits - 1) / kGUnits) * nsim;
         e = sim      ? launch_pdl_if(pdl, k_xgather<true, false>, grid, kThreads, s, a, sm)
             : localr ? launch_pdl_if(pdl, k_xgather<false, true>, grid, kThreads, s, a, sm)
                      : launch_pdl_if(pdl, k_xgather<false, false>, grid, kThreads, s, a, sm);
