@@ -981,7 +981,6 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
     if (G.b() == 0 && threadIdx.x == 0) stamp(x, TR_UPD_GO);
     if (!go || s_range) return;
     const UpdConst c = s_c;
-#pragma unroll
     // every unit's R (a peer load for remote owners) issued before the first update
     // (LMSGD_XUPD_PREFETCH; 0 = load each unit's R right before its update)
 #ifndef LMSGD_XUPD_PREFETCH

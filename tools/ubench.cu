@@ -219,6 +219,48 @@ __global__ void __launch_bounds__(kThreads) k_update_rev(const uint16_t* __restr
     const int64_t v = ((int64_t)gridDim.x - 1 - blockIdx.x) * blockDim.x + threadIdx.x;
     if (v < ((n + 7) >> 3)) update8<true, false>(*reinterpret_cast<const uint4*>(R + (v << 3)), v << 3, n, c, th, d, m);
 }
+
+// ---- out-of-place fused step variants (k_fused1_oop, the N = 1 headline)
+template <int PF>   // 0: ld.global.cs.v8 (prod); 1: + .L2::256B prefetch size
+__device__ __forceinline__ void ld8_pf(const float* p, float v[8]) {
+    if constexpr (PF == 1) {
+        asm volatile("ld.global.cs.L2::256B.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                     : "=f"(v[0]), "=f"(v[1]), "=f"(v[2]), "=f"(v[3]), "=f"(v[4]), "=f"(v[5]), "=f"(v[6]), "=f"(v[7])
+                     : "l"(p));
+    } else {
+        ld8cs<true>(p, v);
+    }
+}
+// G groups of 8 elements per thread (all loads first), block size BS
+template <int G, int BS, int PF>
+__global__ void __launch_bounds__(BS) k_oop_var(const float* __restrict__ g, int64_t n, float s, UpdConst c,
+                                                const float* __restrict__ thi, const float* __restrict__ di,
+                                                const float* __restrict__ mi, float* __restrict__ tho,
+                                                float* __restrict__ dout, float* __restrict__ mo, int64_t* st) {
+    int64_t first = kNone;
+    unsigned sat = 0;
+    const int64_t v0 = ((int64_t)blockIdx.x * BS * G) + threadIdx.x;
+    float x[G][8], tv[G][8], dv[G][8], mv[G][8];
+    int64_t j0[G];
+    bool full[G];
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+        j0[q] = (v0 + q * BS) << 3;
+        full[q] = j0[q] + 8 <= n;
+        if (full[q]) { ld8_pf<PF>(g + j0[q], x[q]); ld8_pf<PF>(thi + j0[q], tv[q]); ld8_pf<PF>(di + j0[q], dv[q]); ld8_pf<PF>(mi + j0[q], mv[q]); }
+    }
+#pragma unroll
+    for (int q = 0; q < G; ++q) {
+        if (j0[q] >= n) continue;
+        if (!full[q]) { load8_g(g, j0[q], n, x[q]); update8_oop<true, false>(pack8(x[q], s, j0[q], first, sat), j0[q], n, c, thi, di, mi, tho, dout, mo); continue; }
+        const uint4 r = pack8(x[q], s, j0[q], first, sat);
+        const uint32_t w[4] = {r.x, r.y, r.z, r.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i) upd1<true>(h2f(w[i >> 1], i & 1) * c.inv_ks, tv[q][i], dv[q][i], mv[q][i], c);
+        st8cs<true>(tho + j0[q], tv[q]); st8cs<true>(dout + j0[q], dv[q]); st8cs<true>(mo + j0[q], mv[q]);
+    }
+    flush_status(first, sat, st, ST_PACK_SAT);
+}
 }  // namespace
 }  // namespace lmsgd
 
@@ -302,7 +344,7 @@ int main(int argc, char** argv) {
     struct V { const char* name; std::function<void()> f; };
     const int gridc = L.grid_cap_stream;
     std::vector<V> vs = {
-        {"V0 update (prod)", [&] { k_update<true, false, true><<<gridc, kThreads>>>(h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); }},
+        {"V0 update (prod)", [&] { k_update<true, false, true, true><<<gridc, kThreads>>>(h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); }},
         {"V1 update unroll2", [&] { k_update_u2<true><<<gridc, kThreads>>>(h, n, c, th, d, m); }},
         {"V2 update flat", [&] { k_update_flat<true><<<(int)(((n >> 3) + kThreads - 1) / kThreads), kThreads>>>(h, n, c, th, d, m); }},
         {"V7 update flat bs512", [&] { k_update_flat_bs<512><<<(int)(((n >> 3) + 511) / 512), 512>>>(h, n, c, th, d, m); }},
@@ -347,6 +389,32 @@ int main(int argc, char** argv) {
         t = time_it(iters, v.f);
         CKE(cudaGetLastError());
         printf("%-30s %8.2f us  %7.1f GB/s  bitexact=%d\n", v.name, t, fused_bytes / t / 1e3, ok);
+    }
+    // out-of-place fused variants vs the production k_fused1_oop (V8)
+    {
+        float *t2, *d2, *m2;
+        int64_t* last;   // the public status record k_repair1 writes
+        CKE(cudaMalloc(&t2, n * 4)); CKE(cudaMalloc(&d2, n * 4)); CKE(cudaMalloc(&m2, n * 4));
+        CKE(cudaMalloc(&last, 64));
+        const double oop_bytes = 28.0 * n;
+        const int64_t nv8 = (n + 7) >> 3;
+        auto prod = [&] { launch_step_oop1(0, L, g, n, 1024.f, c, th, d, m, t2, d2, m2, st, nullptr, last, nullptr); };
+        std::vector<V> os = {
+            {"O0 oop (prod, v8)", prod},
+            {"O1 oop v8 G1 BS256", [&] { k_oop_var<1, 256, 0><<<(int)((nv8 + 255) / 256), 256>>>(g, n, 1024.f, c, th, d, m, t2, d2, m2, st); }},
+            {"O2 oop v8 G1 BS512", [&] { k_oop_var<1, 512, 0><<<(int)((nv8 + 511) / 512), 512>>>(g, n, 1024.f, c, th, d, m, t2, d2, m2, st); }},
+            {"O3 oop v8 G2 BS256", [&] { k_oop_var<2, 256, 0><<<(int)((nv8 + 511) / 512), 256>>>(g, n, 1024.f, c, th, d, m, t2, d2, m2, st); }},
+            {"O4 oop v8 G1 BS256 L2::256B", [&] { k_oop_var<1, 256, 1><<<(int)((nv8 + 255) / 256), 256>>>(g, n, 1024.f, c, th, d, m, t2, d2, m2, st); }},
+            {"O5 oop v8 G2 BS256 L2::256B", [&] { k_oop_var<2, 256, 1><<<(int)((nv8 + 511) / 512), 256>>>(g, n, 1024.f, c, th, d, m, t2, d2, m2, st); }},
+            {"O6 oop v8 G1 BS128", [&] { k_oop_var<1, 128, 0><<<(int)((nv8 + 127) / 128), 128>>>(g, n, 1024.f, c, th, d, m, t2, d2, m2, st); }},
+        };
+        for (auto& v : os) {
+            reset(); v.f(); CKE(cudaGetLastError());
+            t = time_it(iters, v.f);
+            CKE(cudaGetLastError());
+            printf("%-30s %8.2f us  %7.1f GB/s(28B/e)\n", v.name, t, oop_bytes / t / 1e3);
+        }
+        cudaFree(t2); cudaFree(d2); cudaFree(m2); cudaFree(last);
     }
     // guarded pair: pack + update, and the L2-resident variant
     reset(); launch_pack(0, L, g, n, n_pad, 1024.f, h, st, Dev1{}); launch_update(0, L, h, n, c, th, d, m, st, nullptr, nullptr, Dev1{}); snapshot(rt, rd, rm);
