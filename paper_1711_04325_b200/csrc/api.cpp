@@ -827,6 +827,7 @@ lmsgd_status lmsgd_step(lmsgd_ctx* c, void* stream, float* params, const float* 
     const lmsgd::XArgs x = xargs(c, epoch, &c->dstate->xepoch);
     lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, nullptr, 0, nullptr};
     a.v8 = 1;   // 256-bit accesses if params / delta / m are 32-byte aligned (launch_xstep checks)
+    a.riu = 1;  // own-shard reduce inside the update (kernels.cu riu_active)
     CK(c, timed(c, s, 2, [&] { return lmsgd::launch_xstep(s, xlaunch(c), a); }));
     return LMSGD_OK;
 }
@@ -992,6 +993,7 @@ lmsgd_status lmsgd_step_graph(lmsgd_ctx* c, void* stream, float* params, const f
     lmsgd::XStep a{x, grads, c->scale, u, params, delta, m, c->last, c->xctr, c->d_ctab, c->ctab_count,
                    &c->dstate->cursor};
     a.v8 = 1;
+    a.riu = 1;
     CK(c, lmsgd::launch_xstep(s, xlaunch(c), a));
     return LMSGD_OK;
 }
@@ -1200,6 +1202,7 @@ lmsgd_status lmsgd_step_group(lmsgd_ctx* const* ctxs, int count, void* stream, f
         c->mode = 1;
         v[i] = lmsgd::XStep{xargs(c, epoch, &c->dstate->xepoch), grads[i], c->scale, u, params[i], delta[i], m[i],
                             c->last, c->xctr, nullptr, 0, nullptr, nullptr};
+        v[i].riu = 1;
     }
     set_group_v8(v);
     if ((st = group_upload(lead, s, &lead->d_group, v)) != LMSGD_OK) return st;
@@ -1263,6 +1266,7 @@ lmsgd_status lmsgd_step_graph_group(lmsgd_ctx* const* ctxs, int count, void* str
         if (x.trace) { x.trace = nullptr; --c->trace_steps; }
         v[i] = lmsgd::XStep{x, grads[i], c->scale, u, params[i], delta[i], m[i], c->last, c->xctr, c->d_ctab,
                             c->ctab_count, &c->dstate->cursor, nullptr};
+        v[i].riu = 1;
     }
     set_group_v8(v);
     // the arguments do not change between graph-mode calls (everything per-step is read

@@ -286,6 +286,13 @@ __device__ __forceinline__ void reduce8(const uint16_t* __restrict__ slots, int6
                                                   o[4] | (uint32_t)o[5] << 16, o[6] | (uint32_t)o[7] << 16);
 }
 
+// reduce8, also returning the 8 reduced values (the update consumes them directly)
+__device__ __forceinline__ uint4 reduce8_val(const uint16_t* __restrict__ slots, int64_t stride, int k, int64_t j0,
+                                             uint16_t* __restrict__ R, unsigned& sat) {
+    reduce8(slots, stride, k, j0, R, sat);
+    return *reinterpret_cast<const uint4*>(R + j0);   // this thread's own store
+}
+
 __device__ __forceinline__ int64_t gtid() { return (int64_t)blockIdx.x * blockDim.x + threadIdx.x; }
 __device__ __forceinline__ int64_t gstride() { return (int64_t)gridDim.x * blockDim.x; }
 
@@ -719,6 +726,22 @@ static_assert(LMSGD_XPHASES == 1 || LMSGD_XPHASES == 2, "phase flags: A (phase 0
 #ifndef LMSGD_XSTEP_BPS_DEFAULT
 #define LMSGD_XSTEP_BPS_DEFAULT (LMSGD_XPHASES > 1 ? 2 : 8)
 #endif
+// LMSGD_REDUCE_IN_UPDATE (A/B knob, off): in a step (not lmsgd_exchange) on the peer path
+// with one phase, k_xstep1 ends after the skip decision and every rank reduces its own
+// shard's units inside k_xupdate (own units first in each chunk, released per block),
+// so the update does not wait for a separate reduce pass and its hand-over.  Parity green
+// at world 2-8 (emulated and real), but 405.7 vs 202.6 us per step at k = 4 and 332.9 vs
+// 180.8 us at k = 2 (profiles/r2/ab/reduce_in_update.txt): the blocks waiting for other
+// owners' chunks hold the SMs while only 1/k of the blocks produce R, each behind a system
+// fence.  Both kernels decide it the same way.
+#ifndef LMSGD_REDUCE_IN_UPDATE
+#define LMSGD_REDUCE_IN_UPDATE 0
+#endif
+__device__ __forceinline__ bool riu_active(const XStep& a) {
+    const int nph = a.x.lay.nchunks >= LMSGD_XPHASES ? LMSGD_XPHASES : 1;
+    return LMSGD_REDUCE_IN_UPDATE && a.riu && a.x.nv == 0 && nph == 1;
+}
+
 template <bool SIM, int NV>
 __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
     static_assert(!(SIM && NV), "NVLS needs one GPU per rank");
@@ -856,6 +879,10 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
             if (t0) atomicAdd(a.ctr + 1, 1u);
             return;
         }
+        if (riu_active(a)) {   // the reduce happens in k_xupdate
+            if (G.b() == 0 && t0) stamp(x, TR_RED_GO);
+            break;
+        }
 
         // ---- 3. exact reduce of this phase's units of the own shard (unit u on block
         //         u % grid); a chunk is released when the last block holding one of its
@@ -941,35 +968,127 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
     const int64_t gsh = x.lay.shard >> 3;
     const int64_t ups = (gsh + kThreads - 1) / kThreads;
     const int64_t kcu = (int64_t)x.world * x.lay.cu;
-    auto unit_of = [&](int v, int& owner, int64_t& u, int& c) {   // chunk-major, owner-interleaved
+    // chunk-major; inside a chunk owner-major starting with this rank's own units, so that
+    // the blocks reducing own units (reduce in the update) come before the blocks of the
+    // same chunk that wait for other owners -- also when an emulated group interleaves
+    // every rank's blocks in one grid.  (A resident window of ~900 blocks spans dozens of
+    // 32-unit owner segments, so every owner's links still see traffic at once.)
+    auto unit_of = [&](int v, int& owner, int64_t& u, int& c) {
         const int64_t i = G.b() * kXUnits + v;
         c = (int)(i / kcu);
         const int64_t r = i - (int64_t)c * kcu;
-        owner = (int)((r % x.world + x.rank) % x.world);
-        u = c < x.lay.nchunks ? (int64_t)c * x.lay.cu + r / x.world : ups;   // ups: past the last unit
+        owner = (int)((r / x.lay.cu + x.rank) % x.world);
+        u = c < x.lay.nchunks ? (int64_t)c * x.lay.cu + r % x.lay.cu : ups;   // ups: past the last unit
     };
     int owner[kXUnits];
     int64_t us[kXUnits];
     int cch[kXUnits];
 #pragma unroll
     for (int v = 0; v < kXUnits; ++v) unit_of(v, owner[v], us[v], cch[v]);
-    // lane 0 of warp v waits for unit v's chunk flag (the waits overlap), even when the
-    // step is skipped: the step may end only after every owner's reduce has finished
-    // reading its receive slots.  The chunk flag carries the skip decision (spin_cflag).
+    // Reduce in the update (riu_active: the step at world > 1 on the peer path): a unit of
+    // this rank's own shard is reduced here, from the receive slots every rank pushed
+    // before its flag A (warp v acquires all of them, then flag D for the decision), and
+    // its R is released to the other ranks per chunk as k_xstep1's reduce does otherwise.
+    // Own units are reduced, updated and released BEFORE the block waits for any other
+    // owner's chunk: otherwise two ranks' blocks could each hold an own unit while waiting
+    // for the other's.
     const int w = threadIdx.x >> 5;
-    if ((threadIdx.x & 31) == 0 && w < kXUnits) {
-        if (G.b() == 0 && w == 0) stamp(x, TR_UPD_START);
-        int ow, c;
+    const bool riu = riu_active(a);
+    bool own[kXUnits];
+    bool any_own = false;
+#pragma unroll
+    for (int v = 0; v < kXUnits; ++v) {
+        own[v] = riu && owner[v] == x.rank && us[v] < ups;
+        any_own = any_own || own[v];
+    }
+    __shared__ int s_skip;
+    if (threadIdx.x == 0) {
+        s_skip = 0;
+        if (G.b() == 0) stamp(x, TR_UPD_START);
+    }
+#pragma unroll
+    for (int v = 0; v < kXUnits; ++v) s_ok[v] = 1;   // (written by thread 0 of each warp below)
+    __syncthreads();
+    const UpdConst c = s_c;
+    uint4 rv[kXUnits];
+    int64_t j0v[kXUnits];
+#pragma unroll
+    for (int v = 0; v < kXUnits; ++v) {
+        const int64_t gi = us[v] * kThreads + threadIdx.x;
+        j0v[v] = (us[v] < ups && gi < gsh) ? ((int64_t)owner[v] * gsh + gi) << 3 : x.n;
+    }
+    if (any_own) {
+        // ---- own units: every rank's push is in (flag A), the decision is stored (flag D)
+        if (w < kXUnits && own[w]) {
+            int ok = warp_wait_all(x, ep, FLAG_A) ? 1 : 0;
+            if ((threadIdx.x & 31) == 0) {
+                if (ok && !spin_flag(x, ep, flag_slot(x, x.rank, FLAG_D))) {
+                    ok = 0;
+                    status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
+                }
+                if (ok) {
+                    const volatile int64_t* vm = status_of(x, ep, x.rank);
+                    if (vm[ST_G_FIRST] != kNone || vm[ST_G_ERROR] != 0) s_skip = 1;
+                }
+                s_ok[w] = ok;
+            }
+        }
+        __syncthreads();
+        int go = 1;
+#pragma unroll
+        for (int v = 0; v < kXUnits; ++v) go &= s_ok[v];
+        if (!go) return;   // timeout: recorded; the peers time out on this rank's chunks too
+        const bool skip = s_skip || s_range;
+        unsigned sat = 0;
+        if (!skip) {
+#pragma unroll
+            for (int v = 0; v < kXUnits; ++v) {
+                if (!own[v] || j0v[v] >= x.n) continue;
+                const int64_t gi = us[v] * kThreads + threadIdx.x;
+                rv[v] = reduce8_val(reinterpret_cast<const uint16_t*>(x.peers.base[x.rank] + x.lay.off_recv),
+                                    x.lay.shard, x.world, gi << 3,
+                                    reinterpret_cast<uint16_t*>(x.peers.base[x.rank] + x.lay.off_R), sat);
+                update8<RMS, WD, KM, V8>(rv[v], j0v[v], x.n, c, a.th, a.d, a.m);
+            }
+        }
+        // (padding groups of the last unit -- gi >= gsh -- hold no data: nothing to reduce)
+        flush_status(kNone, sat, status_of(x, ep, x.rank), ST_SUM_SAT);
+        __syncthreads();
+        if (threadIdx.x == 0) {   // release: one fence after bar.sync, then the chunk tickets
+            __threadfence_system();
+#pragma unroll
+            for (int v = 0; v < kXUnits; ++v) {
+                if (!own[v]) continue;
+                const int64_t rem = ups - (int64_t)cch[v] * x.lay.cu;
+                const unsigned cnt = (unsigned)(rem < x.lay.cu ? rem : x.lay.cu);
+                if (atomicAdd(a.ctr + 4 + cch[v], 1u) + 1u == cnt) {
+                    a.ctr[4 + cch[v]] = 0;
+                    __threadfence_system();   // the observed tickets' R writes before the flags
+                    const uint32_t fv = cflag_value(x, ep);
+                    for (int p = 0; p < x.world; ++p) st_relaxed_sys(cflag(x, p, cch[v], x.rank), fv);
+                }
+            }
+        }
+    }
+    // ---- other owners' units: lane 0 of warp v waits for unit v's chunk flag (the waits
+    //      overlap), even when the step is skipped: the step may end only after every
+    //      owner has finished reading its receive slots.  The flag carries the decision.
+    bool any_remote = false;
+#pragma unroll
+    for (int v = 0; v < kXUnits; ++v) any_remote = any_remote || (!own[v] && us[v] < ups);
+    if (!any_remote) return;
+    if ((threadIdx.x & 31) == 0 && w < kXUnits && !own[w]) {
+        int ow, cc;
         int64_t u;
-        unit_of(w, ow, u, c);
+        unit_of(w, ow, u, cc);
         int ok = 1;
         if (u < ups) {
             uint32_t fv;
-            if (!spin_cflag(x, ep, cflag(x, x.rank, c, ow), fv)) {
+            if (!spin_cflag(x, ep, cflag(x, x.rank, cc, ow), fv)) {
                 ok = 0;
                 status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
             } else if (fv & 1u) {
-                ok = 0;   // skipped step
+                s_skip = 1;   // skipped step
             }
         }
         s_ok[w] = ok;
@@ -979,24 +1098,19 @@ __global__ void LMSGD_LB(LMSGD_XUPD_MINB) k_xupdate(XStep a_, Sim sim) {
 #pragma unroll
     for (int v = 0; v < kXUnits; ++v) go &= s_ok[v];
     if (G.b() == 0 && threadIdx.x == 0) stamp(x, TR_UPD_GO);
-    if (!go || s_range) return;
-    const UpdConst c = s_c;
-    // every unit's R (a peer load for remote owners) issued before the first update
+    if (!go || s_skip || s_range) return;
+    // every remote unit's R (a peer load) issued before the first update
     // (LMSGD_XUPD_PREFETCH; 0 = load each unit's R right before its update)
 #ifndef LMSGD_XUPD_PREFETCH
 #define LMSGD_XUPD_PREFETCH 1
 #endif
-    uint4 rv[kXUnits];
-    int64_t j0v[kXUnits];
+#pragma unroll
+    for (int v = 0; v < kXUnits; ++v)
+        if (LMSGD_XUPD_PREFETCH && !own[v] && j0v[v] < x.n)
+            rv[v] = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner[v], us[v] * kThreads + threadIdx.x));
 #pragma unroll
     for (int v = 0; v < kXUnits; ++v) {
-        const int64_t gi = us[v] * kThreads + threadIdx.x;
-        j0v[v] = (us[v] < ups && gi < gsh) ? ((int64_t)owner[v] * gsh + gi) << 3 : x.n;
-        if (LMSGD_XUPD_PREFETCH && j0v[v] < x.n) rv[v] = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner[v], gi));
-    }
-#pragma unroll
-    for (int v = 0; v < kXUnits; ++v) {
-        if (j0v[v] >= x.n) continue;
+        if (own[v] || j0v[v] >= x.n) continue;
         if (!LMSGD_XUPD_PREFETCH)
             rv[v] = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner[v], us[v] * kThreads + threadIdx.x));
         update8<RMS, WD, KM, V8>(rv[v], j0v[v], x.n, c, a.th, a.d, a.m);

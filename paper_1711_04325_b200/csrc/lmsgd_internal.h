@@ -138,6 +138,8 @@ struct XStep {
                              // replaces k_xupdate); NULL for a step
     int32_t v8;              // 1: the update may use 256-bit accesses if th/d/m are 32-byte aligned
                              // (an emulated group sets it only if every rank's are)
+    int32_t riu;             // 1: a step whose own-shard units are reduced inside k_xupdate
+                             // (kernels.cu riu_active: peer path, one phase); 0 for lmsgd_exchange
 };
 // d_group / nsim: emulated-group mode (lmsgd_*_group): device array of the nsim ranks'
 // XStep, every rank's blocks in one launch per kernel; NULL for a real (one-rank) launch
