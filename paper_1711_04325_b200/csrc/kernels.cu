@@ -1,8 +1,9 @@
 // sm_100a kernels of the gradient exchange + blended update (arXiv 1711.04325).
 //
 // Everything here is HBM- or NVLink-bound streaming work:
-// there is no dense contraction, so no tensor cores.  The kernels move 16-byte
-// vectors (8 elements per thread per trip), use evict-first streaming hints for
+// there is no dense contraction, so no tensor cores.  The kernels move 8 elements per
+// thread per trip (one 256-bit access per fp32 row where the buffers are 32-byte aligned,
+// else two 128-bit ones; 16-byte fp16 wire vectors), use evict-first streaming hints for
 // data touched once (g, theta, Delta, m), and keep the fp16 wire buffers on the
 // default policy so a consumer launched right after the producer hits L2.
 //
@@ -627,14 +628,10 @@ __device__ bool warp_wait_all(const XArgs& x, const Ep& ep, int which, bool trac
 }
 
 // Work units of the exchange kernels: a unit is kThreads consecutive 8-element groups
-// of one shard.  Units are interleaved over owners -- unit u belongs to owner
-// (u + rank) % world -- so that the blocks in flight on every rank touch all owners
-// evenly (no owner's links are a hot spot) and local and remote traffic mix.
-__device__ __forceinline__ bool map_unit(const XArgs& x, int64_t u, int& owner, int64_t& gi) {
-    owner = (int)((u % x.world + x.rank) % x.world);
-    gi = (u / x.world) * kThreads + threadIdx.x;   // group index inside the owner's shard
-    return gi < (x.lay.shard >> 3);
-}
+// (2048 elements) of one shard.  k_xstep1's push sweeps them owner-interleaved -- unit u
+// belongs to owner (u + rank) % world -- so that the blocks in flight on every rank touch
+// all owners evenly (no owner's links are a hot spot); the update and gather kernels take
+// them chunk-major (see k_xupdate).
 
 // ------------------------------------------------------------------ world > 1, one kernel
 
@@ -695,8 +692,9 @@ __device__ __forceinline__ uint32_t cflag_value(const XArgs& x, const Ep& ep) {
 //      its units are reduced and fenced.
 // k_xupdate -- flat grid, launched with programmatic dependent launch so its blocks
 // take SMs as soon as k_xstep1's blocks retire: kXUnits units per block, chunk-major
-// and owner-interleaved; a block waits only for its units' chunk flags (which carry
-// the skip decision), so the update of early chunks overlaps the reduce of later ones.
+// and owner-major inside a chunk; a block waits only for its units' chunk flags (which
+// carry the skip decision), so the update of early chunks overlaps the reduce of later
+// ones; R is pulled from the owner inside the update (the all-gather).
 // k_xfinalize -- one warp: the step's public status record.
 // Chunk counters in a.ctr are reset by the block that completes them.
 #ifndef LMSGD_XSTEP_MINB
