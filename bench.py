@@ -658,6 +658,9 @@ def main():
         L.lmsgd_trace_enable(ctx, 0)
         xsegs = {"pack_push": ("pack_start", "pack_end"), "wait_all_pushes": ("pack_end", "reduce_start"),
                  "reduce": ("reduce_go", "reduce_end"), "gather_after_reduce": ("reduce_end", "update_end"),
+                 "gather_block0_start": ("reduce_end", "update_start"),
+                 "gather_block0_first_chunk": ("update_start", "update_go"),
+                 "gather_from_first_chunk": ("update_go", "update_end"),
                  "exchange": ("pack_start", "update_end")}
         mine_x = {k_: statistics.median((t[b] - t[a]) / 1e3 for t in tr[10:]) for k_, (a, b) in xsegs.items()}
         allx = [None] * world

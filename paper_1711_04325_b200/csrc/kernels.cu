@@ -1150,6 +1150,7 @@ __global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
         u = c < x.lay.nchunks ? (int64_t)c * x.lay.cu + r / x.world : ups;
     };
     __shared__ int s_go;
+    if (threadIdx.x == 0 && Grid<SIM>{sim}.b() == 0) stamp(x, TR_UPD_START);
     if (threadIdx.x < 32) {
         int go = 1;
         if ((int)threadIdx.x < kGUnits) {
@@ -1164,6 +1165,7 @@ __global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
         }
         go = __all_sync(0xffffffffu, go);
         if (threadIdx.x == 0) s_go = go;
+        if (threadIdx.x == 0 && Grid<SIM>{sim}.b() == 0) stamp(x, TR_UPD_GO);
     }
     __syncthreads();
     if (!s_go) return;
