@@ -27,6 +27,9 @@ namespace lmsgd {
 namespace {
 
 constexpr int kThreads = 256;   // LMSGD_LB below spells the same block size
+#ifndef LMSGD_XGATHER_OWN_IN_REDUCE
+#define LMSGD_XGATHER_OWN_IN_REDUCE 0   // A/B knob: lmsgd_exchange with the own shard of R_out written by the reduce (profiles/r2/ab/exchange_own_shard.txt: no gain)
+#endif
 #ifndef LMSGD_XUNITS
 #define LMSGD_XUNITS 2   // A/B at k = 4 (profiles/r1/ab/xunits_n4.txt): 201.9 vs 206.8 us per step with 1
 #endif
@@ -911,6 +914,15 @@ __global__ void LMSGD_LB(LMSGD_XSTEP_MINB) k_xstep1(XStep a_, Sim sim) {
                     else *reinterpret_cast<uint4*>(R + (off[i] / 2 - (int64_t)x.rank * x.lay.shard)) = v[i];
                 }
             }
+        } else if (LMSGD_XGATHER_OWN_IN_REDUCE && a.rout) {
+            // lmsgd_exchange: the own shard of the caller's output is written here, so the
+            // all-gather (k_xgather) only pulls the other owners' shards
+            for (int64_t su = lo + G.b(); su < hi; su += G.g()) {
+                const int64_t gi = su * kThreads + threadIdx.x;
+                if (gi < gsh)
+                    __stcs(reinterpret_cast<uint4*>(a.rout + (int64_t)x.rank * x.lay.shard + (gi << 3)),
+                           reduce8_val(recv, x.lay.shard, x.world, gi << 3, R, sat));
+            }
         } else {
             for (int64_t su = lo + G.b(); su < hi; su += G.g()) {
                 const int64_t gi = su * kThreads + threadIdx.x;
@@ -1149,6 +1161,8 @@ __global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
         owner = (int)((r % x.world + x.rank) % x.world);
         u = c < x.lay.nchunks ? (int64_t)c * x.lay.cu + r / x.world : ups;
     };
+    // the own shard was written by k_xstep1's reduce (peer path)
+    auto own_done = [&](int owner) { return LMSGD_XGATHER_OWN_IN_REDUCE && x.nv == 0 && owner == x.rank; };
     __shared__ int s_go;
     if (threadIdx.x == 0 && Grid<SIM>{sim}.b() == 0) stamp(x, TR_UPD_START);
     if (threadIdx.x < 32) {
@@ -1158,7 +1172,7 @@ __global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
             int64_t u;
             unit_of(threadIdx.x, owner, u, c);
             uint32_t fv;
-            if (u < ups && !spin_cflag(x, ep, cflag(x, x.rank, c, owner), fv)) {
+            if (u < ups && !own_done(owner) && !spin_cflag(x, ep, cflag(x, x.rank, c, owner), fv)) {
                 go = 0;
                 status_of(x, ep, x.rank)[ST_G_ERROR] = (int64_t)LMSGD_ERR_TIMEOUT;
             }
@@ -1177,7 +1191,7 @@ __global__ void __launch_bounds__(kThreads) k_xgather(XStep a_, Sim sim) {
         int64_t u;
         unit_of(q, owner, u, c);
         const int64_t gi = u * kThreads + threadIdx.x;
-        dst[q] = (u < ups && gi < gsh) ? (((int64_t)owner * gsh + gi) << 3) : -1;
+        dst[q] = (u < ups && gi < gsh && !own_done(owner)) ? (((int64_t)owner * gsh + gi) << 3) : -1;
         if (dst[q] >= 0) v[q] = *reinterpret_cast<const uint4*>(r_src(x, LOCALR, owner, gi));
     }
 #pragma unroll
