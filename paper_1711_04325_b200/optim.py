@@ -159,6 +159,24 @@ class LMSGD:
         L.lmsgd_finalize(self.ctx)
 
 
+def bucket_bounds(n: int, world: int, bucket_elems: int) -> list[tuple[int, int]]:
+    """[lo, hi) flat ranges of the buckets, from the END of the buffer (the last layers'
+    gradients are complete first): every boundary but n is a multiple of 64 * world, so
+    each bucket's exchange output (n_pad = its size rounded up to 64 * world) is a
+    contiguous slice of one R buffer; buckets hold about bucket_elems elements."""
+    if n < 1 or world < 1 or bucket_elems < 1:
+        raise ValueError("bucket_bounds: n, world and bucket_elems must be positive")
+    unit = 64 * world
+    bounds, hi = [], n
+    while hi > 0:
+        lo = max(0, (hi - bucket_elems) // unit * unit)
+        if lo == hi:
+            lo = max(0, hi - unit)
+        bounds.append((lo, hi))
+        hi = lo
+    return bounds
+
+
 class BucketedLMSGD(LMSGD):
     """``LMSGD`` with the exchange split into buckets of the flat gradient and overlapped
     with backward (the communication/iteration overlap of
@@ -195,14 +213,7 @@ class BucketedLMSGD(LMSGD):
 
     def _init_exchange(self, flags, weight_decay):
         dev = self.flat_g.device
-        unit = 64 * self.world
-        bounds, hi = [], self.n
-        while hi > 0:   # from the end of the buffer: the last layers' gradients come first
-            lo = max(0, (hi - self.bucket_elems) // unit * unit)
-            if lo == hi:
-                lo = max(0, hi - unit)
-            bounds.append((lo, hi))
-            hi = lo
+        bounds = bucket_bounds(self.n, self.world, self.bucket_elems)
         self.buckets = []
         top_pad = 0
         for lo, hi in bounds:

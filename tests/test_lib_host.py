@@ -153,3 +153,23 @@ def test_no_undefined_library_symbols():
     out = subprocess.run(["nm", "-D", "--undefined-only", L.LIB_PATH], capture_output=True, text=True).stdout
     bad = [ln for ln in out.splitlines() if " U " in ln and "@" not in ln]   # weak (w) refs are fine
     assert not bad, bad
+
+
+@pytest.mark.parametrize("n,world,b", [(1, 1, 1), (1000, 2, 64), (23_314, 1, 1000), (25_557_032, 4, 1 << 22),
+                                       (25_557_032, 8, 2 << 20), (100, 8, 1 << 30), (513, 8, 512)])
+def test_bucket_bounds_tile_the_buffer(n, world, b):
+    """BucketedLMSGD's partition (host logic): the buckets tile [0, n) from its end, every
+    boundary except n is a multiple of 64 * world (so the buckets' padded exchange outputs
+    are disjoint slices of one R buffer), and no bucket is far from the requested size."""
+    from paper_1711_04325_b200.optim import bucket_bounds
+    bk = bucket_bounds(n, world, b)
+    assert bk[0][1] == n and bk[-1][0] == 0
+    assert all(a[0] == c[1] for a, c in zip(bk, bk[1:]))          # contiguous, descending
+    assert all(lo % (64 * world) == 0 for lo, _ in bk)
+    assert all(hi % (64 * world) == 0 for _, hi in bk[1:])
+    unit = 64 * world
+    for lo, hi in bk[:-1]:
+        assert hi - lo >= min(b, n), (lo, hi)
+        assert hi - lo < max(b, unit) + unit, (lo, hi)
+    _, n_pad_top = L.lmsgd_layout(world, bk[0][1] - bk[0][0])
+    assert bk[0][0] + n_pad_top >= n
