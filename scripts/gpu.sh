@@ -24,7 +24,7 @@ run() {   # run NAME TIMEOUT CMD...
 tr() { echo python -m torch.distributed.run --nnodes=1 --nproc-per-node "$1" --master-addr 127.0.0.1 --master-port "$2"; }
 for task in "$@"; do
   case $task in
-    tests) run pytest_gpu 1500 python -m pytest ${PYTEST_ARGS:-tests} -m gpu -q -rs --durations=15 ;;
+    tests) run pytest_gpu 1500 python -m pytest ${PYTEST_ARGS:-tests} -m gpu -q -rs --timeout 900 --durations=15 ;;
     smoke) run smoke 300 python -c "import __graft_entry__ as g; g.smoke()" ;;
     bench1) run bench_n1 600 python bench.py $BENCH_ARGS ;;
     benchN) for n in 2 4 8; do
