@@ -229,6 +229,7 @@ class BucketedLMSGD(LMSGD):
         self.dstatus = torch.empty(4, dtype=torch.int64, device=dev)
         self.last_status = torch.empty(4, dtype=torch.int64, device=dev)
         L.lmsgd_status_reset(self.dstatus)
+        L.lmsgd_status_reset(self.last_status)   # status() before the first step: clean
         self.comm = torch.cuda.Stream(device=dev)
         self._upd_done = torch.cuda.Event()
         self._upd_done.record(torch.cuda.current_stream(dev))
