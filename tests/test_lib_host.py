@@ -173,3 +173,18 @@ def test_bucket_bounds_tile_the_buffer(n, world, b):
         assert hi - lo < max(b, unit) + unit, (lo, hi)
     _, n_pad_top = L.lmsgd_layout(world, bk[0][1] - bk[0][0])
     assert bk[0][0] + n_pad_top >= n
+
+
+def test_nvls_entry_points_without_a_gpu():
+    """The NVLS calls are exported and fail soft on a machine without a GPU: the support
+    query answers False (no driver entry points / no device) instead of raising, and the
+    binding rejects a malformed handle before calling into the library."""
+    assert L.lmsgd_nvls_supported(0) in (False, True)
+    with pytest.raises(ValueError):
+        L.lmsgd_nvls_connect(L.Context(None, 2, 0, 0, 10), b"short")
+    # NULL context: an argument error, not a crash
+    assert L.lib().lmsgd_nvls_create(None, ctypes.create_string_buffer(64)) == L.LMSGD_ERR_INVALID_ARG
+    assert L.lib().lmsgd_nvls_bind(None, 1) == L.LMSGD_ERR_INVALID_ARG
+    assert L.lib().lmsgd_nvls_mode(None, 1) == L.LMSGD_ERR_INVALID_ARG
+    assert L.lib().lmsgd_status_accumulate(None, None, 0, None) == L.LMSGD_ERR_INVALID_ARG
+    assert L.lib().lmsgd_set_exchange_blocks(None, 4) == L.LMSGD_ERR_INVALID_ARG
